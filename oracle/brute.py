@@ -1,0 +1,73 @@
+"""O2 -- per-trace brute force in pure Python (TEST INFRASTRUCTURE ONLY).
+
+Independent of O1 (oracle.cpp): no sort of the whole table, no single loop.
+Each case is gathered into its own list of (ts, ingest index, activity) and
+sorted on its own (case, then timestamp, then absolute index), then
+every output is enumerated per trace ("enumerate consecutive pairs per
+case by brute force", S:369 hand enumeration of variants).  For tiny logs only.
+"""
+from __future__ import annotations
+
+from collections import defaultdict
+
+
+def traces(case, act, ts):
+    """{case code: [(ts, ingest index, act), ...] sorted by (ts, index)}."""
+    per = defaultdict(list)
+    for i, (c, a, t) in enumerate(zip(case, act, ts)):
+        per[int(c)].append((int(t), i, int(a)))
+    return {c: sorted(v) for c, v in per.items()}
+
+
+def analyse(case, act, ts, A: int) -> dict:
+    """All hot-path outputs as plain Python dicts/lists."""
+    tr = traces(case, act, ts)
+    cnt = defaultdict(int)
+    dsum = defaultdict(int)
+    start = defaultdict(int)
+    end = defaultdict(int)
+    cases = []
+    variants = defaultdict(int)
+    rep = {}
+    for c in sorted(tr):
+        evs = tr[c]
+        seq = tuple(a for _, _, a in evs)
+        for (t0, _, a0), (t1, _, a1) in zip(evs, evs[1:]):
+            cnt[(a0, a1)] += 1
+            dsum[(a0, a1)] += t1 - t0
+        start[seq[0]] += 1
+        end[seq[-1]] += 1
+        cases.append((c, len(evs), evs[-1][0] - evs[0][0]))
+        variants[seq] += 1
+        rep.setdefault(seq, c)
+    mean = {k: dsum[k] / cnt[k] for k in cnt}
+    return {"cnt": dict(cnt), "sum": dict(dsum), "mean": mean, "start": dict(start),
+            "end": dict(end), "cases": cases, "variants": dict(variants), "rep": rep,
+            "sorted": [(c, t, i, a) for c in sorted(tr) for (t, i, a) in tr[c]]}
+
+
+def filter_time(case, ts, t1, t2, mode):
+    """S:413 by enumeration; returns kept row indices in input order."""
+    if t1 > t2:
+        raise ValueError("t1 > t2")
+    if mode == 0:
+        return [i for i, t in enumerate(ts) if t1 <= t <= t2]
+    span = {}
+    for c, t in zip(case, ts):
+        lo, hi = span.get(int(c), (t, t))
+        span[int(c)] = (min(lo, t), max(hi, t))
+    ok = {c: (lo >= t1 and hi <= t2) if mode == 1 else (lo <= t2 and hi >= t1)
+          for c, (lo, hi) in span.items()}
+    return [i for i, c in enumerate(case) if ok[int(c)]]
+
+
+def filter_codes(case, col, codes, level, keep=True):
+    """S:448 by enumeration (u32 in-set predicate); kept row indices."""
+    codes = set(int(x) for x in codes)
+    m = [int(v) in codes for v in col]
+    if level == 0:
+        return [i for i in range(len(m)) if m[i] == keep]
+    anym = defaultdict(bool)
+    for c, x in zip(case, m):
+        anym[int(c)] |= x
+    return [i for i, c in enumerate(case) if anym[int(c)] == keep]
