@@ -1,0 +1,372 @@
+// A5-A8: the fused aggregate pass over the formatted log (K6) and the table
+// finaliser (K11).
+//
+//  A5  DFG ("calculating the frequency/performance directly-follows
+//      graph"; P:110 previous-event columns): for consecutive rows
+//      i, i+1 of one case, cnt[a_i][a_{i+1}] += 1, sum += ts_{i+1} - ts_i.  On
+//      the composite key the duration is key_{i+1} - key_i (the case bits
+//      cancel), so timestamps are never decoded.
+//  A6  start/end activities.
+//  A7  events per case and throughput time = last ts - first ts (P:101,
+//      P:112-114).
+//  A8  per-case variant key ("numerical features that uniquely identify
+//      the case's variant"): two 64-bit polynomial hashes of the
+//      (act + 1) sequence plus the length, verified exactly later (A9).
+//
+// Work split: a CTA owns tiles of 256 consecutive CASES (tile edges are case
+// edges, so no directly-follows pair straddles two CTAs).  Pairs are processed
+// event-parallel (coalesced), per-case work case-parallel.  The A x A table is
+// privatised per CTA in shared memory (u32 counts; u32 lo/hi duration sums
+// with exact carry propagation, because 64-bit shared atomics are CAS loops on
+// sm_100a) and flushed once per CTA with 64-bit global atomics.  When A x A
+// does not fit in shared memory the pass updates the L2-resident global table
+// directly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "pm4g_internal.cuh"
+
+namespace pm4g {
+
+constexpr int AGG_THREADS = 256;
+constexpr int AGG_CASES = 256;   // cases per tile
+constexpr size_t AGG_SMEM_MAX = 100 * 1024;
+
+// Variant-key hash (internal, verified): Horner polynomial mod 2^64 over act+1.
+constexpr uint64_t HB1 = 0x00000100000001B3ull;
+constexpr uint64_t HB2 = 0xC2B2AE3D27D4EB4Full;
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__device__ __forceinline__ void finish_key(uint64_t h1, uint64_t h2, uint32_t len, bool weak,
+                                           uint64_t& k1, uint64_t& k2) {
+    if (weak) {  // debug: 4-bit key, forces collisions (exercises the exact fallback)
+        k1 = 1ull | ((fmix64(h1) & 0xFull) << 1);
+        k2 = 0;
+        return;
+    }
+    k1 = fmix64(h1 ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) | 1ull;
+    k2 = fmix64(h2 + (uint64_t)len * 0xff51afd7ed558ccdull);
+}
+
+template <class P, bool SMEM>
+__global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
+    const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
+    const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A,
+    uint64_t* __restrict__ packed, uint32_t* __restrict__ n_events, int64_t* __restrict__ dur,
+    uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t AA = A * A;
+    uint32_t* s_cnt = sm;
+    uint32_t* s_lo = sm + AA;
+    uint32_t* s_hi = sm + 2 * AA;
+    uint32_t* s_st = sm + 3 * AA;
+    uint32_t* s_en = s_st + A;
+    const bool tables = packed != nullptr;
+    uint64_t* g_cnt = packed;
+    uint64_t* g_sum = packed + AA;
+    uint64_t* g_st = packed + 2 * (size_t)AA;
+    uint64_t* g_en = g_st + A;
+    if (SMEM && tables) {
+        for (uint32_t i = threadIdx.x; i < 3 * AA + 2 * A; i += AGG_THREADS) sm[i] = 0;
+        __syncthreads();
+    }
+    const uint64_t C = *d_n_cases;
+    const uint64_t tiles = (C + AGG_CASES - 1) / AGG_CASES;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t c0 = t * AGG_CASES;
+        const uint64_t c1 = min(c0 + AGG_CASES, C);
+        if (tables) {
+            const uint32_t e0 = off[c0], e1 = off[c1];
+            for (uint32_t i = e0 + threadIdx.x; i + 1 < e1; i += AGG_THREADS) {
+                uint64_t k = key[i], kn = key[i + 1];
+                if (shr64(k, ts_bits) != shr64(kn, ts_bits)) continue;
+                uint32_t e = (uint32_t)act[i] * A + (uint32_t)act[i + 1];
+                uint64_t d = kn - k;
+                if (SMEM) {
+                    atomicAdd(&s_cnt[e], 1u);
+                    uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
+                    uint32_t old = atomicAdd(&s_lo[e], lo);
+                    hi += (old + lo < old) ? 1u : 0u;   // carry out of the low word
+                    if (hi) atomicAdd(&s_hi[e], hi);
+                } else {
+                    atomicAdd((unsigned long long*)&g_cnt[e], 1ull);
+                    atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)d);
+                }
+            }
+        }
+        const uint64_t c = c0 + threadIdx.x;
+        if (c < c1) {
+            const uint32_t f = off[c], l = off[c + 1] - 1;
+            if (tables) {
+                uint32_t as = (uint32_t)act[f], ae = (uint32_t)act[l];
+                if (SMEM) {
+                    atomicAdd(&s_st[as], 1u);
+                    atomicAdd(&s_en[ae], 1u);
+                } else {
+                    atomicAdd((unsigned long long*)&g_st[as], 1ull);
+                    atomicAdd((unsigned long long*)&g_en[ae], 1ull);
+                }
+            }
+            if (n_events) n_events[c] = l - f + 1;
+            if (dur) dur[c] = (int64_t)(key[l] - key[f]);
+            if (k1o) {
+                uint64_t h1 = 0, h2 = 0;
+                for (uint32_t i = f; i <= l; ++i) {
+                    uint64_t a = (uint64_t)act[i] + 1;
+                    h1 = h1 * HB1 + a;
+                    h2 = h2 * HB2 + a;
+                }
+                uint64_t x1, x2;
+                finish_key(h1, h2, l - f + 1, weak != 0, x1, x2);
+                k1o[c] = x1;
+                k2o[c] = x2;
+            }
+        }
+    }
+    if (SMEM && tables) {
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < AA; e += AGG_THREADS) {
+            uint32_t cn = s_cnt[e];
+            if (cn) {
+                atomicAdd((unsigned long long*)&g_cnt[e], (unsigned long long)cn);
+                uint64_t sm64 = ((uint64_t)s_hi[e] << 32) | s_lo[e];
+                if (sm64) atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)sm64);
+            }
+        }
+        for (uint32_t a = threadIdx.x; a < A; a += AGG_THREADS) {
+            if (s_st[a]) atomicAdd((unsigned long long*)&g_st[a], (unsigned long long)s_st[a]);
+            if (s_en[a]) atomicAdd((unsigned long long*)&g_en[a], (unsigned long long)s_en[a]);
+        }
+    }
+}
+
+template <class P, bool SMEM>
+static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
+    const uint32_t A = L->A;
+    size_t smem = (SMEM && o.tables) ? ((size_t)3 * A * A + 2 * A) * 4 : 0;
+    static bool attr = false;
+    if (SMEM && !attr) {
+        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)AGG_SMEM_MAX));
+        attr = true;
+    }
+    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    uint64_t tiles = std::max<uint64_t>(1, (cap + AGG_CASES - 1) / AGG_CASES);
+    int per_sm = smem ? std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (smem + 1024))) : 8;
+    uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
+    // algorithmic bytes: read key + act once per event, + per-case outputs
+    double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 +
+                   (o.n_events ? cap * 4.0 : 0) + (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
+    PM4G_LAUNCH("k_aggregate", bytes, s,
+                (k_aggregate<P, SMEM><<<(unsigned)grid, AGG_THREADS, smem, s>>>(
+                    L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A,
+                    o.tables ? o.packed : nullptr, o.n_events, o.dur, o.k1, o.k2,
+                    debug_weak_hash() ? 1 : 0)));
+    return PM4G_OK;
+}
+
+pm4g_status aggregate(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
+    if (L->n == 0) return PM4G_OK;
+    const uint32_t A = L->A;
+    bool smem_ok = ((size_t)3 * A * A + 2 * A) * 4 <= AGG_SMEM_MAX;
+    switch (L->act_bytes) {
+        case 1: return smem_ok ? launch_agg<uint8_t, true>(L, o, s) : launch_agg<uint8_t, false>(L, o, s);
+        case 2: return smem_ok ? launch_agg<uint16_t, true>(L, o, s) : launch_agg<uint16_t, false>(L, o, s);
+        default: return smem_ok ? launch_agg<uint32_t, true>(L, o, s) : launch_agg<uint32_t, false>(L, o, s);
+    }
+}
+
+// ------------------------------------------------------------------ K11 finalise
+// R6: mean = (double)sum / (double)cnt for cnt > 0 (IEEE round-to-nearest), else 0.
+__global__ void k_finalize(const uint64_t* __restrict__ packed, uint32_t A, uint64_t* cnt,
+                           int64_t* sum, double* mean, uint64_t* st, uint64_t* en) {
+    const size_t AA = (size_t)A * A;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < AA + A;
+         e += (size_t)gridDim.x * blockDim.x) {
+        if (e < AA) {
+            uint64_t c = packed[e];
+            int64_t sm = (int64_t)packed[AA + e];
+            if (cnt) cnt[e] = c;
+            if (sum) sum[e] = sm;
+            if (mean) mean[e] = c ? __ddiv_rn((double)sm, (double)c) : 0.0;
+        } else {
+            size_t a = e - AA;
+            if (st) st[a] = packed[2 * AA + a];
+            if (en) en[a] = packed[2 * AA + A + a];
+        }
+    }
+}
+
+pm4g_status finalize_tables(const uint64_t* packed, uint32_t A, uint64_t* cnt, int64_t* sum,
+                            double* mean, uint64_t* st, uint64_t* en, cudaStream_t s) {
+    size_t total = (size_t)A * A + A;
+    int g = (int)std::min<size_t>((total + 255) / 256, (size_t)num_sms() * 4);
+    PM4G_LAUNCH("k_finalize", total * 8.0 * 2, s,
+                k_finalize<<<std::max(g, 1), 256, 0, s>>>(packed, A, cnt, sum, mean, st, en));
+    return PM4G_OK;
+}
+
+static pm4g_status require_sorted(const pm4g_log* L) {
+    if (!L) return fail(PM4G_EINVAL, "null log");
+    if (!L->sorted) return fail(PM4G_EINVAL, "log is not sorted (call pm4g_sort first)");
+    return PM4G_OK;
+}
+
+static size_t packed_len(uint32_t A) { return 2 * (size_t)A * A + 2 * (size_t)A; }
+
+static pm4g_status tables_into(const pm4g_log* L, uint64_t* packed, cudaStream_t s) {
+    PM4G_CK(cudaMemsetAsync(packed, 0, packed_len(L->A) * 8, s));
+    AggOut o;
+    o.packed = packed;
+    o.tables = true;
+    return aggregate(L, o, s);
+}
+
+}  // namespace pm4g
+
+using namespace pm4g;
+
+extern "C" {
+
+pm4g_status pm4g_tables_partial(const pm4g_log* L, uint64_t* packed, pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    if (!packed) return fail(PM4G_EINVAL, "null packed buffer");
+    return tables_into(L, packed, (cudaStream_t)stream);
+}
+
+pm4g_status pm4g_tables_finalize(const uint64_t* packed, uint32_t A, uint64_t* cnt,
+                                 int64_t* dur_sum, double* mean, uint64_t* start, uint64_t* end,
+                                 pm4g_stream_t stream) {
+    if (!packed || A == 0) return fail(PM4G_EINVAL, "bad arguments");
+    return finalize_tables(packed, A, cnt, dur_sum, mean, start, end, (cudaStream_t)stream);
+}
+
+pm4g_status pm4g_dfg(const pm4g_log* L, uint64_t* cnt, int64_t* dur_sum, double* mean,
+                     pm4g_comm* comm, pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    if (!cnt || !dur_sum) return fail(PM4G_EINVAL, "cnt and dur_sum are required");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch pk(s);
+    PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
+    PM4G_TRY(tables_into(L, pk.as<uint64_t>(), s));
+    if (comm) PM4G_TRY(comm_allreduce_u64(comm, pk.as<uint64_t>(), packed_len(L->A), s));
+    return finalize_tables(pk.as<uint64_t>(), L->A, cnt, dur_sum, mean, nullptr, nullptr, s);
+}
+
+pm4g_status pm4g_start_end(const pm4g_log* L, uint64_t* start, uint64_t* end, pm4g_comm* comm,
+                           pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    if (!start || !end) return fail(PM4G_EINVAL, "start and end are required");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch pk(s);
+    PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
+    PM4G_TRY(tables_into(L, pk.as<uint64_t>(), s));
+    if (comm) PM4G_TRY(comm_allreduce_u64(comm, pk.as<uint64_t>(), packed_len(L->A), s));
+    return finalize_tables(pk.as<uint64_t>(), L->A, nullptr, nullptr, nullptr, start, end, s);
+}
+
+pm4g_status pm4g_case_durations(const pm4g_log* L, uint32_t* case_code, uint32_t* n_events,
+                                int64_t* dur, uint64_t capacity, uint64_t* n_cases_out,
+                                pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    cudaStream_t s = (cudaStream_t)stream;
+    PM4G_TRY(fetch_n_cases(L, s));
+    if (n_cases_out) *n_cases_out = (uint64_t)L->n_cases;
+    if ((case_code || n_events || dur) && capacity < (uint64_t)L->n_cases)
+        return fail(PM4G_EINVAL, "capacity < n_cases");
+    if (L->n_cases == 0) return PM4G_OK;
+    if (case_code)
+        PM4G_CK(cudaMemcpyAsync(case_code, L->s_case_code, L->n_cases * 4, cudaMemcpyDeviceToDevice, s));
+    if (n_events || dur) {
+        AggOut o;
+        o.n_events = n_events;
+        o.dur = dur;
+        PM4G_TRY(aggregate(L, o, s));
+    }
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_variants(const pm4g_log* L, pm4g_comm* comm, pm4g_stream_t stream,
+                          pm4g_variant_table** out) {
+    PM4G_TRY(require_sorted(L));
+    if (!out) return fail(PM4G_EINVAL, "null out");
+    *out = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    Scratch keys(s);
+    PM4G_TRY(keys.alloc(std::max<uint64_t>(cap, 1) * 16));
+    AggOut o;
+    o.k1 = keys.as<uint64_t>();
+    o.k2 = o.k1 + std::max<uint64_t>(cap, 1);
+    PM4G_TRY(aggregate(L, o, s));
+    pm4g_variant_table* local = nullptr;
+    PM4G_TRY(variants_from_keys(L, o.k1, o.k2, s, &local));
+    if (!comm) {
+        *out = local;
+        return PM4G_OK;
+    }
+    pm4g_status st = comm_variants_allgather_merge(comm, local, s, out);
+    free_variants(local);
+    return st;
+}
+
+pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* comm,
+                         pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    if (!out) return fail(PM4G_EINVAL, "null outputs");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool want_tables = out->cnt || out->dur_sum || out->mean || out->start || out->end;
+    const bool want_cases = out->case_code || out->n_events || out->dur;
+    if (want_cases) {
+        PM4G_TRY(fetch_n_cases(L, s));
+        if (out->capacity < (uint64_t)L->n_cases) return fail(PM4G_EINVAL, "capacity < n_cases");
+    }
+    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    Scratch pk(s), keys(s);
+    AggOut o;
+    if (want_tables) {
+        PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
+        PM4G_CK(cudaMemsetAsync(pk.p, 0, packed_len(L->A) * 8, s));
+        o.packed = pk.as<uint64_t>();
+        o.tables = true;
+    }
+    o.n_events = out->n_events;
+    o.dur = out->dur;
+    if (out->variants) {
+        PM4G_TRY(keys.alloc(std::max<uint64_t>(cap, 1) * 16));
+        o.k1 = keys.as<uint64_t>();
+        o.k2 = o.k1 + std::max<uint64_t>(cap, 1);
+    }
+    PM4G_TRY(aggregate(L, o, s));
+    if (out->case_code && L->n_cases > 0)
+        PM4G_CK(cudaMemcpyAsync(out->case_code, L->s_case_code, L->n_cases * 4, cudaMemcpyDeviceToDevice, s));
+    if (want_tables) {
+        if (comm) PM4G_TRY(comm_allreduce_u64(comm, o.packed, packed_len(L->A), s));
+        PM4G_TRY(finalize_tables(o.packed, L->A, out->cnt, out->dur_sum, out->mean, out->start,
+                                 out->end, s));
+    }
+    if (out->variants) {
+        *out->variants = nullptr;
+        pm4g_variant_table* local = nullptr;
+        PM4G_TRY(variants_from_keys(L, o.k1, o.k2, s, &local));
+        if (!comm) {
+            *out->variants = local;
+        } else {
+            pm4g_status st = comm_variants_allgather_merge(comm, local, s, out->variants);
+            free_variants(local);
+            PM4G_TRY(st);
+        }
+    }
+    return PM4G_OK;
+}
+
+}  // extern "C"

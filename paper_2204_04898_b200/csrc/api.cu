@@ -1,0 +1,445 @@
+// libpm4g: handles, status/error machinery, profiling, log creation (K1) and
+// the thin C-ABI dispatch layer.  See include/pm4g.h for the contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pm4g_internal.cuh"
+
+namespace pm4g {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+pm4g_status fail(pm4g_status st, const std::string& m) {
+    g_err = m;
+    return st;
+}
+pm4g_status cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? PM4G_ENOMEM : PM4G_ECUDA;
+}
+
+// ------------------------------------------------------------------ launches / profiling
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct ProfRec {
+    const char* name;
+    double bytes;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_event_pool;
+struct ProfAgg {
+    std::string name;
+    uint64_t launches;
+    double ms, bytes;
+};
+static std::vector<ProfAgg> g_prof_aggs;
+
+static cudaEvent_t get_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(const char* name, double bytes, cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    ProfRec r{name, bytes, get_event(), get_event()};
+    cudaEventRecord(r.a, s);
+    g_prof_recs.push_back(r);
+}
+void prof_end(cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_recs.empty()) cudaEventRecord(g_prof_recs.back().b, s);
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+bool debug_weak_hash() {
+    const char* e = getenv("PM4G_DEBUG_WEAK_HASH");
+    return e && e[0] == '1';
+}
+
+// ------------------------------------------------------------------ memory
+static void setup_pool() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+pm4g_status dalloc(void** p, size_t bytes, cudaStream_t s) {
+    setup_pool();
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return cuda_fail(e, "cudaMallocAsync");
+    }
+    return PM4G_OK;
+}
+void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ------------------------------------------------------------------ K1: validate + metadata
+struct Meta {
+    long long ts_min, ts_max;
+    unsigned int case_min, case_max;
+    unsigned long long bad_case, bad_act, bad_extra;
+};
+
+template <class P>
+__global__ void k_validate(const uint32_t* __restrict__ cs, const P* __restrict__ act,
+                           const int64_t* __restrict__ ts, int64_t n, uint32_t lo, uint32_t hi,
+                           uint32_t A, Meta* m) {
+    long long tmin = LLONG_MAX, tmax = LLONG_MIN;
+    unsigned cmin = 0xffffffffu, cmax = 0;
+    unsigned long long bc = ~0ull, ba = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c = cs[i];
+        long long t = ts[i];
+        uint32_t a = (uint32_t)act[i];
+        tmin = min(tmin, t);
+        tmax = max(tmax, t);
+        cmin = min(cmin, c);
+        cmax = max(cmax, c);
+        if ((c < lo || c >= hi) && (unsigned long long)i < bc) bc = i;
+        if (a >= A && (unsigned long long)i < ba) ba = i;
+    }
+    for (int o = 16; o; o >>= 1) {
+        tmin = min(tmin, __shfl_xor_sync(~0u, tmin, o));
+        tmax = max(tmax, __shfl_xor_sync(~0u, tmax, o));
+        cmin = min(cmin, __shfl_xor_sync(~0u, cmin, o));
+        cmax = max(cmax, __shfl_xor_sync(~0u, cmax, o));
+        bc = min(bc, __shfl_xor_sync(~0u, bc, o));
+        ba = min(ba, __shfl_xor_sync(~0u, ba, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&m->ts_min, tmin);
+        atomicMax(&m->ts_max, tmax);
+        atomicMin(&m->case_min, cmin);
+        atomicMax(&m->case_max, cmax);
+        if (bc != ~0ull) atomicMin(&m->bad_case, bc);
+        if (ba != ~0ull) atomicMin(&m->bad_act, ba);
+    }
+}
+
+__global__ void k_validate_codes(const uint32_t* __restrict__ col, const uint8_t* __restrict__ valid,
+                                 int64_t n, uint64_t dict, Meta* m) {
+    unsigned long long b = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (valid && !valid[i]) continue;
+        if ((uint64_t)col[i] >= dict && (unsigned long long)i < b) b = i;
+    }
+    for (int o = 16; o; o >>= 1) b = min(b, __shfl_xor_sync(~0u, b, o));
+    if ((threadIdx.x & 31) == 0 && b != ~0ull) atomicMin(&m->bad_extra, b);
+}
+
+static int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    int64_t cap = (int64_t)num_sms() * 8;
+    return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
+    Meta h{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u, ~0ull, ~0ull, ~0ull};
+    Scratch md(s);
+    PM4G_TRY(md.alloc(sizeof(Meta)));
+    Meta* dm = md.as<Meta>();
+    PM4G_CK(cudaMemcpyAsync(dm, &h, sizeof(Meta), cudaMemcpyHostToDevice, s));
+    const int64_t n = L->n;
+    uint32_t hi = L->case_hi;
+    if (n > 0) {
+        int g = grid_for(n, 256);
+        double bytes = (double)n * (12 + L->act_bytes);
+        switch (L->act_bytes) {
+            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
+            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
+            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
+        }
+        for (auto& c : L->extra)
+            if (c.kind == PM4G_KIND_CODES)
+                PM4G_LAUNCH("k_validate_codes", n * 4.0, s, k_validate_codes<<<g, 256, 0, s>>>((const uint32_t*)c.data, c.valid, n, c.dict_size, dm));
+    }
+    PM4G_CK(cudaMemcpyAsync(&h, dm, sizeof(Meta), cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    if (h.bad_case != ~0ull)
+        return fail(PM4G_EDATA, "case code out of range [case_lo, case_hi) at row " + std::to_string(h.bad_case));
+    if (h.bad_act != ~0ull)
+        return fail(PM4G_EDATA, "activity code out of range (>= n_activities) at row " + std::to_string(h.bad_act));
+    if (h.bad_extra != ~0ull)
+        return fail(PM4G_EDATA, "extra-column code out of range at row " + std::to_string(h.bad_extra));
+    if (n == 0) {
+        L->ts_min = 0;
+        L->ts_max = -1;
+        L->case_min = L->case_max = L->case_lo;
+    } else {
+        L->ts_min = h.ts_min;
+        L->ts_max = h.ts_max;
+        L->case_min = h.case_min;
+        L->case_max = h.case_max;
+    }
+    uint64_t ts_span = n ? (uint64_t)L->ts_max - (uint64_t)L->ts_min : 0;
+    L->case_bits = bit_width_u64((uint64_t)(L->case_max - L->case_min));
+    L->ts_bits = bit_width_u64(ts_span);
+    L->key_bits = L->case_bits + L->ts_bits;
+    L->passes = (std::min(L->key_bits, 64) + 7) / 8;
+    return PM4G_OK;
+}
+
+pm4g_status fetch_n_cases(const pm4g_log* Lc, cudaStream_t s) {
+    pm4g_log* L = const_cast<pm4g_log*>(Lc);
+    if (L->n_cases >= 0) return PM4G_OK;
+    uint64_t v = 0;
+    PM4G_CK(cudaMemcpyAsync(&v, L->d_n_cases, sizeof(v), cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    L->n_cases = (int64_t)v;
+    return PM4G_OK;
+}
+
+static void free_log_cols(pm4g_log* L, cudaStream_t s) {
+    if (L->owns_cols) {
+        dfree(L->case_, s);
+        dfree(L->act, s);
+        dfree(L->ts, s);
+    }
+    L->case_ = nullptr;
+    L->act = nullptr;
+    L->ts = nullptr;
+    L->owns_cols = false;
+}
+
+}  // namespace pm4g
+
+using namespace pm4g;
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* pm4g_last_error(void) { return g_err.c_str(); }
+const char* pm4g_version(void) { return "pm4g 0.1 (sm_100a)"; }
+uint64_t pm4g_launch_count(void) { return g_launches.load(); }
+
+pm4g_status pm4g_prof_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return PM4G_OK;
+}
+pm4g_status pm4g_prof_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof_recs) {
+        g_event_pool.push_back(r.a);
+        g_event_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    g_prof_aggs.clear();
+    return PM4G_OK;
+}
+pm4g_status pm4g_prof_collect(int32_t* n_names) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_aggs.clear();
+    for (auto& r : g_prof_recs) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto it = std::find_if(g_prof_aggs.begin(), g_prof_aggs.end(),
+                               [&](const ProfAgg& a) { return a.name == r.name; });
+        if (it == g_prof_aggs.end()) {
+            g_prof_aggs.push_back({r.name, 0, 0.0, 0.0});
+            it = g_prof_aggs.end() - 1;
+        }
+        it->launches += 1;
+        it->ms += ms;
+        it->bytes += r.bytes;
+    }
+    if (n_names) *n_names = (int32_t)g_prof_aggs.size();
+    return PM4G_OK;
+}
+pm4g_status pm4g_prof_entry(int32_t i, const char** name, uint64_t* launches, double* total_ms,
+                            double* bytes) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (i < 0 || i >= (int32_t)g_prof_aggs.size()) return fail(PM4G_EINVAL, "prof entry out of range");
+    if (name) *name = g_prof_aggs[i].name.c_str();
+    if (launches) *launches = g_prof_aggs[i].launches;
+    if (total_ms) *total_ms = g_prof_aggs[i].ms;
+    if (bytes) *bytes = g_prof_aggs[i].bytes;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_log_create(const pm4g_log_desc* d, pm4g_stream_t stream, pm4g_log** out) {
+    if (!d || !out) return fail(PM4G_EINVAL, "null argument");
+    *out = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d->n_events < 0) return fail(PM4G_EINVAL, "n_events < 0");
+    if (d->n_events > (int64_t)ST_VAL)
+        return fail(PM4G_EINVAL, "n_events exceeds 2^30-1 per shard; shard the log across ranks");
+    if (d->act_bytes != 1 && d->act_bytes != 2 && d->act_bytes != 4)
+        return fail(PM4G_EINVAL, "act_bytes must be 1, 2 or 4");
+    if (d->n_activities == 0) return fail(PM4G_EINVAL, "n_activities must be >= 1");
+    if (d->act_bytes == 1 && d->n_activities > 256) return fail(PM4G_EINVAL, "n_activities > 256 needs act_bytes >= 2");
+    if (d->act_bytes == 2 && d->n_activities > 65536) return fail(PM4G_EINVAL, "n_activities > 65536 needs act_bytes = 4");
+    if (d->n_events > 0 && (!d->case_code || !d->act || !d->ts)) return fail(PM4G_EINVAL, "null column");
+    if (d->n_extra < 0 || (d->n_extra > 0 && !d->extra)) return fail(PM4G_EINVAL, "bad extra columns");
+    uint64_t hi = d->case_hi ? d->case_hi : d->n_case_codes;
+    if (hi > d->n_case_codes || d->case_lo > hi || hi > 0xffffffffull)
+        return fail(PM4G_EINVAL, "bad case range");
+    const bool host = d->flags & PM4G_HOST_INPUT;
+    const bool borrow = (d->flags & PM4G_BORROW) && !host;
+
+    pm4g_log* L = new pm4g_log();
+    L->n = d->n_events;
+    L->A = d->n_activities;
+    L->act_bytes = d->act_bytes;
+    L->n_case_codes = d->n_case_codes;
+    L->case_lo = d->case_lo;
+    L->case_hi = (uint32_t)hi;
+    L->stream = s;
+    const int64_t n = L->n;
+    auto bail = [&](pm4g_status st) {
+        pm4g_log_destroy(L);
+        return st;
+    };
+    pm4g_status st;
+    if (borrow) {
+        L->case_ = (uint32_t*)d->case_code;
+        L->act = (void*)d->act;
+        L->ts = (int64_t*)d->ts;
+        L->owns_cols = false;
+    } else {
+        L->owns_cols = true;
+        if ((st = dalloc((void**)&L->case_, n * 4, s)) != PM4G_OK) return bail(st);
+        if ((st = dalloc(&L->act, n * L->act_bytes, s)) != PM4G_OK) return bail(st);
+        if ((st = dalloc((void**)&L->ts, n * 8, s)) != PM4G_OK) return bail(st);
+        cudaMemcpyKind k = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        if (n > 0) {
+            cudaError_t e = cudaMemcpyAsync(L->case_, d->case_code, n * 4, k, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(L->act, d->act, n * L->act_bytes, k, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(L->ts, d->ts, n * 8, k, s);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "column copy"));
+        }
+    }
+    for (int i = 0; i < d->n_extra; ++i) {
+        const pm4g_column& c = d->extra[i];
+        if (c.kind < 0 || c.kind > 2 || (n > 0 && !c.data)) {
+            fail(PM4G_EINVAL, "bad extra column descriptor");
+            return bail(PM4G_EINVAL);
+        }
+        ExtraCol x;
+        x.kind = c.kind;
+        x.elem = c.kind == PM4G_KIND_CODES ? 4 : 8;
+        x.dict_size = c.dict_size;
+        if (borrow) {
+            x.data = (void*)c.data;
+            x.valid = (uint8_t*)c.valid;
+        } else {
+            x.owned = true;
+            if ((st = dalloc(&x.data, n * x.elem, s)) != PM4G_OK) return bail(st);
+            cudaMemcpyKind k = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+            if (n > 0) {
+                cudaError_t e = cudaMemcpyAsync(x.data, c.data, n * x.elem, k, s);
+                if (e != cudaSuccess) return bail(cuda_fail(e, "extra copy"));
+            }
+            if (c.valid) {
+                if ((st = dalloc((void**)&x.valid, n, s)) != PM4G_OK) return bail(st);
+                if (n > 0) {
+                    cudaError_t e = cudaMemcpyAsync(x.valid, c.valid, n, k, s);
+                    if (e != cudaSuccess) return bail(cuda_fail(e, "valid copy"));
+                }
+            }
+        }
+        L->extra.push_back(x);
+    }
+    if ((st = dalloc((void**)&L->d_n_cases, 8, s)) != PM4G_OK) return bail(st);
+    if ((st = validate_and_meta(L, s)) != PM4G_OK) return bail(st);
+    *out = L;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_log_destroy(pm4g_log* L) {
+    if (!L) return PM4G_OK;
+    cudaStream_t s = L->stream;
+    free_log_cols(L, s);
+    dfree(L->key, s);
+    dfree(L->s_act, s);
+    dfree(L->perm, s);
+    dfree(L->off, s);
+    dfree(L->s_case_code, s);
+    dfree(L->d_n_cases, s);
+    for (auto& x : L->extra)
+        if (x.owned) {
+            dfree(x.data, s);
+            dfree(x.valid, s);
+        }
+    delete L;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_log_info_get(const pm4g_log* L, pm4g_log_info* info) {
+    if (!L || !info) return fail(PM4G_EINVAL, "null argument");
+    if (L->sorted) PM4G_TRY(fetch_n_cases(L, L->stream));
+    info->n_events = L->n;
+    info->n_cases = L->sorted ? L->n_cases : -1;
+    info->sorted = L->sorted ? 1 : 0;
+    info->act_bytes = L->act_bytes;
+    info->n_activities = L->A;
+    info->case_lo = L->case_lo;
+    info->case_hi = L->case_hi;
+    info->ts_min = L->ts_min;
+    info->ts_max = L->ts_max;
+    info->case_bits = L->case_bits;
+    info->ts_bits = L->ts_bits;
+    info->key_bits = L->key_bits;
+    info->radix_passes = L->passes;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
+    if (!L) return fail(PM4G_EINVAL, "null log");
+    if (L->sorted) return PM4G_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (L->key_bits > 64)
+        return fail(PM4G_EKEYWIDTH, "case_bits + ts_bits = " + std::to_string(L->key_bits) +
+                                        " > 64: composite key does not fit");
+    PM4G_TRY(sort_log(L, s));
+    PM4G_TRY(segments(L, s));
+    free_log_cols(L, s);
+    L->sorted = true;
+    L->stream = s;
+    return PM4G_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+// A11: cross-GPU merge over NCCL (NVLink 5 / NVSwitch on an 8xB200 node).
+//
+// The log is sharded by contiguous case-code ranges (R19), so every
+// per-case quantity is local; only the A x A / A tables and the variant tables
+// need an exchange (associative, commutative merge with identity).
+//   C1  one ncclAllReduce(sum, uint64) of the packed [cnt | sum | start | end]
+//       table: integer sums are exact in any order (two's complement wraps
+//       identically), so the result is independent of the rank count.
+//   C2  ncclAllGather of (V_r, T_r), then padded all-gathers of the per-rank
+//       variant entries and representative sequences, merged on every rank
+//       with the same exact hash-and-verify engine used locally
+//       (merge_variant_tables).
+// NCCL is loaded with dlopen on first use so that libpm4g itself has no hard
+// link-time dependency on it; torch.distributed only carries the unique id.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pm4g_internal.cuh"
+
+namespace pm4g {
+
+typedef struct { char internal[128]; } NcclUid;
+typedef void* NcclComm;
+typedef int NcclResult;  // ncclSuccess = 0
+enum { NCCL_UINT64 = 5, NCCL_UINT8 = 1 };  // ncclDataType_t: ncclUint8 = 1, ncclUint64 = 5
+enum { NCCL_SUM = 0 };
+
+struct NcclApi {
+    void* h = nullptr;
+    NcclResult (*getUniqueId)(NcclUid*) = nullptr;
+    NcclResult (*commInitRank)(NcclComm*, int, NcclUid, int) = nullptr;
+    NcclResult (*commDestroy)(NcclComm) = nullptr;
+    NcclResult (*allReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    NcclResult (*allGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t) = nullptr;
+    const char* (*getErrorString)(NcclResult) = nullptr;
+};
+
+static NcclApi g_nccl;
+
+static pm4g_status load_nccl() {
+    if (g_nccl.h) return PM4G_OK;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* nm : names)
+        if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return fail(PM4G_ENCCL, std::string("cannot load NCCL: ") + dlerror());
+    g_nccl.h = h;
+    g_nccl.getUniqueId = (NcclResult(*)(NcclUid*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.commInitRank = (NcclResult(*)(NcclComm*, int, NcclUid, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.commDestroy = (NcclResult(*)(NcclComm))dlsym(h, "ncclCommDestroy");
+    g_nccl.allReduce = (NcclResult(*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllReduce");
+    g_nccl.allGather = (NcclResult(*)(const void*, void*, size_t, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllGather");
+    g_nccl.getErrorString = (const char* (*)(NcclResult))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.allReduce ||
+        !g_nccl.allGather) {
+        g_nccl = NcclApi();
+        return fail(PM4G_ENCCL, "NCCL symbols missing");
+    }
+    return PM4G_OK;
+}
+
+static pm4g_status nccl_fail(NcclResult r, const char* what) {
+    std::string m = std::string("NCCL error in ") + what + ": " +
+                    (g_nccl.getErrorString ? g_nccl.getErrorString(r) : std::to_string(r));
+    return fail(PM4G_ENCCL, m);
+}
+
+}  // namespace pm4g
+
+struct pm4g_comm {
+    pm4g::NcclComm comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+namespace pm4g {
+
+pm4g_status comm_allreduce_u64(pm4g_comm* c, uint64_t* buf, size_t count, cudaStream_t s) {
+    if (c->nranks == 1) return PM4G_OK;
+    NcclResult r = g_nccl.allReduce(buf, buf, count, NCCL_UINT64, NCCL_SUM, c->comm, s);
+    if (r) return nccl_fail(r, "ncclAllReduce");
+    return PM4G_OK;
+}
+
+__global__ void k_pack_entries(const pm4g_variant_table v, uint64_t* out) {
+    // per entry: k1, k2, count, (rep_case | len << 32)
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < v.V;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        out[4 * i + 0] = v.k1[i];
+        out[4 * i + 1] = v.k2[i];
+        out[4 * i + 2] = v.count[i];
+        out[4 * i + 3] = (uint64_t)v.rep_case[i] | ((uint64_t)v.len[i] << 32);
+    }
+}
+
+__global__ void k_unpack_entries(const uint64_t* in, uint64_t V, const uint32_t* acts_in,
+                                 uint64_t T, pm4g_variant_table v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        v.k1[i] = in[4 * i + 0];
+        v.k2[i] = in[4 * i + 1];
+        v.count[i] = in[4 * i + 2];
+        v.rep_case[i] = (uint32_t)in[4 * i + 3];
+        v.len[i] = (uint32_t)(in[4 * i + 3] >> 32);
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < T;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        v.seq_act[i] = acts_in[i];
+}
+
+pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
+                                          pm4g_variant_table** out) {
+    const int R = c->nranks;
+    if (R == 1) {
+        const pm4g_variant_table* parts[1] = {local};
+        return merge_variant_tables(parts, 1, s, out);
+    }
+    // sizes
+    Scratch sz(s);
+    PM4G_TRY(sz.alloc((size_t)R * 16 + 16));
+    uint64_t* d_sz = sz.as<uint64_t>();
+    uint64_t mine[2] = {local->V, local->total_len};
+    PM4G_CK(cudaMemcpyAsync(d_sz + 2 * R, mine, 16, cudaMemcpyHostToDevice, s));
+    NcclResult r = g_nccl.allGather(d_sz + 2 * R, d_sz, 2, NCCL_UINT64, c->comm, s);
+    if (r) return nccl_fail(r, "ncclAllGather(sizes)");
+    std::vector<uint64_t> sizes(2 * R);
+    PM4G_CK(cudaMemcpyAsync(sizes.data(), d_sz, 16 * R, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    uint64_t Vmax = 1, Tmax = 1;
+    for (int i = 0; i < R; ++i) {
+        Vmax = std::max(Vmax, sizes[2 * i]);
+        Tmax = std::max(Tmax, sizes[2 * i + 1]);
+    }
+    Scratch send(s), recv(s);
+    PM4G_TRY(send.alloc(Vmax * 32 + Tmax * 4));
+    PM4G_TRY(recv.alloc((size_t)R * (Vmax * 32 + Tmax * 4)));
+    uint64_t* se = send.as<uint64_t>();
+    uint32_t* sa = (uint32_t*)(se + 4 * Vmax);
+    if (local->V) {
+        int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((local->V + 255) / 256, 1024));
+        PM4G_LAUNCH("k_pack_entries", local->V * 64.0, s, k_pack_entries<<<g, 256, 0, s>>>(*local, se));
+        PM4G_CK(cudaMemcpyAsync(sa, local->seq_act, local->total_len * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    uint64_t* re = recv.as<uint64_t>();
+    uint32_t* ra = (uint32_t*)(re + 4 * Vmax * R);
+    r = g_nccl.allGather(se, re, 4 * Vmax, NCCL_UINT64, c->comm, s);
+    if (r) return nccl_fail(r, "ncclAllGather(entries)");
+    r = g_nccl.allGather(sa, ra, Tmax * 4, NCCL_UINT8, c->comm, s);
+    if (r) return nccl_fail(r, "ncclAllGather(sequences)");
+    // unpack into R temporary tables and merge
+    std::vector<pm4g_variant_table*> parts(R, nullptr);
+    pm4g_status st = PM4G_OK;
+    for (int i = 0; i < R && st == PM4G_OK; ++i) {
+        pm4g_variant_table* v = new pm4g_variant_table();
+        v->stream = s;
+        v->V = sizes[2 * i];
+        v->total_len = sizes[2 * i + 1];
+        parts[i] = v;
+        uint64_t V1 = std::max<uint64_t>(v->V, 1);
+        if ((st = dalloc_t(&v->k1, V1, s)) || (st = dalloc_t(&v->k2, V1, s)) ||
+            (st = dalloc_t(&v->count, V1, s)) || (st = dalloc_t(&v->rep_case, V1, s)) ||
+            (st = dalloc_t(&v->len, V1, s)) ||
+            (st = dalloc_t(&v->seq_act, std::max<uint64_t>(v->total_len, 1), s)))
+            break;
+        uint64_t n = std::max(v->V, v->total_len);
+        if (n) {
+            int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 1024));
+            prof_begin("k_unpack_entries", v->V * 64.0, s);
+            k_unpack_entries<<<g, 256, 0, s>>>(re + 4 * Vmax * i, v->V, ra + Tmax * i, v->total_len, *v);
+            cudaError_t e = cudaGetLastError();
+            prof_end(s);
+            count_launch();
+            if (e != cudaSuccess) st = cuda_fail(e, "k_unpack_entries");
+        }
+    }
+    if (st == PM4G_OK) st = merge_variant_tables(parts.data(), R, s, out);
+    for (auto* v : parts) free_variants(v);
+    return st;
+}
+
+__global__ void k_sum_parts(const uint64_t* parts, int R, uint64_t len, uint64_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t a = 0;
+        for (int r = 0; r < R; ++r) a += parts[(uint64_t)r * len + i];
+        out[i] = a;
+    }
+}
+
+}  // namespace pm4g
+
+using namespace pm4g;
+
+extern "C" {
+
+pm4g_status pm4g_comm_unique_id(void* id_out, size_t* id_bytes) {
+    if (!id_out) return fail(PM4G_EINVAL, "null id");
+    PM4G_TRY(load_nccl());
+    NcclUid uid;
+    NcclResult r = g_nccl.getUniqueId(&uid);
+    if (r) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id_out, &uid, sizeof(uid));
+    if (id_bytes) *id_bytes = sizeof(uid);
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_comm_create(const void* id, int32_t nranks, int32_t rank, pm4g_comm** out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(PM4G_EINVAL, "bad arguments");
+    *out = nullptr;
+    pm4g_comm* c = new pm4g_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks > 1) {
+        pm4g_status st = load_nccl();
+        if (st) {
+            delete c;
+            return st;
+        }
+        NcclUid uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        NcclResult r = g_nccl.commInitRank(&c->comm, nranks, uid, rank);
+        if (r) {
+            delete c;
+            return nccl_fail(r, "ncclCommInitRank");
+        }
+    }
+    *out = c;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_comm_destroy(pm4g_comm* c) {
+    if (!c) return PM4G_OK;
+    if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    delete c;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_sum_u64(const uint64_t* parts, int32_t n_parts, uint64_t len, uint64_t* out,
+                         pm4g_stream_t stream) {
+    if (!parts || !out || n_parts <= 0) return fail(PM4G_EINVAL, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!len) return PM4G_OK;
+    int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((len + 255) / 256, (uint64_t)num_sms() * 4));
+    PM4G_LAUNCH("k_sum_parts", (double)len * 8 * (n_parts + 1), s,
+                k_sum_parts<<<g, 256, 0, s>>>(parts, n_parts, len, out));
+    return PM4G_OK;
+}
+
+}  // extern "C"

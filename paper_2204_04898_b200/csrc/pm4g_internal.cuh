@@ -1,0 +1,240 @@
+// Internal declarations shared by the libpm4g translation units.
+// Product code: sm_100a only, no CPU fallback, no dependency on oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pm4g.h"
+
+namespace pm4g {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+pm4g_status fail(pm4g_status st, const std::string& msg);
+pm4g_status cuda_fail(cudaError_t e, const char* what);
+
+#define PM4G_CK(call)                                          \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return ::pm4g::cuda_fail(_e, #call); \
+    } while (0)
+
+#define PM4G_TRY(call)                          \
+    do {                                        \
+        pm4g_status _s = (call);                \
+        if (_s != PM4G_OK) return _s;           \
+    } while (0)
+
+// ------------------------------------------------------------------ launches
+// Every kernel launch goes through PM4G_LAUNCH: it counts the launch and, when
+// profiling is on, brackets it with CUDA events on the launching stream.
+void prof_begin(const char* name, double bytes, cudaStream_t s);
+void prof_end(cudaStream_t s);
+void count_launch();
+
+#define PM4G_LAUNCH(name, bytes, stream, ...)                                  \
+    do {                                                                       \
+        ::pm4g::prof_begin(name, (double)(bytes), stream);                     \
+        __VA_ARGS__;                                                           \
+        cudaError_t _le = cudaGetLastError();                                  \
+        ::pm4g::prof_end(stream);                                              \
+        ::pm4g::count_launch();                                                \
+        if (_le != cudaSuccess) return ::pm4g::cuda_fail(_le, name);           \
+    } while (0)
+
+int num_sms();
+bool debug_weak_hash();
+
+// ------------------------------------------------------------------ memory
+// Stream-ordered allocations from the device's default pool (kept cached).
+pm4g_status dalloc(void** p, size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+
+template <class T>
+pm4g_status dalloc_t(T** p, size_t count, cudaStream_t s) {
+    return dalloc((void**)p, count * sizeof(T), s);
+}
+
+// RAII scratch buffer freed (stream-ordered) at scope exit.
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() { if (p) dfree(p, s); }
+    pm4g_status alloc(size_t bytes) { return dalloc(&p, bytes ? bytes : 16, s); }
+    template <class T> T* as() const { return (T*)p; }
+};
+
+// ------------------------------------------------------------------ the log
+struct ExtraCol {
+    int32_t kind = 0;
+    int elem = 4;               // bytes per element (4 codes, 8 i64 / f64)
+    void* data = nullptr;       // device [n]
+    uint8_t* valid = nullptr;   // device [n] or nullptr
+    uint64_t dict_size = 0;
+    bool owned = false;
+};
+
+}  // namespace pm4g
+
+struct pm4g_log {
+    int64_t n = 0;
+    uint32_t A = 1;
+    int act_bytes = 1;          // internal activity width (1, 2, 4)
+    uint64_t n_case_codes = 0;
+    uint32_t case_lo = 0, case_hi = 0;
+    int64_t ts_min = 0, ts_max = -1;
+    uint32_t case_min = 0, case_max = 0;   // present range
+    // composite key ((case - case_min) << ts_bits) | (ts - ts_min)
+    int case_bits = 0, ts_bits = 0, key_bits = 0, passes = 0;
+    bool sorted = false;
+    // ingested state
+    uint32_t* case_ = nullptr;
+    void* act = nullptr;
+    int64_t* ts = nullptr;
+    bool owns_cols = false;
+    // formatted state
+    uint64_t* key = nullptr;    // [n] sorted composite keys
+    void* s_act = nullptr;      // [n] sorted activities
+    uint32_t* perm = nullptr;   // [n] ingest row of each formatted row (only with extras)
+    uint32_t* off = nullptr;    // [n_cases + 1] case row offsets (CSR)
+    uint32_t* s_case_code = nullptr;  // [n_cases] case code of each case
+    uint64_t* d_n_cases = nullptr;    // device scalar
+    int64_t n_cases = -1;             // host copy (-1 until fetched)
+    std::vector<pm4g::ExtraCol> extra;
+    cudaStream_t stream = nullptr;
+};
+
+struct pm4g_variant_table {
+    uint64_t V = 0, total_len = 0, n_cases = 0;
+    uint64_t* count = nullptr;     // [V]
+    uint32_t* len = nullptr;       // [V]
+    uint32_t* rep_case = nullptr;  // [V] case code
+    uint64_t* seq_off = nullptr;   // [V+1]
+    uint32_t* seq_act = nullptr;   // [total_len]
+    uint64_t* k1 = nullptr;        // [V] variant key (for cross-rank merge)
+    uint64_t* k2 = nullptr;        // [V]
+    uint32_t* case_variant = nullptr;  // [n_cases]
+    cudaStream_t stream = nullptr;
+};
+
+namespace pm4g {
+
+// ------------------------------------------------------------------ helpers
+__host__ __device__ inline int bit_width_u64(uint64_t x) {
+#ifdef __CUDA_ARCH__
+    return x ? 64 - __clzll((long long)x) : 0;
+#else
+    return x ? 64 - __builtin_clzll(x) : 0;
+#endif
+}
+__host__ __device__ inline uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0 : (x >> s); }
+__host__ __device__ inline uint64_t low_mask(int bits) {
+    return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+}
+
+template <class T>
+__device__ __forceinline__ T ld_volatile(const T* p) { return *(const volatile T*)p; }
+template <class T>
+__device__ __forceinline__ void st_volatile(T* p, T v) { *(volatile T*)p = v; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Decoupled look-back (single value per tile), status word = flag(2) | value(30).
+constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
+
+// Called by ONE thread per tile: publishes the tile's aggregate, walks back to
+// an inclusive prefix, publishes its own inclusive value and returns the
+// exclusive prefix.
+__device__ __forceinline__ uint32_t lookback_single(uint32_t* status, uint32_t tile,
+                                                    uint32_t aggregate) {
+    if (tile == 0) {
+        st_volatile(&status[0], ST_INC | aggregate);
+        return 0;
+    }
+    st_volatile(&status[tile], ST_AGG | aggregate);
+    uint32_t prefix = 0;
+    int64_t p = (int64_t)tile - 1;
+    while (true) {
+        uint32_t v;
+        do { v = ld_volatile(&status[p]); } while ((v >> 30) == 0);
+        prefix += v & ST_VAL;
+        if ((v >> 30) == 2) break;
+        --p;
+    }
+    st_volatile(&status[tile], ST_INC | (prefix + aggregate));
+    return prefix;
+}
+
+// Block-wide exclusive scan of one u32 per thread (BLOCK threads, multiple of 32).
+template <int BLOCK>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp, uint32_t* total) {
+    constexpr int W = BLOCK / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < W ? s_warp[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < W) s_warp[lane] = wi - w;
+        if (lane == W - 1) s_warp[W] = wi;
+    }
+    __syncthreads();
+    uint32_t r = s_warp[warp] + inc - x;
+    if (total) *total = s_warp[W];
+    return r;
+}
+
+// ------------------------------------------------------------------ entry points
+// (implemented across the .cu files)
+pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s);   // K1
+pm4g_status sort_log(pm4g_log* L, cudaStream_t s);            // A2-A4
+pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4
+pm4g_status fetch_n_cases(const pm4g_log* L, cudaStream_t s);
+pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits,
+                           cudaStream_t s);  // generic: (key, u32 payload), in place
+pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s);
+
+struct AggOut {
+    uint64_t* packed = nullptr;   // [cnt A2 | sum A2 | start A | end A] (zeroed by caller)
+    uint32_t* n_events = nullptr; // [n_cases]
+    int64_t* dur = nullptr;       // [n_cases]
+    uint64_t* k1 = nullptr;       // [n_cases] variant keys
+    uint64_t* k2 = nullptr;
+    bool tables = false;
+};
+pm4g_status aggregate(const pm4g_log* L, const AggOut& o, cudaStream_t s);   // K6
+pm4g_status finalize_tables(const uint64_t* packed, uint32_t A, uint64_t* cnt, int64_t* sum,
+                            double* mean, uint64_t* start, uint64_t* end, cudaStream_t s);
+pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint64_t* k2,
+                               cudaStream_t s, pm4g_variant_table** out);
+pm4g_status comm_allreduce_u64(pm4g_comm* c, uint64_t* buf, size_t count, cudaStream_t s);
+pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
+                                          pm4g_variant_table** out);
+pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
+                                 pm4g_variant_table** out);
+void free_variants(pm4g_variant_table* v);
+
+}  // namespace pm4g

@@ -1,0 +1,596 @@
+// A9: variants -- group-count of cases by exact activity sequence.
+//
+// P:102-103 "This requires a double aggregation: first, the events need to be
+// grouped in cases. Then this grouping is used to aggregate the cases into the
+// variants."  P:113: the cases dataframe carries "numerical features that
+// uniquely identify the case's variant" -- here a 128-bit key (two 64-bit
+// polynomial hashes + length, computed in the fused pass A8).  Identity is the
+// exact sequence (R10), so hashing is only an accelerator:
+//
+//   round r:  every unresolved item inserts its (salted) key into a device
+//             open-addressing table (one 128-bit CAS claims a slot), adds its
+//             weight, and atomicMin's its order key (-> the group's
+//             representative = smallest case code, R11);
+//             every item compares its sequence with its representative's;
+//             mismatches (hash collisions) are taken back out of the group and
+//             retried in round r+1 with a fresh salt.  Each round resolves at
+//             least the representative's sequence of every slot, so the loop
+//             terminates even with a degenerate hash (PM4G_DEBUG_WEAK_HASH=1
+//             uses a 4-bit key to exercise exactly this path).
+//
+// The same engine merges per-shard variant tables (items = table entries,
+// weight = count, order = representative case code) for the multi-GPU path.
+// Output order: count desc, then representative case code asc (R11), via the
+// library's radix sort on ((~count) << 32 | order).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "pm4g_internal.cuh"
+
+namespace pm4g {
+
+struct alignas(16) Slot {
+    unsigned long long k1, k2;
+    unsigned long long weight;
+    unsigned int rep;   // min order key
+    unsigned int len;
+};
+struct alignas(16) K128 {
+    unsigned long long a, b;
+};
+
+__device__ __forceinline__ K128 ld_k128(const void* p) {
+    K128 r;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.a), "=l"(r.b) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t vmix(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__global__ void k_init_table(Slot* table, uint64_t cap) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        Slot z;
+        z.k1 = 0;
+        z.k2 = 0;
+        z.weight = 0;
+        z.rep = 0xffffffffu;
+        z.len = 0;
+        table[i] = z;
+    }
+}
+
+// Items: i in [0, n_items) (or list[i] when list != nullptr)
+template <class OFF>
+__global__ void k_insert(const uint32_t* __restrict__ list, uint64_t n_items,
+                         const uint64_t* __restrict__ k1, const uint64_t* __restrict__ k2,
+                         const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
+                         const uint32_t* __restrict__ order, Slot* table, uint64_t mask,
+                         uint64_t salt, uint32_t* __restrict__ item_slot,
+                         uint8_t* __restrict__ pending, uint32_t* overflow) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = list ? list[t] : (uint32_t)t;
+        uint64_t a = k1[it], b = k2[it];
+        if (salt) {
+            a = vmix(a ^ salt) | 1ull;
+            b = vmix(b + salt);
+        }
+        const uint32_t len = (uint32_t)(off[it + 1] - off[it]);
+        const uint64_t w = weight ? weight[it] : 1ull;
+        const uint32_t ord = order ? order[it] : it;
+        uint64_t h = (a ^ (a >> 29) ^ (b * 0x9E3779B97F4A7C15ull)) & mask;
+        uint64_t probes = 0;
+        bool done = false;
+        while (!done) {
+            Slot* sp = &table[h];
+            K128 cur = ld_k128(sp);
+            if (cur.a == a && cur.b == b) {
+                done = true;
+            } else if (cur.a == 0 && cur.b == 0) {
+                K128 exp{0, 0}, des{a, b};
+                K128 old = atomicCAS((K128*)sp, exp, des);
+                if ((old.a == 0 && old.b == 0)) {
+                    sp->len = len;
+                    done = true;
+                } else if (old.a == a && old.b == b) {
+                    done = true;
+                }
+            }
+            if (!done) {
+                h = (h + 1) & mask;
+                if (++probes > mask) {
+                    atomicExch(overflow, 1u);
+                    break;
+                }
+            }
+        }
+        if (!done) continue;
+        atomicAdd(&table[h].weight, (unsigned long long)w);
+        atomicMin(&table[h].rep, ord);
+        item_slot[it] = (uint32_t)h;
+        pending[it] = 0;
+    }
+}
+
+// Each item compares its sequence with its slot representative's; the rep is
+// the item whose order key equals slot.rep: item_of_order maps order -> item
+// (identity when order == nullptr).
+template <class OFF, class ACT>
+__global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
+                         const OFF* __restrict__ off, const ACT* __restrict__ acts,
+                         const uint64_t* __restrict__ weight, const uint32_t* __restrict__ order,
+                         const uint32_t* __restrict__ item_of_rep_slot, Slot* table,
+                         const uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending,
+                         uint32_t* __restrict__ next_list, uint32_t* __restrict__ next_count) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = list ? list[t] : (uint32_t)t;
+        const uint32_t sl = item_slot[it];
+        const uint32_t ord = order ? order[it] : it;
+        if (table[sl].rep == ord) continue;             // the representative itself
+        const uint32_t rep_it = item_of_rep_slot[sl];
+        const OFF f = off[it], l = off[it + 1], rf = off[rep_it], rl = off[rep_it + 1];
+        bool same = (l - f) == (rl - rf);
+        for (OFF i = 0; same && i < l - f; ++i) same = acts[f + i] == acts[rf + i];
+        if (!same) {
+            atomicAdd(&table[sl].weight, (unsigned long long)(0ull - (weight ? weight[it] : 1ull)));
+            pending[it] = 1;
+            next_list[atomicAdd(next_count, 1u)] = it;
+        }
+    }
+}
+
+// slot -> representative item (the item whose order == slot.rep)
+__global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
+                           const uint32_t* __restrict__ order, const Slot* __restrict__ table,
+                           const uint32_t* __restrict__ item_slot, uint32_t* __restrict__ item_of_rep_slot) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = list ? list[t] : (uint32_t)t;
+        const uint32_t sl = item_slot[it];
+        if (table[sl].rep == (order ? order[it] : it)) item_of_rep_slot[sl] = it;
+    }
+}
+
+// occupied slots with weight > 0 -> groups (append order is irrelevant: the
+// final sort is a total order)
+__global__ void k_compact(const Slot* __restrict__ table, uint64_t cap,
+                          const uint32_t* __restrict__ item_of_rep_slot, uint32_t* __restrict__ slot_group,
+                          uint64_t* __restrict__ g_weight, uint32_t* __restrict__ g_rep_item,
+                          uint32_t* __restrict__ g_order, uint32_t* __restrict__ n_groups) {
+    for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < cap;
+         sl += (uint64_t)gridDim.x * blockDim.x) {
+        const Slot& s = table[sl];
+        if ((s.k1 | s.k2) == 0 || s.weight == 0) continue;
+        uint32_t g = atomicAdd(n_groups, 1u);
+        g_weight[g] = s.weight;
+        g_rep_item[g] = item_of_rep_slot[sl];
+        g_order[g] = s.rep;
+        slot_group[sl] = g;
+    }
+}
+
+__global__ void k_item_group(const uint32_t* __restrict__ list, uint64_t n_items,
+                             const uint32_t* __restrict__ item_slot, const uint8_t* __restrict__ pending,
+                             const uint32_t* __restrict__ slot_group, uint32_t* __restrict__ item_group) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t it = list ? list[t] : (uint32_t)t;
+        if (!pending[it]) item_group[it] = slot_group[item_slot[it]];
+    }
+}
+
+__global__ void k_sort_keys(const uint64_t* __restrict__ g_weight, const uint32_t* __restrict__ g_order,
+                            uint64_t G, uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t w = g_weight[g];
+        uint32_t wc = w > 0xffffffffull ? 0xffffffffu : (uint32_t)w;
+        key[g] = ((uint64_t)(0xffffffffu - wc) << 32) | g_order[g];
+        val[g] = (uint32_t)g;
+    }
+}
+
+struct Groups {
+    uint64_t G = 0;
+    uint64_t* weight = nullptr;     // [G]
+    uint32_t* rep_item = nullptr;   // [G]
+    uint32_t* order = nullptr;      // [G] (rep's order key)
+    uint32_t* item_group = nullptr; // [n_items]
+    uint32_t* sorted = nullptr;     // [G] group ids in output order
+    uint32_t* inv = nullptr;        // [G] group -> output position
+    void free(cudaStream_t s) {
+        dfree(weight, s);
+        dfree(rep_item, s);
+        dfree(order, s);
+        dfree(item_group, s);
+        dfree(sorted, s);
+        dfree(inv, s);
+    }
+};
+
+__global__ void k_inv(const uint32_t* __restrict__ sorted, uint64_t G, uint32_t* __restrict__ inv) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < G;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        inv[sorted[p]] = (uint32_t)p;
+}
+
+static int gsz(uint64_t n) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 8));
+}
+
+static uint64_t pow2_at_least(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Group n_items items by exact sequence.  order: unique u32 per item (nullptr
+// = item index).  order_bits: bits needed by the order key (for the sort).
+template <class OFF, class ACT>
+static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint64_t* k2,
+                               const OFF* off, const ACT* acts, const uint64_t* weight,
+                               const uint32_t* order, int order_bits, cudaStream_t s, Groups* out) {
+    Groups g;
+    auto bail = [&](pm4g_status st) {
+        g.free(s);
+        return st;
+    };
+    pm4g_status st;
+    const uint64_t N = std::max<uint64_t>(n_items, 1);
+    if ((st = dalloc_t(&g.item_group, N, s))) return bail(st);
+    if ((st = dalloc_t(&g.weight, N, s))) return bail(st);
+    if ((st = dalloc_t(&g.rep_item, N, s))) return bail(st);
+    if ((st = dalloc_t(&g.order, N, s))) return bail(st);
+    if (n_items == 0) {
+        *out = g;
+        return PM4G_OK;
+    }
+    Scratch work(s);
+    // item_slot u32 | pending u8 | list_a u32 | list_b u32 | counters
+    const size_t wbytes = N * 4 + N + 16 + N * 4 * 2 + 64;
+    if ((st = work.alloc(wbytes))) return bail(st);
+    uint32_t* item_slot = work.as<uint32_t>();
+    uint8_t* pending = (uint8_t*)(item_slot + N);
+    uint32_t* list_a = (uint32_t*)(((uintptr_t)(pending + N) + 15) & ~(uintptr_t)15);
+    uint32_t* list_b = list_a + N;
+    uint32_t* counters = list_b + N;  // [0] next_count, [1] overflow, [2] n_groups
+    PM4G_CK(cudaMemsetAsync(counters, 0, 16, s));
+
+    const uint32_t* list = nullptr;   // round 0: all items
+    uint64_t n_active = n_items;
+    uint64_t G = 0;
+    uint64_t cap_hint = pow2_at_least(std::max<uint64_t>(1024, 2 * std::min<uint64_t>(n_items, 1ull << 20)));
+    const bool weak = debug_weak_hash();
+    for (int round = 0; n_active > 0; ++round) {
+        uint64_t cap = std::min<uint64_t>(cap_hint, pow2_at_least(std::max<uint64_t>(1024, 2 * n_active)));
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            Scratch tab(s), aux(s);
+            if ((st = tab.alloc(cap * sizeof(Slot)))) return bail(st);
+            if ((st = aux.alloc(cap * 8))) return bail(st);
+            Slot* table = tab.as<Slot>();
+            uint32_t* item_of_rep_slot = aux.as<uint32_t>();
+            uint32_t* slot_group = item_of_rep_slot + cap;
+            PM4G_LAUNCH("k_variant_init", cap * 32.0, s, (k_init_table<<<gsz(cap), 256, 0, s>>>(table, cap)));
+            PM4G_CK(cudaMemsetAsync(counters, 0, 8, s));
+            uint64_t salt = (round == 0 || weak) ? 0ull : 0x9E3779B97F4A7C15ull * (uint64_t)round;
+            uint32_t* next_list = (list == list_a) ? list_b : list_a;
+            const int gs = gsz(n_active);
+            PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
+                        (k_insert<OFF><<<gs, 256, 0, s>>>(list, n_active, k1, k2, off, weight, order,
+                                                          table, cap - 1, salt, item_slot, pending,
+                                                          counters + 1)));
+            PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
+                        (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot)));
+            PM4G_LAUNCH("k_variant_verify", n_active * 16.0, s,
+                        (k_verify<OFF, ACT><<<gs, 256, 0, s>>>(list, n_active, off, acts, weight, order,
+                                                               item_of_rep_slot, table, item_slot,
+                                                               pending, next_list, counters)));
+            uint32_t h[2] = {0, 0};
+            PM4G_CK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, s));
+            PM4G_CK(cudaStreamSynchronize(s));
+            if (h[1]) {  // table overflow: retry this round with a full-size table
+                if (attempt == 1) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
+                cap = pow2_at_least(2 * n_active + 1024);
+                continue;
+            }
+            PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
+                        (k_compact<<<gsz(cap), 256, 0, s>>>(table, cap, item_of_rep_slot, slot_group,
+                                                            g.weight, g.rep_item, g.order,
+                                                            counters + 2)));
+            PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
+                        (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
+                                                         g.item_group)));
+            n_active = h[0];
+            list = next_list;
+            if (round > 64 * 1024) return bail(fail(PM4G_ECUDA, "variant grouping did not converge"));
+            break;
+        }
+    }
+    {   // total groups over all rounds (counters[2] accumulates across rounds)
+        uint32_t ng = 0;
+        PM4G_CK(cudaMemcpyAsync(&ng, counters + 2, 4, cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaStreamSynchronize(s));
+        G = ng;
+    }
+    g.G = G;
+    // sort groups: count desc, order asc
+    Scratch sk(s);
+    if ((st = sk.alloc(G * 8 + 16))) return bail(st);
+    if ((st = dalloc_t(&g.sorted, std::max<uint64_t>(G, 1), s))) return bail(st);
+    if ((st = dalloc_t(&g.inv, std::max<uint64_t>(G, 1), s))) return bail(st);
+    PM4G_LAUNCH("k_variant_sortkeys", G * 16.0, s,
+                (k_sort_keys<<<gsz(G), 256, 0, s>>>(g.weight, g.order, G, sk.as<uint64_t>(), g.sorted)));
+    PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, 32 + order_bits, s));
+    PM4G_LAUNCH("k_variant_inv", G * 8.0, s, (k_inv<<<gsz(G), 256, 0, s>>>(g.sorted, G, g.inv)));
+    *out = g;
+    return PM4G_OK;
+}
+
+
+// ------------------------------------------------------------------ exclusive scan
+constexpr int SCAN_THREADS = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_THREADS * SCAN_IPT;
+
+__global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __restrict__ in,
+                                                            uint64_t* __restrict__ out, int64_t n,
+                                                            uint32_t* status, uint32_t* counter) {
+    __shared__ uint32_t s_tile, s_scan[SCAN_THREADS / 32 + 1], s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t b = (int64_t)tile * SCAN_TILE + threadIdx.x * SCAN_IPT;
+    uint32_t v[SCAN_IPT], sum = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; ++j) {
+        v[j] = (b + j < n) ? in[b + j] : 0u;
+        sum += v[j];
+    }
+    uint32_t total;
+    uint32_t ex = block_excl_scan<SCAN_THREADS>(sum, s_scan, &total);
+    if (threadIdx.x == 0) s_prefix = lookback_single(status, tile, total);
+    __syncthreads();
+    uint64_t r = (uint64_t)s_prefix + ex;
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; ++j) {
+        if (b + j < n) out[b + j] = r;
+        r += v[j];
+    }
+    if (threadIdx.x == 0 && (int64_t)(tile + 1) * SCAN_TILE >= n) out[n] = (uint64_t)s_prefix + total;
+}
+
+// out[0..n] = exclusive prefix sums of in[0..n), out[n] = total (< 2^30)
+pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
+    if (n == 0) {
+        PM4G_CK(cudaMemsetAsync(out, 0, 8, s));
+        return PM4G_OK;
+    }
+    const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    Scratch st(s);
+    PM4G_TRY(st.alloc((tiles + 1) * 4));
+    PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * 4, s));
+    PM4G_LAUNCH("k_excl_scan", n * 12.0, s,
+                (k_excl_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, st.as<uint32_t>() + 1,
+                                                                     st.as<uint32_t>())));
+    return PM4G_OK;
+}
+
+// ------------------------------------------------------------------ emission
+// rep_code: per item -> case code of the item (local: case code of the case;
+// merge: the entry's representative code).
+template <class OFF>
+__global__ void k_emit(const Groups g, const OFF* __restrict__ off, const uint32_t* __restrict__ rep_code,
+                       const uint64_t* __restrict__ k1, const uint64_t* __restrict__ k2,
+                       uint64_t* __restrict__ count, uint32_t* __restrict__ len,
+                       uint32_t* __restrict__ rep_case, uint64_t* __restrict__ ok1,
+                       uint64_t* __restrict__ ok2) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < g.G;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t gid = g.sorted[p];
+        const uint32_t it = g.rep_item[gid];
+        count[p] = g.weight[gid];
+        len[p] = (uint32_t)(off[it + 1] - off[it]);
+        rep_case[p] = rep_code[it];
+        ok1[p] = k1[it];
+        ok2[p] = k2[it];
+    }
+}
+
+// one warp per variant: copy the representative's sequence
+template <class OFF, class ACT>
+__global__ void k_seq_gather(const Groups g, const OFF* __restrict__ off, const ACT* __restrict__ acts,
+                             const uint64_t* __restrict__ seq_off, uint32_t* __restrict__ seq_act) {
+    const uint64_t warps = (uint64_t)gridDim.x * blockDim.x / 32;
+    for (uint64_t p = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; p < g.G; p += warps) {
+        const uint32_t it = g.rep_item[g.sorted[p]];
+        const OFF f = off[it];
+        const uint64_t o = seq_off[p], L = seq_off[p + 1] - o;
+        for (uint64_t i = threadIdx.x & 31; i < L; i += 32) seq_act[o + i] = (uint32_t)acts[f + i];
+    }
+}
+
+__global__ void k_case_variant(const uint32_t* __restrict__ item_group, const uint32_t* __restrict__ inv,
+                               uint64_t n, uint32_t* __restrict__ out) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < n;
+         c += (uint64_t)gridDim.x * blockDim.x)
+        out[c] = inv[item_group[c]];
+}
+
+void free_variants(pm4g_variant_table* v) {
+    if (!v) return;
+    cudaStream_t s = v->stream;
+    dfree(v->count, s);
+    dfree(v->len, s);
+    dfree(v->rep_case, s);
+    dfree(v->seq_off, s);
+    dfree(v->seq_act, s);
+    dfree(v->k1, s);
+    dfree(v->k2, s);
+    dfree(v->case_variant, s);
+    delete v;
+}
+
+template <class OFF, class ACT>
+static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const uint64_t* k2,
+                                  const OFF* off, const ACT* acts, const uint64_t* weight,
+                                  const uint32_t* order, int order_bits, const uint32_t* rep_code,
+                                  bool with_case_variant, cudaStream_t s, pm4g_variant_table** out) {
+    Groups g;
+    PM4G_TRY((group_items<OFF, ACT>(n_items, k1, k2, off, acts, weight, order, order_bits, s, &g)));
+    pm4g_variant_table* v = new pm4g_variant_table();
+    v->stream = s;
+    v->V = g.G;
+    v->n_cases = with_case_variant ? n_items : 0;
+    auto bail = [&](pm4g_status st) {
+        g.free(s);
+        free_variants(v);
+        return st;
+    };
+    pm4g_status st;
+    const uint64_t V1 = std::max<uint64_t>(g.G, 1);
+    if ((st = dalloc_t(&v->count, V1, s))) return bail(st);
+    if ((st = dalloc_t(&v->len, V1, s))) return bail(st);
+    if ((st = dalloc_t(&v->rep_case, V1, s))) return bail(st);
+    if ((st = dalloc_t(&v->seq_off, V1 + 1, s))) return bail(st);
+    if ((st = dalloc_t(&v->k1, V1, s))) return bail(st);
+    if ((st = dalloc_t(&v->k2, V1, s))) return bail(st);
+    if (g.G) {
+        PM4G_LAUNCH("k_variant_emit", g.G * 40.0, s,
+                    (k_emit<OFF><<<gsz(g.G), 256, 0, s>>>(g, off, rep_code, k1, k2, v->count, v->len,
+                                                          v->rep_case, v->k1, v->k2)));
+    }
+    if ((st = excl_scan_u32_to_u64(v->len, v->seq_off, (int64_t)g.G, s))) return bail(st);
+    uint64_t total = 0;
+    if (cudaMemcpyAsync(&total, v->seq_off + g.G, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(cuda_fail(cudaGetLastError(), "variant total length"));
+    v->total_len = total;
+    if ((st = dalloc_t(&v->seq_act, std::max<uint64_t>(total, 1), s))) return bail(st);
+    if (g.G) {
+        int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>((g.G * 32 + 255) / 256, (uint64_t)num_sms() * 8));
+        PM4G_LAUNCH("k_variant_seq", (double)total * 8.0, s,
+                    (k_seq_gather<OFF, ACT><<<gs, 256, 0, s>>>(g, off, acts, v->seq_off, v->seq_act)));
+    }
+    if (with_case_variant) {
+        if ((st = dalloc_t(&v->case_variant, std::max<uint64_t>(n_items, 1), s))) return bail(st);
+        if (n_items)
+            PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
+                        (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items,
+                                                                    v->case_variant)));
+    }
+    g.free(s);
+    *out = v;
+    return PM4G_OK;
+}
+
+pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint64_t* k2,
+                               cudaStream_t s, pm4g_variant_table** out) {
+    PM4G_TRY(fetch_n_cases(L, s));
+    const uint64_t C = (uint64_t)L->n_cases;
+    int order_bits = bit_width_u64(C);
+    switch (L->act_bytes) {
+        case 1: return build_variants<uint32_t, uint8_t>(C, k1, k2, L->off, (const uint8_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
+        case 2: return build_variants<uint32_t, uint16_t>(C, k1, k2, L->off, (const uint16_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
+        default: return build_variants<uint32_t, uint32_t>(C, k1, k2, L->off, (const uint32_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
+    }
+}
+
+// Merge R per-shard tables (disjoint case ranges): items = entries.
+pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
+                                 pm4g_variant_table** out) {
+    uint64_t V = 0, T = 0;
+    for (int r = 0; r < n_parts; ++r) {
+        V += parts[r]->V;
+        T += parts[r]->total_len;
+    }
+    Scratch buf(s);
+    // k1 k2 weight (u64) | order len (u32) | seq_off (u64, V+1) | seq_act (u32, T)
+    PM4G_TRY(buf.alloc((V + 1) * 8 * 4 + (V + 1) * 4 * 2 + (T + 1) * 4));
+    uint64_t* k1 = buf.as<uint64_t>();
+    uint64_t* k2 = k1 + V + 1;
+    uint64_t* w = k2 + V + 1;
+    uint64_t* so = w + V + 1;
+    uint32_t* ord = (uint32_t*)(so + V + 1);
+    uint32_t* ln = ord + V + 1;
+    uint32_t* sa = ln + V + 1;
+    uint64_t vo = 0, to = 0;
+    for (int r = 0; r < n_parts; ++r) {
+        const pm4g_variant_table* p = parts[r];
+        if (!p->V) continue;
+        PM4G_CK(cudaMemcpyAsync(k1 + vo, p->k1, p->V * 8, cudaMemcpyDeviceToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(k2 + vo, p->k2, p->V * 8, cudaMemcpyDeviceToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(w + vo, p->count, p->V * 8, cudaMemcpyDeviceToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(ord + vo, p->rep_case, p->V * 4, cudaMemcpyDeviceToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(ln + vo, p->len, p->V * 4, cudaMemcpyDeviceToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(sa + to, p->seq_act, p->total_len * 4, cudaMemcpyDeviceToDevice, s));
+        vo += p->V;
+        to += p->total_len;
+    }
+    PM4G_TRY(excl_scan_u32_to_u64(ln, so, (int64_t)V, s));
+    return build_variants<uint64_t, uint32_t>(V, k1, k2, so, sa, w, ord, 32, ord, false, s, out);
+}
+
+}  // namespace pm4g
+
+using namespace pm4g;
+
+extern "C" {
+
+pm4g_status pm4g_variants_size(const pm4g_variant_table* v, uint64_t* n_variants, uint64_t* total_len) {
+    if (!v) return fail(PM4G_EINVAL, "null variants");
+    if (n_variants) *n_variants = v->V;
+    if (total_len) *total_len = v->total_len;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_variants_get(const pm4g_variant_table* v, uint64_t* count, uint32_t* len,
+                              uint32_t* rep_case, uint64_t* seq_off, uint32_t* seq_act,
+                              pm4g_stream_t stream) {
+    if (!v) return fail(PM4G_EINVAL, "null variants");
+    cudaStream_t s = (cudaStream_t)stream;
+    auto cp = [&](void* dst, const void* src, size_t b) -> pm4g_status {
+        if (dst && b) PM4G_CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, s));
+        return PM4G_OK;
+    };
+    PM4G_TRY(cp(count, v->count, v->V * 8));
+    PM4G_TRY(cp(len, v->len, v->V * 4));
+    PM4G_TRY(cp(rep_case, v->rep_case, v->V * 4));
+    PM4G_TRY(cp(seq_off, v->seq_off, (v->V + 1) * 8));
+    PM4G_TRY(cp(seq_act, v->seq_act, v->total_len * 4));
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_variants_case_index(const pm4g_variant_table* v, uint32_t* case_variant,
+                                     pm4g_stream_t stream) {
+    if (!v || !case_variant) return fail(PM4G_EINVAL, "null argument");
+    if (!v->case_variant) return fail(PM4G_EINVAL, "merged tables carry no per-case index");
+    if (v->n_cases)
+        PM4G_CK(cudaMemcpyAsync(case_variant, v->case_variant, v->n_cases * 4,
+                                cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_variants_destroy(pm4g_variant_table* v) {
+    free_variants(v);
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts,
+                                pm4g_stream_t stream, pm4g_variant_table** out) {
+    if (!parts || n_parts <= 0 || !out) return fail(PM4G_EINVAL, "bad arguments");
+    for (int i = 0; i < n_parts; ++i)
+        if (!parts[i]) return fail(PM4G_EINVAL, "null part");
+    *out = nullptr;
+    return merge_variant_tables(parts, n_parts, (cudaStream_t)stream, out);
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+"""GPU filters vs the oracle (P:126 time filters, P:96-101/P:128 attribute filters)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen.synth import CONFIGS, generate
+from gen.tinylogs import random_log
+from tests.parity import assert_parity, collect, to_device_cols
+from paper_2204_04898_b200 import pm4g
+
+pytestmark = pytest.mark.gpu
+
+
+def _log(case, act, ts, A, ncodes, extra=None, sort_first=False):
+    c, a, t = to_device_cols(case, act, ts, A)
+    log = pm4g.pm4g_log_create(c, a, t, A, n_case_codes=ncodes, extra=extra)
+    if sort_first:
+        log.sort()
+    return log
+
+
+def _expect(case, act, ts, A, keep):
+    keep = np.asarray(keep, dtype=bool)
+    sub = lambda x: np.asarray(x, dtype=np.int64)[keep]  # noqa: E731
+    return oracle.run(sub(case), sub(act), sub(ts), A)
+
+
+def _check(out_log, r):
+    out_log.sort()
+    assert_parity(collect(out_log), r)
+
+
+@pytest.mark.parametrize("sort_first", [False, True])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_time_filter_l1(l1, mode, sort_first):
+    rows = l1["rows_ingest_order"]
+    case, act, ts = rows["case"], rows["act"], rows["ts"]
+    t1, t2 = {0: (0, 15), 1: (0, 20), 2: (90, 200)}[mode]
+    log = _log(case, act, ts, 3, 3, sort_first=sort_first)
+    out = log.filter_time(t1, t2, mode)
+    keep = oracle.filter_time(case, ts, t1, t2, mode)
+    _check(out, _expect(case, act, ts, 3, keep))
+    ex = l1["expected"]
+    if mode == 0:
+        sc, sa, st = out.sorted_columns()
+        got = [[int(x), int(y), int(z)] for x, y, z in zip(sc.cpu(), sa.cpu(), st.cpu())]
+        assert got == ex["filter_events_0_15"]["value"]
+
+
+@pytest.mark.parametrize("sort_first", [False, True])
+@pytest.mark.parametrize("seed", range(0, 60, 3))
+def test_time_filters_random(seed, sort_first):
+    case, act, ts, A, ncodes = random_log(seed)
+    if not case:
+        return
+    lo, hi = min(ts), max(ts)
+    t1, t2 = lo + (hi - lo) // 5, lo + 4 * (hi - lo) // 5
+    for mode in (0, 1, 2):
+        log = _log(case, act, ts, A, ncodes, sort_first=sort_first)
+        out = log.filter_time(t1, t2, mode)
+        keep = oracle.filter_time(case, ts, t1, t2, mode)
+        _check(out, _expect(case, act, ts, A, keep))
+
+
+def test_time_filter_rejects_bad_range():
+    log = _log([0, 1], [0, 0], [1, 2], 1, 2)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        log.filter_time(5, 1)
+    assert e.value.status == pm4g.PM4G_EINVAL
+
+
+def test_filter_removing_everything_and_keeping_everything():
+    L = generate(CONFIGS["tiny"])
+    case, act, ts = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    log = _log(case, act, ts, L.n_activities, L.n_case_codes)
+    none = log.filter_time(0, 1)
+    assert none.n == 0
+    none.sort()
+    cnt, _, _ = none.dfg()
+    assert int(cnt.sum()) == 0
+    allr = log.filter_time(int(ts.min()), int(ts.max()))
+    _check(allr, oracle.run(case, act, ts, L.n_activities))
+
+
+@pytest.mark.parametrize("sort_first", [False, True])
+@pytest.mark.parametrize("level", [0, 1])
+@pytest.mark.parametrize("keep", [True, False])
+def test_activity_filter(level, keep, sort_first):
+    L = generate(CONFIGS["tiny"])
+    case, act, ts = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    log = _log(case, act, ts, L.n_activities, L.n_case_codes, sort_first=sort_first)
+    out = log.filter_attr(pm4g.PM4G_COL_ACTIVITY, codes=[1, 4, 7], level=level, keep=keep)
+    k = oracle.filter_attr(case, act, codes=[1, 4, 7], level=level, keep=keep)
+    _check(out, _expect(case, act, ts, L.n_activities, k))
+
+
+def test_activity_filter_l1_cases(l1):
+    rows = l1["rows_ingest_order"]
+    log = _log(rows["case"], rows["act"], rows["ts"], 3, 3)
+    out = log.filter_attr(pm4g.PM4G_COL_ACTIVITY, codes=[1], level=pm4g.PM4G_LEVEL_CASES)
+    out.sort()
+    cc, _, _ = out.case_durations()
+    assert cc.cpu().tolist() == l1["expected"]["filter_attr_act_B_cases"]["value"]
+
+
+@pytest.mark.parametrize("sort_first", [False, True])
+@pytest.mark.parametrize("level", [0, 1])
+def test_extra_columns_with_nulls(level, sort_first):
+    L = generate(CONFIGS["tiny"])
+    case, act, ts = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    n = case.size
+    rng = np.random.default_rng(5)
+    res = rng.integers(0, 50, n).astype(np.int64)         # resource codes
+    cost = rng.integers(0, 2000, n).astype(np.int64)      # numeric i64
+    amt = rng.random(n) * 100.0                           # numeric f64
+    valid = (rng.random(n) > 0.1).astype(np.uint8)
+    dev = "cuda"
+    extra = [pm4g.Extra(pm4g.PM4G_KIND_CODES, torch.as_tensor(res).to(torch.int32).to(dev), None, 50),
+             pm4g.Extra(pm4g.PM4G_KIND_I64, torch.as_tensor(cost).to(dev), torch.as_tensor(valid).to(dev)),
+             pm4g.Extra(pm4g.PM4G_KIND_F64, torch.as_tensor(amt).to(dev), None)]
+    log = _log(case, act, ts, L.n_activities, L.n_case_codes, extra=extra, sort_first=sort_first)
+    # cost > 1000 (P:96 example) with nulls that never match
+    out = log.filter_attr(1, lo=1001, hi=2**62, level=level)
+    k = oracle.filter_attr(case, cost, lo=1001, hi=2**62, valid=valid, level=level)
+    _check(out, _expect(case, act, ts, L.n_activities, k))
+    out = log.filter_attr(0, codes=[3, 9, 11], level=level, keep=False)
+    k = oracle.filter_attr(case, res, codes=[3, 9, 11], level=level, keep=False)
+    _check(out, _expect(case, act, ts, L.n_activities, k))
+    out = log.filter_attr(2, lo=10.0, hi=55.5, level=level)
+    k = oracle.filter_attr(case, amt, lo=10.0, hi=55.5, level=level)
+    _check(out, _expect(case, act, ts, L.n_activities, k))
+    # chained: attribute filter on the filtered log (extra columns travel with rows)
+    out2 = log.filter_attr(1, lo=0, hi=1500, level=0).filter_attr(0, codes=list(range(25)), level=level)
+    k1 = oracle.filter_attr(case, cost, lo=0, hi=1500, valid=valid, level=0)
+    sub = lambda x: np.asarray(x)[k1]  # noqa: E731
+    k2 = oracle.filter_attr(sub(case), sub(res), codes=list(range(25)), level=level)
+    r = oracle.run(sub(case)[k2], sub(act)[k2], sub(ts)[k2], L.n_activities)
+    _check(out2, r)
+
+
+def test_kind_mismatch_rejected():
+    L = generate(CONFIGS["tiny"])
+    case, act, ts = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    extra = [pm4g.Extra(pm4g.PM4G_KIND_I64, torch.zeros(case.size, dtype=torch.int64, device="cuda"))]
+    log = _log(case, act, ts, L.n_activities, L.n_case_codes, extra=extra)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        log.filter_attr(0, codes=[1])
+    assert e.value.status == pm4g.PM4G_EINVAL
+    with pytest.raises(pm4g.Pm4gError):
+        log.filter_attr(5, codes=[1])
+
+
+def test_contained_subset_of_intersecting():
+    """S:486 / S:619 law on the GPU outputs."""
+    L = generate(CONFIGS["tiny"])
+    case, act, ts = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    log = _log(case, act, ts, L.n_activities, L.n_case_codes)
+    lo, hi = int(ts.min()), int(ts.max())
+    for j in range(4):
+        t1 = lo + (hi - lo) * j // 8
+        t2 = t1 + (hi - lo) // 2
+        a = log.filter_time(t1, t2, 1).sort()
+        b = log.filter_time(t1, t2, 2).sort()
+        ca = set(a.case_durations()[0].cpu().tolist())
+        cb = set(b.case_durations()[0].cpu().tolist())
+        assert ca <= cb

@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle O1, element by element.
+
+Integer outputs bit-exact; fp64 means within 1e-12 relative (north_star).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen.synth import CONFIGS, generate
+from gen.tinylogs import random_log
+from tests.parity import assert_parity, check_log, gpu_run, to_device_cols
+from paper_2204_04898_b200 import pm4g
+
+pytestmark = pytest.mark.gpu
+
+
+def _l1(l1):
+    r = l1["rows_ingest_order"]
+    return r["case"], r["act"], r["ts"], l1["n_activities"]
+
+
+def test_l1_fixture(l1):
+    g, r = check_log(*_l1(l1))
+    ex = l1["expected"]
+    assert g["dur"].tolist() == ex["throughput_ms"]["value"]
+    assert g["cnt"][0, 1] == 2 and g["cnt"][1, 2] == 2 and g["cnt"][0, 2] == 1
+
+
+def test_l1_separate_calls(l1):
+    case, act, ts, A = _l1(l1)
+    g = gpu_run(case, act, ts, A, fused=False)
+    assert_parity(g, oracle.run(case, act, ts, A))
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_tiny_logs(seed):
+    case, act, ts, A, ncodes = random_log(seed)
+    check_log(case, act, ts, A, n_case_codes=ncodes)
+
+
+@pytest.mark.parametrize("name", ["tiny", "roadtraffic", "bpic2019"])
+def test_configs_full_size(name):
+    L = generate(CONFIGS[name])
+    g, r = check_log(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities,
+                     n_case_codes=L.n_case_codes)
+    if name == "roadtraffic":
+        assert len(r.v_count) == 231 and g["v_count"].size == 231
+    if name == "bpic2019":
+        assert g["v_count"].size == 11_973
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_log():
+    g = gpu_run([], [], [], 4, n_case_codes=1)
+    assert g["cnt"].sum() == 0 and g["v_count"].size == 0 and g["case_code"].size == 0
+
+
+def test_single_event():
+    check_log([3], [1], [42], 2, n_case_codes=4)
+
+
+def test_one_case_many_events():
+    rng = np.random.default_rng(0)
+    n = 20000
+    check_log([7] * n, rng.integers(0, 5, n).tolist(), rng.integers(0, 1000, n).tolist(), 5)
+
+
+def test_all_same_activity_and_timestamp():
+    rng = np.random.default_rng(1)
+    n = 9000
+    case = rng.integers(0, 300, n)
+    check_log(case.tolist(), [0] * n, [5] * n, 1)
+
+
+@pytest.mark.parametrize("A", [1, 2, 255, 256, 257, 1000])
+def test_activity_widths(A):
+    rng = np.random.default_rng(A)
+    n = 30000
+    case = rng.integers(0, 2000, n)
+    act = rng.integers(0, A, n)
+    ts = rng.integers(-10**9, 10**9, n)
+    check_log(case.tolist(), act.tolist(), ts.tolist(), A)
+
+
+@pytest.mark.parametrize("n", [4095, 4096, 4097, 8191, 8193, 3 * 4096 + 1, 65537])
+def test_ragged_tiles(n):
+    rng = np.random.default_rng(n)
+    case = rng.integers(0, max(1, n // 7), n)
+    act = rng.integers(0, 9, n)
+    ts = rng.integers(0, 10**6, n)
+    check_log(case.tolist(), act.tolist(), ts.tolist(), 9)
+
+
+def test_max_case_code_and_sparse_codes():
+    codes = np.array([0, 5, 2**32 - 2, 2**31, 77], dtype=np.int64)
+    rng = np.random.default_rng(3)
+    case = rng.choice(codes, 5000)
+    act = rng.integers(0, 4, 5000)
+    ts = rng.integers(0, 10**9, 5000)
+    check_log(case.tolist(), act.tolist(), ts.tolist(), 4, n_case_codes=2**32 - 1)
+
+
+def test_extreme_timestamps_wide_span():
+    """ts span near 2^63 with a single case code: key = 63-64 ts bits, 0 case bits."""
+    ts = [-(2**62), 2**62, 0, 5, -5, 2**62 - 1]
+    check_log([1] * 6, [0, 1, 0, 1, 0, 1], ts, 2)
+
+
+def test_key_too_wide_is_reported():
+    """case_bits + ts_bits > 64 -> PM4G_EKEYWIDTH (wide-key path is future work)."""
+    c, a, t = to_device_cols([0, 2**31, 5], [0, 0, 0], [-(2**62), 2**62, 0], 1)
+    log = pm4g.pm4g_log_create(c, a, t, 1, n_case_codes=2**32 - 1)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        log.sort()
+    assert e.value.status == pm4g.PM4G_EKEYWIDTH
+
+
+def test_validation_errors():
+    c, a, t = to_device_cols([0, 1, 9], [0, 1, 0], [1, 2, 3], 2)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        pm4g.pm4g_log_create(c, a, t, 2, n_case_codes=5)          # case 9 >= 5
+    assert e.value.status == pm4g.PM4G_EDATA and "row 2" in str(e.value)
+    c, a, t = to_device_cols([0, 1, 2], [0, 3, 0], [1, 2, 3], 4)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        pm4g.pm4g_log_create(c, a, t, 3, n_case_codes=5)          # act 3 >= 3
+    assert e.value.status == pm4g.PM4G_EDATA
+
+
+def test_unsorted_log_rejected_by_aggregates():
+    c, a, t = to_device_cols([0, 1], [0, 1], [1, 2], 2)
+    log = pm4g.pm4g_log_create(c, a, t, 2)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        log.dfg()
+    assert e.value.status == pm4g.PM4G_EINVAL
+
+
+def test_host_input_path(l1):
+    """PM4G_HOST_INPUT: columns in host memory are copied inside the call."""
+    case, act, ts, A = _l1(l1)
+    c, a, t = to_device_cols(case, act, ts, A, device=None)
+    log = pm4g.pm4g_log_create(c.pin_memory(), a.pin_memory(), t.pin_memory(), A, n_case_codes=3)
+    log.sort()
+    cnt, sm, mean = log.dfg()
+    assert cnt.cpu().numpy()[0, 1] == 2 and sm.cpu().numpy()[1, 2] == 60
+
+
+def test_sort_idempotent_and_deterministic():
+    L = generate(CONFIGS["tiny"])
+    c, a, t = to_device_cols(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities)
+    outs = []
+    for _ in range(3):
+        log = pm4g.pm4g_log_create(c, a, t, L.n_activities, n_case_codes=L.n_case_codes)
+        log.sort()
+        log.sort()
+        from tests.parity import collect
+        outs.append(collect(log))
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]) and np.array_equal(outs[0][k], outs[2][k]), k
+
+
+def test_weak_hash_collisions_resolved_exactly(monkeypatch):
+    """PM4G_DEBUG_WEAK_HASH=1 reduces the variant key to 4 bits: every bucket collides,
+    the verify-and-rekey rounds must still give the exact variant multiset."""
+    monkeypatch.setenv("PM4G_DEBUG_WEAK_HASH", "1")
+    L = generate(CONFIGS["tiny"])
+    check_log(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities, n_case_codes=L.n_case_codes)
+    case, act, ts, A, ncodes = random_log(11)
+    check_log(case, act, ts, A, n_case_codes=ncodes)
