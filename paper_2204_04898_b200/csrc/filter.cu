@@ -246,7 +246,7 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
     if (n > 0) {
         const int64_t tiles = (n + CMP_TILE - 1) / CMP_TILE;
         Scratch stt(s);
-        if ((st = stt.alloc((tiles + 1) * 4 + 8))) return bail(st);
+        if ((st = stt.alloc((tiles + 1) * 4 + 16))) return bail(st);
         uint32_t* status = stt.as<uint32_t>();
         uint64_t* d_kept = (uint64_t*)(((uintptr_t)(status + tiles + 1) + 7) & ~(uintptr_t)7);
         if (cudaMemsetAsync(stt.p, 0, (tiles + 1) * 4, s) != cudaSuccess)

@@ -258,9 +258,10 @@ static pm4g_status lsd_sort(const uint32_t* cs, const int64_t* ts, const uint64_
     // ping-pong so that the last pass lands in the output buffers
     const size_t per = (size_t)n * (8 + sizeof(P) + (WI ? 4 : 0));
     PM4G_TRY(tmp.alloc(per));
+    // layout keeps every array naturally aligned: keys (8n) | idx (4n) | act
     uint64_t* tkey = tmp.as<uint64_t>();
-    P* tact = (P*)((char*)tmp.p + (size_t)n * 8);
-    uint32_t* tidx = (uint32_t*)((char*)tmp.p + (size_t)n * (8 + sizeof(P)));
+    uint32_t* tidx = (uint32_t*)((char*)tmp.p + (size_t)n * 8);
+    P* tact = (P*)((char*)tmp.p + (size_t)n * (8 + (WI ? 4 : 0)));
     const uint64_t* ck = keys_in;
     const P* ca = act_in;
     const uint32_t* ci = idx_in;

@@ -571,7 +571,8 @@ pm4g_status pm4g_variants_get(const pm4g_variant_table* v, uint64_t* count, uint
 
 pm4g_status pm4g_variants_case_index(const pm4g_variant_table* v, uint32_t* case_variant,
                                      pm4g_stream_t stream) {
-    if (!v || !case_variant) return fail(PM4G_EINVAL, "null argument");
+    if (!v) return fail(PM4G_EINVAL, "null variants");
+    if (v->n_cases && !case_variant) return fail(PM4G_EINVAL, "null output");
     if (!v->case_variant) return fail(PM4G_EINVAL, "merged tables carry no per-case index");
     if (v->n_cases)
         PM4G_CK(cudaMemcpyAsync(case_variant, v->case_variant, v->n_cases * 4,
