@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- events/s of the PM4Py-GPU hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 100M] [--impl pm4g|reference]
+
+One step = one pass of the hot path over one batch (the config's log shard):
+  A0 pm4g_log_create (validate + metadata, columns borrowed in HBM)
+  [A1 events-mode time filter, only with --filter]
+  A2-A4 pm4g_sort (composite key, onesweep LSD radix sort, case segments)
+  A5-A9 pm4g_analyze (fused DFG + start/end + case durations + variant keys,
+        then the variant group-count / verify / order)
+  A11 with N > 1: NCCL allreduce of the tables + allgather/merge of variants.
+Default workload: BASELINE.json configs[3], the synthetic 100M-event log
+(10M cases, 64 activities, fully shuffled rows -> full radix sort), one such
+shard per GPU (weak scaling: rank r holds case codes [r*10M, (r+1)*10M) of a
+global log of N*100M events).  Inputs (1.3 GB/GPU) are larger than L2.
+
+Rank 0 prints ONE JSON line.  `value` = total input events of all ranks / max
+over ranks of the device time of the K timed steps.  `e2e` = the same metric
+through the C-ABI with HOST input buffers (pinned; H2D inside the call) and a
+D2H read of every result.  `roofline` = the dominant kernel (k_onesweep, the
+radix scatter pass) -- algorithmic bytes / CUDA-event time of its launches in
+the timed region, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the
+oracle (single-threaded C++) on a bounded sample of the same workload.
+`--impl reference` times the oracle alone (the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+METRIC = "events/sec for sort+DFG+variants at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [x for x in sm if mx and x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def make_shard(cfg: str, rank: int, world: int, device):
+    from gen.synth import CONFIGS
+    from gen.synth import generate
+    base = CONFIGS[cfg]
+    spec = base.with_(n_cases=base.n_cases * world,
+                      n_events=None if base.n_events is None else base.n_events * world)
+    lo = rank * base.n_cases
+    L = generate(spec, lo, lo + base.n_cases, device=device)
+    case = L.case.to(torch.uint32)
+    act = L.act.to(L.act_dtype()) if L.act_dtype() != torch.uint8 else L.act.to(torch.uint8)
+    ts = L.ts.contiguous()
+    meta = dict(n_case_codes=L.n_case_codes, case_lo=lo, case_hi=lo + base.n_cases, A=L.n_activities)
+    del L
+    return case.contiguous(), act.contiguous(), ts, meta, spec
+
+
+def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None):
+    tick = (lambda nm: trace.append((nm, time.perf_counter()))) if trace is not None else (lambda nm: None)
+    tick("start")
+    log = pm4g.pm4g_log_create(case, act, ts, meta["A"], n_case_codes=meta["n_case_codes"],
+                               case_lo=meta["case_lo"], case_hi=meta["case_hi"], borrow=not host)
+    tick("log_create")
+    if filt is not None:
+        f = log.filter_time(filt[0], filt[1], pm4g.PM4G_TIME_EVENTS)
+        log.close()
+        log = f
+        tick("filter_time")
+    log.sort()
+    tick("sort (async)")
+    res = log.analyze(comm=comm, out=out)
+    tick("analyze")
+    v = res["variants"]
+    log.close()
+    tick("close")
+    return res, v
+
+
+def cpu_baseline(cfg, cases: int, device):
+    """O1 on a bounded sample (the first `cases` cases of the workload), 1 core."""
+    import oracle
+    from gen.synth import CONFIGS, generate
+    spec = CONFIGS[cfg]
+    L = generate(spec, 0, min(cases, spec.n_cases), device=device)
+    c, a, t = L.case.cpu().numpy(), L.act.cpu().numpy(), L.ts.cpu().numpy()
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.run(c, a, t, spec.n_activities)
+    dt = time.perf_counter() - t0
+    return {"value": c.size / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {min(cases, spec.n_cases):,} cases ({c.size:,} events) of the {cfg} "
+                      f"workload; single-threaded O1 (stable sort + loop), {dt:.2f} s"}
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from gen.synth import CONFIGS, generate
+    spec = CONFIGS[args.config]
+    cases = args.ref_cases
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    L = generate(spec, 0, min(cases, spec.n_cases), device=dev)
+    c, a, t = L.case.cpu().numpy(), L.act.cpu().numpy(), L.ts.cpu().numpy()
+    oracle.build()
+    for _ in range(args.warmup):
+        oracle.run(c, a, t, spec.n_activities)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.run(c, a, t, spec.n_activities)
+    dt = time.perf_counter() - t0
+    v = c.size * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": f"synthetic-{args.config} (sample)", "events_per_step": int(c.size)},
+            "cpu_baseline": {"value": v, "unit": "events/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {min(cases, spec.n_cases):,} cases ({c.size:,} events) of "
+                                       f"the {args.config} workload per step; single-threaded O1"},
+            "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="100M")
+    ap.add_argument("--impl", default="pm4g", choices=["pm4g", "reference"])
+    ap.add_argument("--filter", action="store_true", help="events-mode time filter in the step (1B-style)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-cases", type=int, default=1_000_000)
+    ap.add_argument("--ref-cases", type=int, default=50_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stages", action="store_true", help="print the per-kernel table to stderr")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2204_04898_b200 import pm4g
+    comm = None
+    if world > 1:
+        uid = [pm4g.pm4g_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = pm4g.pm4g_comm_create(uid[0], world, rank)
+
+    case, act, ts, meta, spec = make_shard(args.config, rank, world, dev)
+    n_local = int(case.numel())
+    filt = None
+    if args.filter:
+        from gen.synth import T0_MS
+        filt = (T0_MS + int(36.5 * 86_400_000), T0_MS + int(328.5 * 86_400_000))
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    out = {}
+    for _ in range(args.warmup):
+        _, v = run_step(pm4g, case, act, ts, meta, comm, out, filt)
+        v.close()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device time, CUDA events on the launching stream)
+    clocks = Clocks(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.2)
+    pm4g.pm4g_prof_reset()
+    pm4g.pm4g_prof_enable(True)
+    l0 = pm4g.pm4g_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    trace = []
+    for i in range(args.steps):
+        _, v = run_step(pm4g, case, act, ts, meta, comm, out, filt,
+                        trace=trace if (args.stages and i == args.steps - 1) else None)
+        v.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = pm4g.pm4g_launch_count() - l0
+    pm4g.pm4g_prof_enable(False)
+    prof = pm4g.pm4g_prof_collect()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    n_total = n_local * world
+    value = n_total * args.steps / (ms / 1e3)
+
+    # ---------------- end to end through the C-ABI with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        hc, ha, ht = case.cpu().pin_memory(), act.cpu().pin_memory(), ts.cpu().pin_memory()
+        torch.cuda.synchronize()
+        d2h = 0
+        hosts = {}
+
+        def e2e_step():
+            nonlocal d2h
+            res, v = run_step(pm4g, hc, ha, ht, meta, comm, out, filt, host=True)
+            tabs = v.get()
+            d2h = 0
+            for k in ("cnt", "dur_sum", "mean", "start", "end", "case_code", "n_events", "dur"):
+                x = res[k]
+                if k not in hosts or hosts[k].numel() != x.numel():
+                    hosts[k] = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                hosts[k].copy_(x, non_blocking=True)
+                d2h += x.numel() * x.element_size()
+            for k, x in tabs.items():
+                hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                hx.copy_(x, non_blocking=True)
+                d2h += x.numel() * x.element_size()
+            v.close()
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if dist:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": n_total * args.e2e_steps / (ems / 1e3), "unit": "events/s",
+               "h2d_bytes_per_step": n_local * (4 + act.element_size() + 8), "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / args.e2e_steps}
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = _peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roof = None
+    if "k_onesweep" in prof:
+        la, kms, kbytes = prof["k_onesweep"]
+        achieved = kbytes / (kms / 1e3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                tj = json.load(open(tf))
+                ent = tj.get("k_onesweep")
+                if ent and ent.get("config") == args.config:
+                    traffic = ent["dram_bytes_per_launch"]
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": "k_onesweep", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": kbytes / la, "launches": la,
+                "avg_launch_ms": kms / la, "share_of_step": round(kms / ms, 4), "peak_source": peak_src}
+    step_bytes = sum(b for (_, _, b) in prof.values())
+    stages = {k: {"launches": la, "ms": round(m, 3), "GB/s": round(b / (m / 1e3) / 1e9, 1) if m > 0 else None}
+              for k, (la, m, b) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    if args.stages and rank == 0:
+        for k, s in stages.items():
+            print(f"{k:28s} {s}", file=sys.stderr)
+        if trace:
+            print("host trace of the last step (ms since step start):", file=sys.stderr)
+            for nm, tt in trace:
+                print(f"  {1e3 * (tt - trace[0][1]):9.3f}  {nm}", file=sys.stderr)
+        recs = pm4g.pm4g_prof_records()
+        per = len(recs) // max(1, args.steps)
+        last = recs[-per:] if per else []
+        if last:
+            t00, prev_end = last[0][1], last[0][1]
+            print("timeline of the last timed step (start ms, gap before, duration ms):", file=sys.stderr)
+            for nm, t0, d in last:
+                print(f"  {t0 - t00:9.3f} gap {t0 - prev_end:8.3f}  {d:8.3f}  {nm}", file=sys.stderr)
+                prev_end = t0 + d
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.cpu_cases, dev)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"synthetic-{args.config}: {n_local:,} events / {meta['case_hi'] - meta['case_lo']:,} "
+                                   f"cases / {meta['A']} activities per GPU, fully shuffled rows (full radix sort)"
+                                   + (", events-mode time filter" if filt else ""),
+                       "events_per_gpu": n_local, "global_events": n_total, "parallelism": f"case-sharded x{world}",
+                       "l2": "inputs (13 B/event) larger than L2; no flush needed",
+                       "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")},
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "cpu_baseline": cpu,
+            "hbm_pipeline": {"algorithmic_GB_per_step": step_bytes / args.steps / 1e9,
+                             "achieved_GB_per_s": step_bytes / (ms / 1e3) / 1e9,
+                             "frac_of_peak": step_bytes / (ms / 1e3) / 1e9 / peak},
+            "stages": stages,
+        }
+        print(json.dumps(line))
+    if comm is not None:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -282,6 +282,10 @@ pm4g_status pm4g_prof_reset(void);
 pm4g_status pm4g_prof_collect(int32_t* n_names);
 pm4g_status pm4g_prof_entry(int32_t i, const char** name, uint64_t* launches, double* total_ms,
                             double* bytes);
+/* The individual launches of the last collect, in launch order: start time
+ * relative to the first recorded launch and duration (ms). */
+int32_t pm4g_prof_n_records(void);
+pm4g_status pm4g_prof_record(int32_t i, const char** name, double* start_ms, double* dur_ms);
 
 #ifdef __cplusplus
 }

@@ -57,57 +57,85 @@ __device__ __forceinline__ void finish_key(uint64_t h1, uint64_t h2, uint32_t le
     k2 = fmix64(h2 + (uint64_t)len * 0xff51afd7ed558ccdull);
 }
 
+constexpr uint32_t AGG_STAGE = 4096;   // events of a case tile staged in smem
+
 template <class P, bool SMEM>
 __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A,
     uint64_t* __restrict__ packed, uint32_t* __restrict__ n_events, int64_t* __restrict__ dur,
     uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
+    const bool tables = packed != nullptr;
     const uint32_t AA = A * A;
+    const uint32_t tab_words = (SMEM && tables) ? 3 * AA + 2 * A : 0;
     uint32_t* s_cnt = sm;
     uint32_t* s_lo = sm + AA;
     uint32_t* s_hi = sm + 2 * AA;
     uint32_t* s_st = sm + 3 * AA;
     uint32_t* s_en = s_st + A;
-    const bool tables = packed != nullptr;
+    uint32_t* s_off = sm + tab_words;                       // [AGG_CASES + 1]
+    P* s_act = (P*)(s_off + AGG_CASES + 4);                 // [AGG_STAGE]
     uint64_t* g_cnt = packed;
     uint64_t* g_sum = packed + AA;
     uint64_t* g_st = packed + 2 * (size_t)AA;
     uint64_t* g_en = g_st + A;
-    if (SMEM && tables) {
-        for (uint32_t i = threadIdx.x; i < 3 * AA + 2 * A; i += AGG_THREADS) sm[i] = 0;
-        __syncthreads();
-    }
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = threadIdx.x; i < tab_words; i += AGG_THREADS) sm[i] = 0;
+    __syncthreads();
     const uint64_t C = *d_n_cases;
     const uint64_t tiles = (C + AGG_CASES - 1) / AGG_CASES;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const uint64_t c0 = t * AGG_CASES;
-        const uint64_t c1 = min(c0 + AGG_CASES, C);
+        const uint32_t nc = (uint32_t)min((uint64_t)AGG_CASES, C - c0);
+        for (uint32_t i = threadIdx.x; i <= nc; i += AGG_THREADS) s_off[i] = off[c0 + i];
+        __syncthreads();
+        const uint32_t e0 = s_off[0], e1 = s_off[nc], ne = e1 - e0;
+        const bool staged = ne <= AGG_STAGE;
+        if (staged)
+            for (uint32_t i = threadIdx.x; i < ne; i += AGG_THREADS) s_act[i] = act[e0 + i];
+        __syncthreads();
+        auto A_at = [&](uint32_t i) -> uint32_t { return staged ? (uint32_t)s_act[i - e0] : (uint32_t)act[i]; };
         if (tables) {
-            const uint32_t e0 = off[c0], e1 = off[c1];
-            for (uint32_t i = e0 + threadIdx.x; i + 1 < e1; i += AGG_THREADS) {
-                uint64_t k = key[i], kn = key[i + 1];
-                if (shr64(k, ts_bits) != shr64(kn, ts_bits)) continue;
-                uint32_t e = (uint32_t)act[i] * A + (uint32_t)act[i + 1];
-                uint64_t d = kn - k;
-                if (SMEM) {
-                    atomicAdd(&s_cnt[e], 1u);
-                    uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
-                    uint32_t old = atomicAdd(&s_lo[e], lo);
-                    hi += (old + lo < old) ? 1u : 0u;   // carry out of the low word
-                    if (hi) atomicAdd(&s_hi[e], hi);
-                } else {
-                    atomicAdd((unsigned long long*)&g_cnt[e], 1ull);
-                    atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)d);
+            // directly-follows pairs (i, i+1), 4 independent key loads in flight per thread;
+            // the successor's key comes from the next lane
+            for (uint32_t base = e0; base + 1 < e1; base += 4 * AGG_THREADS) {
+                uint64_t kk[4], kn[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
+                    kk[u] = i < e1 ? key[i] : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
+                    kn[u] = __shfl_down_sync(0xffffffffu, kk[u], 1);
+                    if (lane == 31 && i + 1 < e1) kn[u] = key[i + 1];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
+                    if (i + 1 >= e1 || shr64(kk[u], ts_bits) != shr64(kn[u], ts_bits)) continue;
+                    uint32_t e = A_at(i) * A + A_at(i + 1);
+                    uint64_t d = kn[u] - kk[u];
+                    if (SMEM) {
+                        atomicAdd(&s_cnt[e], 1u);
+                        uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
+                        uint32_t old = atomicAdd(&s_lo[e], lo);
+                        hi += (old + lo < old) ? 1u : 0u;   // carry out of the low word
+                        if (hi) atomicAdd(&s_hi[e], hi);
+                    } else {
+                        atomicAdd((unsigned long long*)&g_cnt[e], 1ull);
+                        atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)d);
+                    }
                 }
             }
         }
-        const uint64_t c = c0 + threadIdx.x;
-        if (c < c1) {
-            const uint32_t f = off[c], l = off[c + 1] - 1;
+        if (threadIdx.x < nc) {
+            const uint64_t c = c0 + threadIdx.x;
+            const uint32_t f = s_off[threadIdx.x], l = s_off[threadIdx.x + 1] - 1;
             if (tables) {
-                uint32_t as = (uint32_t)act[f], ae = (uint32_t)act[l];
+                uint32_t as = A_at(f), ae = A_at(l);
                 if (SMEM) {
                     atomicAdd(&s_st[as], 1u);
                     atomicAdd(&s_en[ae], 1u);
@@ -121,7 +149,7 @@ __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
             if (k1o) {
                 uint64_t h1 = 0, h2 = 0;
                 for (uint32_t i = f; i <= l; ++i) {
-                    uint64_t a = (uint64_t)act[i] + 1;
+                    uint64_t a = (uint64_t)A_at(i) + 1;
                     h1 = h1 * HB1 + a;
                     h2 = h2 * HB2 + a;
                 }
@@ -131,9 +159,9 @@ __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
                 k2o[c] = x2;
             }
         }
+        __syncthreads();
     }
     if (SMEM && tables) {
-        __syncthreads();
         for (uint32_t e = threadIdx.x; e < AA; e += AGG_THREADS) {
             uint32_t cn = s_cnt[e];
             if (cn) {
@@ -152,16 +180,17 @@ __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
 template <class P, bool SMEM>
 static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
-    size_t smem = (SMEM && o.tables) ? ((size_t)3 * A * A + 2 * A) * 4 : 0;
+    size_t smem = ((SMEM && o.tables) ? ((size_t)3 * A * A + 2 * A) * 4 : 0) +
+                  (AGG_CASES + 4) * 4 + (size_t)AGG_STAGE * sizeof(P);
     static bool attr = false;
-    if (SMEM && !attr) {
+    if (!attr) {
         PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)AGG_SMEM_MAX));
+                                     (int)(AGG_SMEM_MAX + (AGG_CASES + 4) * 4 + AGG_STAGE * sizeof(P))));
         attr = true;
     }
     uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     uint64_t tiles = std::max<uint64_t>(1, (cap + AGG_CASES - 1) / AGG_CASES);
-    int per_sm = smem ? std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (smem + 1024))) : 8;
+    int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (smem + 1024)));
     uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case outputs
     double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 +

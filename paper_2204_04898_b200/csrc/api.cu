@@ -45,6 +45,11 @@ struct ProfAgg {
     double ms, bytes;
 };
 static std::vector<ProfAgg> g_prof_aggs;
+struct ProfLine {
+    std::string name;
+    double start_ms, dur_ms;
+};
+static std::vector<ProfLine> g_prof_lines;
 
 static cudaEvent_t get_event() {
     if (!g_event_pool.empty()) {
@@ -99,17 +104,78 @@ static void setup_pool() {
         }
     });
 }
+// Stream-aware block cache over cudaMallocAsync: a freed block is kept and
+// handed back to the next request of the same size class on the same stream
+// (stream order makes the reuse safe).  The hot path allocates the same
+// buffers every call, so after the first call no allocator work remains on
+// the host between kernel launches.
+struct CachedBlock {
+    void* p;
+    cudaStream_t s;
+};
+static std::mutex g_alloc_mu;
+static std::vector<std::pair<size_t, CachedBlock>> g_free_blocks;
+static std::vector<std::pair<void*, size_t>> g_live_blocks;
+static size_t g_cached_bytes = 0;
+static const size_t kCacheCap = 48ull << 30;
+
+static size_t size_class(size_t b) {
+    if (b <= 4096) return 4096;
+    size_t p = 1;
+    while (p < b) p <<= 1;
+    size_t q = p >> 3;  // eighth-of-power-of-two steps (<= 12.5% waste)
+    return (b + q - 1) / q * q;
+}
+
 pm4g_status dalloc(void** p, size_t bytes, cudaStream_t s) {
     setup_pool();
-    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
+    const size_t cls = size_class(bytes ? bytes : 16);
+    {
+        std::lock_guard<std::mutex> lk(g_alloc_mu);
+        for (size_t i = g_free_blocks.size(); i-- > 0;) {
+            if (g_free_blocks[i].first == cls && g_free_blocks[i].second.s == s) {
+                *p = g_free_blocks[i].second.p;
+                g_cached_bytes -= cls;
+                g_free_blocks.erase(g_free_blocks.begin() + i);
+                g_live_blocks.push_back({*p, cls});
+                return PM4G_OK;
+            }
+        }
+    }
+    cudaError_t e = cudaMallocAsync(p, cls, s);
+    if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry once
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(g_alloc_mu);
+        for (auto& fb : g_free_blocks) cudaFreeAsync(fb.second.p, fb.second.s);
+        g_free_blocks.clear();
+        g_cached_bytes = 0;
+        e = cudaMallocAsync(p, cls, s);
+    }
     if (e != cudaSuccess) {
         *p = nullptr;
         return cuda_fail(e, "cudaMallocAsync");
     }
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_live_blocks.push_back({*p, cls});
     return PM4G_OK;
 }
 void dfree(void* p, cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    size_t cls = 0;
+    for (size_t i = g_live_blocks.size(); i-- > 0;) {
+        if (g_live_blocks[i].first == p) {
+            cls = g_live_blocks[i].second;
+            g_live_blocks.erase(g_live_blocks.begin() + i);
+            break;
+        }
+    }
+    if (!cls || g_cached_bytes + cls > kCacheCap) {
+        cudaFreeAsync(p, s);
+        return;
+    }
+    g_free_blocks.push_back({cls, {p, s}});
+    g_cached_bytes += cls;
 }
 
 // ------------------------------------------------------------------ K1: validate + metadata
@@ -271,11 +337,14 @@ pm4g_status pm4g_prof_reset(void) {
 pm4g_status pm4g_prof_collect(int32_t* n_names) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof_aggs.clear();
+    g_prof_lines.clear();
     for (auto& r : g_prof_recs) {
         cudaError_t e = cudaEventSynchronize(r.b);
         if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
-        float ms = 0;
+        float ms = 0, t0 = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
+        cudaEventElapsedTime(&t0, g_prof_recs.front().a, r.a);
+        g_prof_lines.push_back({r.name, (double)t0, (double)ms});
         auto it = std::find_if(g_prof_aggs.begin(), g_prof_aggs.end(),
                                [&](const ProfAgg& a) { return a.name == r.name; });
         if (it == g_prof_aggs.end()) {
@@ -297,6 +366,15 @@ pm4g_status pm4g_prof_entry(int32_t i, const char** name, uint64_t* launches, do
     if (launches) *launches = g_prof_aggs[i].launches;
     if (total_ms) *total_ms = g_prof_aggs[i].ms;
     if (bytes) *bytes = g_prof_aggs[i].bytes;
+    return PM4G_OK;
+}
+
+int32_t pm4g_prof_n_records(void) { return (int32_t)g_prof_lines.size(); }
+pm4g_status pm4g_prof_record(int32_t i, const char** name, double* start_ms, double* dur_ms) {
+    if (i < 0 || i >= (int32_t)g_prof_lines.size()) return fail(PM4G_EINVAL, "record out of range");
+    if (name) *name = g_prof_lines[i].name.c_str();
+    if (start_ms) *start_ms = g_prof_lines[i].start_ms;
+    if (dur_ms) *dur_ms = g_prof_lines[i].dur_ms;
     return PM4G_OK;
 }
 

@@ -164,7 +164,10 @@ __global__ __launch_bounds__(CMP_THREADS) void k_compact_rows(const uint8_t* __r
     uint32_t total;
     uint32_t wex = block_excl_scan<CMP_THREADS>(tid < CMP_THREADS / 32 ? s_wt[tid] : 0u, s_scan, &total);
     if (tid < CMP_THREADS / 32) s_wt[tid] = wex;
-    if (tid == 0) s_prefix = lookback_single(status, tile, total);
+    if (warp == 0) {
+        uint32_t pf = lookback_warp(status, tile, total);
+        if (lane == 0) s_prefix = pf;
+    }
     __syncthreads();
     const uint32_t lt = lanemask_lt();
     uint64_t r = (uint64_t)s_prefix + s_wt[warp];

@@ -131,13 +131,21 @@ __global__ __launch_bounds__(SORT_THREADS) void k_onesweep(PassArgs<P, FROM_COLS
         v[j] = ok ? a.in_act[i] : (P)0;
     }
 
-    // ---- stable local rank: warp-striped order (warp, j, lane) == index order
+    // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
+    // Peers (lanes holding the same digit) come from 8 ballots, one per digit
+    // bit: cheaper than MATCH.ANY, whose latency serialised the first version.
     uint32_t rank[SORT_IPT];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         uint32_t d = (uint32_t)(k[j] >> a.shift) & 0xffu;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t peers = 0xffffffffu;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const bool bit = (d >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
         int leader = __ffs(peers) - 1;
         uint32_t b = 0;
         if (lane == leader) {
@@ -173,15 +181,24 @@ __global__ __launch_bounds__(SORT_THREADS) void k_onesweep(PassArgs<P, FROM_COLS
     s_start[d] = start;
 
     // ---- decoupled look-back for this digit
+    // batched: 4 predecessors per round trip (tile 0 is always inclusive)
     uint32_t prefix = 0;
     if (tile > 0) {
-        const uint32_t* sp = a.status + (size_t)(tile - 1) * RADIX + d;
-        while (true) {
-            uint32_t w;
-            do { w = ld_volatile(sp); } while ((w >> 30) == 0);
-            prefix += w & ST_VAL;
-            if ((w >> 30) == 2) break;
-            sp -= RADIX;
+        int64_t p = (int64_t)tile - 1;
+        bool done = false;
+        while (!done) {
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : ST_INC;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (done) break;
+                while ((w[q] >> 30) == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
+                prefix += w[q] & ST_VAL;
+                if ((w[q] >> 30) == 2) done = true;
+            }
+            p -= 4;
         }
         st_volatile(st, ST_INC | (prefix + pub));
     }
@@ -337,7 +354,10 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
     uint32_t total;
     uint32_t wex = block_excl_scan<SEG_THREADS>(wt, s_scan, &total);
     if (tid < SEG_THREADS / 32) s_warp_tot[tid] = wex;
-    if (tid == 0) s_prefix = lookback_single(status, tile, total);
+    if (warp == 0) {
+        uint32_t pf = lookback_warp(status, tile, total);
+        if (lane == 0) s_prefix = pf;
+    }
     __syncthreads();
     uint32_t r = s_prefix + s_warp_tot[warp];
 #pragma unroll

@@ -69,56 +69,134 @@ __global__ void k_init_table(Slot* table, uint64_t cap) {
     }
 }
 
-// Items: i in [0, n_items) (or list[i] when list != nullptr)
+// Find or claim the global slot of key (a, b): linear probing, one 128-bit CAS
+// claims an empty slot.  Returns the slot, or ~0 when the table is full.
+__device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint64_t a, uint64_t b,
+                                               uint32_t* overflow) {
+    uint64_t h = (a ^ (a >> 29) ^ (b * 0x9E3779B97F4A7C15ull)) & mask;
+    for (uint64_t probes = 0; probes <= mask; ++probes) {
+        Slot* sp = &table[h];
+        K128 cur = ld_k128(sp);
+        if (cur.a == a && cur.b == b) return h;
+        if (cur.a == 0 && cur.b == 0) {
+            K128 exp{0, 0}, des{a, b};
+            K128 old = atomicCAS((K128*)sp, exp, des);
+            if ((old.a == 0 && old.b == 0) || (old.a == a && old.b == b)) return h;
+        }
+        h = (h + 1) & mask;
+    }
+    atomicExch(overflow, 1u);
+    return ~0ull;
+}
+
+// Items: t in [0, n_items) -> item list[t] (or t).  Each CTA first aggregates a
+// chunk of items in a shared-memory table keyed by (k1, k2) -- so a hot variant
+// (Zipf head) costs one global atomic per CTA, not one per case -- then
+// publishes every distinct key of the chunk to the global table.
+constexpr int INS_THREADS = 256, INS_IPT = 4, INS_CHUNK = INS_THREADS * INS_IPT, INS_SLOTS = 2048;
+constexpr size_t INS_SMEM = (size_t)INS_SLOTS * (8 + 8 + 4 + 4 + 8);
+
 template <class OFF>
-__global__ void k_insert(const uint32_t* __restrict__ list, uint64_t n_items,
-                         const uint64_t* __restrict__ k1, const uint64_t* __restrict__ k2,
-                         const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
-                         const uint32_t* __restrict__ order, Slot* table, uint64_t mask,
-                         uint64_t salt, uint32_t* __restrict__ item_slot,
-                         uint8_t* __restrict__ pending, uint32_t* overflow) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t it = list ? list[t] : (uint32_t)t;
-        uint64_t a = k1[it], b = k2[it];
-        if (salt) {
-            a = vmix(a ^ salt) | 1ull;
-            b = vmix(b + salt);
+__global__ __launch_bounds__(INS_THREADS) void k_insert(
+    const uint32_t* __restrict__ list, uint64_t n_items, const uint64_t* __restrict__ k1,
+    const uint64_t* __restrict__ k2, const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
+    const uint32_t* __restrict__ order, Slot* table, uint64_t mask, uint64_t salt,
+    uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* overflow) {
+    extern __shared__ __align__(16) unsigned char ins_sm[];
+    unsigned long long* s_k1 = (unsigned long long*)ins_sm;
+    unsigned long long* s_k2 = s_k1 + INS_SLOTS;
+    unsigned long long* s_g = s_k2 + INS_SLOTS;
+    uint32_t* s_w = (uint32_t*)(s_g + INS_SLOTS);
+    uint32_t* s_rep = s_w + INS_SLOTS;
+    (void)off;
+    for (uint64_t chunk = blockIdx.x; chunk * INS_CHUNK < n_items; chunk += gridDim.x) {
+        for (int i = threadIdx.x; i < INS_SLOTS; i += INS_THREADS) {
+            s_k1[i] = 0;
+            s_w[i] = 0;
+            s_rep[i] = 0xffffffffu;
         }
-        const uint32_t len = (uint32_t)(off[it + 1] - off[it]);
-        const uint64_t w = weight ? weight[it] : 1ull;
-        const uint32_t ord = order ? order[it] : it;
-        uint64_t h = (a ^ (a >> 29) ^ (b * 0x9E3779B97F4A7C15ull)) & mask;
-        uint64_t probes = 0;
-        bool done = false;
-        while (!done) {
-            Slot* sp = &table[h];
-            K128 cur = ld_k128(sp);
-            if (cur.a == a && cur.b == b) {
-                done = true;
-            } else if (cur.a == 0 && cur.b == 0) {
-                K128 exp{0, 0}, des{a, b};
-                K128 old = atomicCAS((K128*)sp, exp, des);
-                if ((old.a == 0 && old.b == 0)) {
-                    sp->len = len;
-                    done = true;
-                } else if (old.a == a && old.b == b) {
-                    done = true;
-                }
+        __syncthreads();
+        uint32_t it[INS_IPT], loc[INS_IPT], ord[INS_IPT], w[INS_IPT];
+        uint64_t ka[INS_IPT], kb[INS_IPT];
+        bool claimed[INS_IPT], live[INS_IPT];
+#pragma unroll
+        for (int u = 0; u < INS_IPT; ++u) {
+            const uint64_t t = chunk * INS_CHUNK + u * INS_THREADS + threadIdx.x;
+            live[u] = t < n_items;
+            claimed[u] = false;
+            if (!live[u]) continue;
+            it[u] = list ? list[t] : (uint32_t)t;
+            uint64_t a = k1[it[u]], b = k2[it[u]];
+            if (salt) {
+                a = vmix(a ^ salt) | 1ull;
+                b = vmix(b + salt);
             }
-            if (!done) {
-                h = (h + 1) & mask;
-                if (++probes > mask) {
-                    atomicExch(overflow, 1u);
-                    break;
+            ka[u] = a;
+            kb[u] = b;
+            w[u] = weight ? (uint32_t)weight[it[u]] : 1u;
+            ord[u] = order ? order[it[u]] : it[u];
+        }
+        // phase A: claim / find the local slot by k1 (k1 is odd, never 0)
+#pragma unroll
+        for (int u = 0; u < INS_IPT; ++u) {
+            if (!live[u]) continue;
+            uint32_t h = (uint32_t)(ka[u] ^ (ka[u] >> 31)) & (INS_SLOTS - 1);
+            while (true) {
+                unsigned long long cur = s_k1[h];
+                if (cur == ka[u]) break;
+                if (cur == 0) {
+                    unsigned long long old = atomicCAS(&s_k1[h], 0ull, (unsigned long long)ka[u]);
+                    if (old == 0) { claimed[u] = true; break; }
+                    if (old == ka[u]) break;
                 }
+                h = (h + 1) & (INS_SLOTS - 1);
+            }
+            loc[u] = h;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < INS_IPT; ++u)
+            if (live[u] && claimed[u]) s_k2[loc[u]] = kb[u];
+        __syncthreads();
+        // phase B: aggregate; a k1 match with a different k2 goes straight to global
+        bool direct[INS_IPT];
+#pragma unroll
+        for (int u = 0; u < INS_IPT; ++u) {
+            direct[u] = live[u] && s_k2[loc[u]] != kb[u];
+            if (live[u] && !direct[u]) {
+                atomicAdd(&s_w[loc[u]], w[u]);
+                atomicMin(&s_rep[loc[u]], ord[u]);
             }
         }
-        if (!done) continue;
-        atomicAdd(&table[h].weight, (unsigned long long)w);
-        atomicMin(&table[h].rep, ord);
-        item_slot[it] = (uint32_t)h;
-        pending[it] = 0;
+        __syncthreads();
+        // phase C: publish each distinct local key once
+        for (int sl = threadIdx.x; sl < INS_SLOTS; sl += INS_THREADS) {
+            if (s_k1[sl] == 0 || s_w[sl] == 0) continue;
+            uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], overflow);
+            s_g[sl] = g;
+            if (g == ~0ull) continue;
+            atomicAdd(&table[g].weight, (unsigned long long)s_w[sl]);
+            atomicMin(&table[g].rep, s_rep[sl]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < INS_IPT; ++u) {
+            if (!live[u]) continue;
+            uint64_t g;
+            if (direct[u]) {
+                g = table_slot(table, mask, ka[u], kb[u], overflow);
+                if (g != ~0ull) {
+                    atomicAdd(&table[g].weight, (unsigned long long)w[u]);
+                    atomicMin(&table[g].rep, ord[u]);
+                }
+            } else {
+                g = s_g[loc[u]];
+            }
+            if (g == ~0ull) continue;
+            item_slot[it[u]] = (uint32_t)g;
+            pending[it[u]] = 0;
+        }
+        __syncthreads();
     }
 }
 
@@ -286,10 +364,20 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
             uint64_t salt = (round == 0 || weak) ? 0ull : 0x9E3779B97F4A7C15ull * (uint64_t)round;
             uint32_t* next_list = (list == list_a) ? list_b : list_a;
             const int gs = gsz(n_active);
-            PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
-                        (k_insert<OFF><<<gs, 256, 0, s>>>(list, n_active, k1, k2, off, weight, order,
-                                                          table, cap - 1, salt, item_slot, pending,
-                                                          counters + 1)));
+            {
+                static bool attr = false;
+                if (!attr) {
+                    PM4G_CK(cudaFuncSetAttribute(k_insert<OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)INS_SMEM));
+                    attr = true;
+                }
+                uint64_t chunks = (n_active + INS_CHUNK - 1) / INS_CHUNK;
+                int gi = (int)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (uint64_t)num_sms() * 3));
+                PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
+                            (k_insert<OFF><<<gi, INS_THREADS, INS_SMEM, s>>>(
+                                list, n_active, k1, k2, off, weight, order, table, cap - 1, salt,
+                                item_slot, pending, counters + 1)));
+            }
             PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
                         (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot)));
             PM4G_LAUNCH("k_variant_verify", n_active * 16.0, s,
@@ -357,7 +445,10 @@ __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __re
     }
     uint32_t total;
     uint32_t ex = block_excl_scan<SCAN_THREADS>(sum, s_scan, &total);
-    if (threadIdx.x == 0) s_prefix = lookback_single(status, tile, total);
+    if (threadIdx.x < 32) {
+        uint32_t pf = lookback_warp(status, tile, total);
+        if (threadIdx.x == 0) s_prefix = pf;
+    }
     __syncthreads();
     uint64_t r = (uint64_t)s_prefix + ex;
 #pragma unroll

@@ -98,6 +98,9 @@ _SIGS = {
     "pm4g_prof_enable": ([I32], I32),
     "pm4g_prof_reset": ([], I32),
     "pm4g_prof_collect": ([ctypes.POINTER(I32)], I32),
+    "pm4g_prof_n_records": ([], I32),
+    "pm4g_prof_record": ([I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double)], I32),
     "pm4g_prof_entry": ([I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(U64),
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], I32),
 }
@@ -433,6 +436,16 @@ def pm4g_prof_collect() -> dict:
         nm, la, ms, by = ctypes.c_char_p(), U64(0), ctypes.c_double(0), ctypes.c_double(0)
         _check(lib().pm4g_prof_entry(i, ctypes.byref(nm), ctypes.byref(la), ctypes.byref(ms), ctypes.byref(by)))
         out[nm.value.decode()] = (la.value, ms.value, by.value)
+    return out
+
+
+def pm4g_prof_records() -> list:
+    """[(name, start_ms, dur_ms)] of the last pm4g_prof_collect, in launch order."""
+    out = []
+    for i in range(int(lib().pm4g_prof_n_records())):
+        nm, t0, d = ctypes.c_char_p(), ctypes.c_double(0), ctypes.c_double(0)
+        _check(lib().pm4g_prof_record(i, ctypes.byref(nm), ctypes.byref(t0), ctypes.byref(d)))
+        out.append((nm.value.decode(), t0.value, d.value))
     return out
 
 
