@@ -512,8 +512,7 @@ pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
     if (L->key_bits > 64)
         return fail(PM4G_EKEYWIDTH, "case_bits + ts_bits = " + std::to_string(L->key_bits) +
                                         " > 64: composite key does not fit");
-    PM4G_TRY(sort_log(L, s));
-    PM4G_TRY(segments(L, s));
+    PM4G_TRY(sort_log(L, s));   // sort + case offsets (format kernel)
     free_log_cols(L, s);
     L->sorted = true;
     L->stream = s;

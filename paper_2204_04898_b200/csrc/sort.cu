@@ -1,23 +1,31 @@
-// A2-A4: composite-key build, stable LSD radix sort (onesweep), case segments.
+// A2-A4: stable sort of the log by (case, ts, ingest index) and case segments.
 //
 // P:108 "The dataframe is ordered based on three criteria (in order, case
 // identifier, the timestamp, and the absolute index of the event in the
-// dataframe)".  Reading R1/R2: case order = dictionary code, ties = ingest index.
-// We sort the composite key  key = ((case - case_min) << ts_bits) | (ts - ts_min)
-// with a STABLE least-significant-digit radix sort, so equal keys keep
-// ingest order: stability realises the third criterion without storing it.
+// dataframe)".  Readings R1/R2: case order = dictionary code, ties = ingest
+// index.  Output (the "formatted log"): the composite key
+//     key = ((case - case_min) << ts_bits) | (ts - ts_min)
+// in sorted order, the activity (and, with extra columns, the ingest row)
+// alongside, and the case offsets (CSR) of the cases dataframe.
 //
-// Design (B200): 8-bit digits; one up-front kernel reads (case, ts) once and
-// builds the histograms of every digit; each pass is one "onesweep" kernel
-// (tiles of 4096 keys, tile ids from an atomic counter, per-digit decoupled
-// look-back over the tile status array, local ranking with __match_any_sync
-// warp aggregation, smem staging so the scatter writes runs of equal digits).
-// The first pass reads the raw columns and builds the key on the fly, so the
-// key is never written unsorted.  HBM bytes per event (act u8, P passes):
-// hist 12 + pass0 (13 read + 9 write) + (P-1) * 18.
+// B200 design: a radix pass on B200 is instruction-issue bound
+// (6.5 TB/s over 148 SMs is 23 B per SM clock), so the number of passes is
+// what matters.  Instead of ceil(key_bits / 8) passes over the 60-bit
+// composite key we do
+//   1. a stable LSD "onesweep" radix sort on the CASE code only
+//      (ceil(case_bits / 8) passes, 4-byte keys, ts/act carried as payload):
+//      events end up grouped by case, in ingest order inside each case;
+//   2. one fused "format" kernel: per tile it finds case heads, ranks them
+//      with a decoupled look-back (-> case offsets), sorts every case by
+//      timestamp in shared memory (rank = #earlier-or-smaller, ties by
+//      position => stable) and writes the composite key.  Cases longer than a
+//      tile extension go to an exact fallback (a stable radix sort of that
+//      case's timestamps).
+// HBM bytes per event (u8 act, P case passes): hist 4 + P * 26 + format 22.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "pm4g_internal.cuh"
 
@@ -30,31 +38,23 @@ constexpr int SORT_IPT = 16;
 constexpr int SORT_TILE = SORT_THREADS * SORT_IPT;  // 4096
 constexpr int MAX_PASSES = 8;
 
-struct KeyParams {
-    uint32_t case_min;
-    int64_t ts_min;
-    int ts_bits;
-};
-
-__device__ __forceinline__ uint64_t make_key(uint32_t c, int64_t t, const KeyParams& kp) {
-    uint64_t cr = (uint64_t)(c - kp.case_min);
-    uint64_t tr = (uint64_t)t - (uint64_t)kp.ts_min;
-    return (kp.ts_bits >= 64 ? 0 : (cr << kp.ts_bits)) | tr;
+__host__ __device__ inline uint64_t make_key(uint64_t case_rel, int64_t t, int64_t ts_min, int ts_bits) {
+    return (ts_bits >= 64 ? 0 : (case_rel << ts_bits)) | ((uint64_t)t - (uint64_t)ts_min);
 }
 
 // ------------------------------------------------------------------ histograms
-template <bool FROM_COLS>
-__global__ __launch_bounds__(256) void k_hist(const uint64_t* __restrict__ keys,
-                                              const uint32_t* __restrict__ cs,
-                                              const int64_t* __restrict__ ts, int64_t n,
-                                              KeyParams kp, int passes, uint32_t* __restrict__ hist) {
+// digit p of a key = ((key - sub) >> (p * bits)) & ((1 << bits) - 1)
+template <class K>
+__global__ __launch_bounds__(256) void k_hist(const K* __restrict__ keys, int64_t n, K sub, int bits,
+                                              int passes, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[MAX_PASSES][RADIX];
     for (int i = threadIdx.x; i < MAX_PASSES * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
+    const uint32_t mask = (1u << bits) - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t k = FROM_COLS ? make_key(cs[i], ts[i], kp) : keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 0xff], 1u);
+        K k = keys[i] - sub;
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(k >> (p * bits)) & mask], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * RADIX; i += blockDim.x) {
@@ -76,30 +76,32 @@ __global__ void k_hist_scan(const uint32_t* __restrict__ hist, uint32_t* __restr
 }
 
 // ------------------------------------------------------------------ one onesweep pass
-template <class P, bool FROM_COLS, bool WITH_IDX>
+// Stable scatter of (key, [ts], act-like payload, [idx]) by one digit.
+template <class K, class P, bool HAS_TS, bool WITH_IDX>
 struct PassArgs {
-    const uint64_t* in_key;
-    const uint32_t* in_case;
+    const K* in_key;
     const int64_t* in_ts;
     const P* in_act;
-    const uint32_t* in_idx;
-    uint64_t* out_key;
+    const uint32_t* in_idx;   // nullptr with WITH_IDX: generate the ingest row
+    K* out_key;
+    int64_t* out_ts;
     P* out_act;
     uint32_t* out_idx;
     int64_t n;
-    int shift;
+    K sub;                    // subtracted from every input key (case_min in pass 0)
+    int shift, bits;
     const uint32_t* bucket_off;  // [256]
     uint32_t* status;            // [tiles * 256]
     uint32_t* tile_counter;
-    KeyParams kp;
 };
 
-template <class P, bool FROM_COLS, bool WITH_IDX>
-__global__ __launch_bounds__(SORT_THREADS) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
+template <class K, class P, bool HAS_TS, bool WITH_IDX>
+__global__ __launch_bounds__(SORT_THREADS, 3) void k_onesweep(PassArgs<K, P, HAS_TS, WITH_IDX> a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* s_key = (uint64_t*)smem;
-    P* s_act = (P*)(smem + SORT_TILE * 8);
-    uint32_t* s_idx = (uint32_t*)(smem + SORT_TILE * 8 + SORT_TILE * sizeof(P));
+    K* s_key = (K*)smem;
+    int64_t* s_ts = (int64_t*)(smem + SORT_TILE * sizeof(K));
+    uint32_t* s_idx = (uint32_t*)(smem + SORT_TILE * (sizeof(K) + (HAS_TS ? 8 : 0)));
+    P* s_act = (P*)(smem + SORT_TILE * (sizeof(K) + (HAS_TS ? 8 : 0) + (WITH_IDX ? 4 : 0)));
     __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
     __shared__ uint32_t s_start[RADIX];
     __shared__ long long s_gbase[RADIX];
@@ -113,52 +115,44 @@ __global__ __launch_bounds__(SORT_THREADS) void k_onesweep(PassArgs<P, FROM_COLS
     const uint32_t tile = s_tile;
     const int64_t base = (int64_t)tile * SORT_TILE;
     const int64_t wbase = base + warp * (32 * SORT_IPT);
+    const uint32_t dmask = (1u << a.bits) - 1;
 
-    uint64_t k[SORT_IPT];
-    P v[SORT_IPT];
-    uint32_t ix[SORT_IPT];
+    K k[SORT_IPT];
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         int64_t i = wbase + j * 32 + lane;
-        bool ok = i < a.n;
-        if (FROM_COLS) {
-            k[j] = ok ? make_key(a.in_case[i], a.in_ts[i], a.kp) : ~0ull;
-            if (WITH_IDX) ix[j] = (uint32_t)i;
-        } else {
-            k[j] = ok ? a.in_key[i] : ~0ull;
-            if (WITH_IDX) ix[j] = ok ? a.in_idx[i] : 0u;
-        }
-        v[j] = ok ? a.in_act[i] : (P)0;
+        k[j] = i < a.n ? (K)(a.in_key[i] - a.sub) : (K)~(K)0;
     }
 
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
-    // Peers (lanes holding the same digit) come from 8 ballots, one per digit
-    // bit: cheaper than MATCH.ANY, whose latency serialised the first version.
-    uint32_t rank[SORT_IPT];
+    // Peers (lanes holding the same digit) from one ballot per digit bit.
+    uint32_t pos[SORT_IPT];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
-        uint32_t d = (uint32_t)(k[j] >> a.shift) & 0xffu;
+        const uint32_t d = (uint32_t)(k[j] >> a.shift) & dmask;
         uint32_t peers = 0xffffffffu;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
-            const bool bit = (d >> b) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
+            if (b < a.bits) {
+                const bool bit = (d >> b) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
         }
-        int leader = __ffs(peers) - 1;
-        uint32_t b = 0;
+        const int leader = __ffs(peers) - 1;
+        uint32_t bse = 0;
         if (lane == leader) {
-            b = s_whist[warp][d];
-            s_whist[warp][d] = b + __popc(peers);
+            bse = s_whist[warp][d];
+            s_whist[warp][d] = bse + __popc(peers);
         }
-        b = __shfl_sync(0xffffffffu, b, leader);
-        rank[j] = b + __popc(peers & lt);
+        bse = __shfl_sync(0xffffffffu, bse, leader);
+        pos[j] = bse + __popc(peers & lt);
         __syncwarp();
     }
     __syncthreads();
 
-    // ---- per-digit totals, warp-exclusive prefixes (thread == digit)
+    // ---- per-digit totals and warp-exclusive prefixes (thread == digit)
     const int d = tid;
     uint32_t tot = 0;
 #pragma unroll
@@ -167,143 +161,458 @@ __global__ __launch_bounds__(SORT_THREADS) void k_onesweep(PassArgs<P, FROM_COLS
         s_whist[w][d] = tot;
         tot += c;
     }
-    // invalid items (past n, only in the last tile) carry digit 255 of ~0 and
-    // rank last; they are not part of the published counts.
-    int64_t nvalid64 = a.n - base;
-    const uint32_t nvalid = (uint32_t)(nvalid64 < SORT_TILE ? nvalid64 : SORT_TILE);
+    // invalid items (only in the last tile) carry the all-ones digit and rank
+    // last; they are not part of the published counts
+    const int64_t nv64 = a.n - base;
+    const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
     uint32_t pub = tot;
-    if (d == (int)((~0ull >> a.shift) & 0xffu)) pub -= (SORT_TILE - nvalid);
+    if (d == (int)dmask) pub -= (SORT_TILE - nvalid);
     uint32_t* st = a.status + (size_t)tile * RADIX + d;
-    if (tile == 0) st_volatile(st, ST_INC | pub);
-    else st_volatile(st, ST_AGG | pub);
-
-    uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, nullptr);
-    s_start[d] = start;
-
-    // ---- decoupled look-back for this digit
-    // batched: 4 predecessors per round trip (tile 0 is always inclusive)
-    uint32_t prefix = 0;
-    if (tile > 0) {
-        int64_t p = (int64_t)tile - 1;
-        bool done = false;
-        while (!done) {
-            uint32_t w[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : ST_INC;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (done) break;
-                while ((w[q] >> 30) == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
-                prefix += w[q] & ST_VAL;
-                if ((w[q] >> 30) == 2) done = true;
-            }
-            p -= 4;
-        }
-        st_volatile(st, ST_INC | (prefix + pub));
+    if (d <= (int)dmask) {
+        if (tile == 0) st_volatile(st, ST_INC | pub);
+        else st_volatile(st, ST_AGG | pub);
     }
-    s_gbase[d] = (long long)a.bucket_off[d] + prefix - start;
+    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, nullptr);
+    s_start[d] = start;
     __syncthreads();
 
-    // ---- scatter into smem in digit order
+    // ---- scatter keys and payloads into smem in digit order (payload loads
+    // are issued here, after ranking, so they never occupy registers earlier)
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
-        uint32_t dd = (uint32_t)(k[j] >> a.shift) & 0xffu;
-        uint32_t pos = s_start[dd] + s_whist[warp][dd] + rank[j];
-        s_key[pos] = k[j];
-        s_act[pos] = v[j];
-        if (WITH_IDX) s_idx[pos] = ix[j];
+        const uint32_t dd = (uint32_t)(k[j] >> a.shift) & dmask;
+        pos[j] += s_start[dd] + s_whist[warp][dd];
+        s_key[pos[j]] = k[j];
+    }
+#pragma unroll
+    for (int j = 0; j < SORT_IPT; ++j) {
+        const int64_t i = wbase + j * 32 + lane;
+        if (i < a.n) {
+            if (HAS_TS) s_ts[pos[j]] = a.in_ts[i];
+            s_act[pos[j]] = a.in_act[i];
+            if (WITH_IDX) s_idx[pos[j]] = a.in_idx ? a.in_idx[i] : (uint32_t)i;
+        }
+    }
+
+    // ---- decoupled look-back for this digit, 4 predecessors per round trip
+    if (d <= (int)dmask) {
+        uint32_t prefix = 0;
+        if (tile > 0) {
+            int64_t p = (int64_t)tile - 1;
+            bool done = false;
+            while (!done) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : ST_INC;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (done) break;
+                    while ((w[q] >> 30) == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
+                    prefix += w[q] & ST_VAL;
+                    if ((w[q] >> 30) == 2) done = true;
+                }
+                p -= 4;
+            }
+            st_volatile(st, ST_INC | (prefix + pub));
+        }
+        s_gbase[d] = (long long)a.bucket_off[d] + prefix - start;
     }
     __syncthreads();
 
     // ---- coalesced write-out: consecutive threads, consecutive positions
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
-        uint32_t sidx = j * SORT_THREADS + tid;
+        const uint32_t sidx = j * SORT_THREADS + tid;
         if (sidx < nvalid) {
-            uint64_t kk = s_key[sidx];
-            uint32_t dd = (uint32_t)(kk >> a.shift) & 0xffu;
-            long long g = s_gbase[dd] + sidx;
+            const K kk = s_key[sidx];
+            const long long g = s_gbase[(uint32_t)(kk >> a.shift) & dmask] + sidx;
             a.out_key[g] = kk;
+            if (HAS_TS) a.out_ts[g] = s_ts[sidx];
             a.out_act[g] = s_act[sidx];
             if (WITH_IDX) a.out_idx[g] = s_idx[sidx];
         }
     }
 }
 
-template <class P, bool FC, bool WI>
-static pm4g_status launch_pass(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
+template <class K, class P, bool TS, bool WI>
+static pm4g_status launch_pass(const PassArgs<K, P, TS, WI>& args, int64_t tiles, cudaStream_t s,
                                const char* name, double bytes) {
-    size_t smem = (size_t)SORT_TILE * (8 + sizeof(P) + (WI ? 4 : 0));
+    const size_t smem = (size_t)SORT_TILE * (sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P));
     static bool attr = false;
     if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_onesweep<P, FC, WI>,
+        PM4G_CK(cudaFuncSetAttribute(k_onesweep<K, P, TS, WI>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    PM4G_LAUNCH(name, bytes, s, k_onesweep<P, FC, WI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args));
+    PM4G_LAUNCH(name, bytes, s, (k_onesweep<K, P, TS, WI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
     return PM4G_OK;
 }
 
-// LSD sort of (key, act[, idx]).  FROM_COLS first pass builds keys from (case, ts).
-template <class P, bool WI>
-static pm4g_status lsd_sort(const uint32_t* cs, const int64_t* ts, const uint64_t* keys_in,
-                            const P* act_in, const uint32_t* idx_in, uint64_t* key_out,
-                            P* act_out, uint32_t* idx_out, int64_t n, int passes, KeyParams kp,
-                            cudaStream_t s) {
-    const bool from_cols = (keys_in == nullptr);
-    passes = std::max(1, std::min(passes, MAX_PASSES));
+// Stable LSD sort of `bits_total` low bits of (key - sub), payloads carried.
+// Result lands in the *_out buffers; tmp holds the ping-pong copy.
+template <class K, class P, bool TS, bool WI>
+static pm4g_status lsd_sort(const K* key_in, const int64_t* ts_in, const P* act_in,
+                            const uint32_t* idx_in, K* key_out, int64_t* ts_out, P* act_out,
+                            uint32_t* idx_out, int64_t n, K sub, int bits_total, cudaStream_t s) {
+    const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
+    const int bits = std::max(1, (bits_total + passes - 1) / passes);
     const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
     Scratch aux(s), tmp(s);
-    size_t status_words = (size_t)tiles * RADIX * passes;
-    size_t aux_bytes = (status_words + passes /*counters*/ + 2 * MAX_PASSES * RADIX) * 4;
-    PM4G_TRY(aux.alloc(aux_bytes));
+    const size_t status_words = (size_t)tiles * RADIX * passes;
+    PM4G_TRY(aux.alloc((status_words + passes + 2 * MAX_PASSES * RADIX) * 4));
     uint32_t* status = aux.as<uint32_t>();
     uint32_t* counters = status + status_words;
     uint32_t* hist = counters + passes;
     uint32_t* off = hist + MAX_PASSES * RADIX;
     PM4G_CK(cudaMemsetAsync(status, 0, (status_words + passes + MAX_PASSES * RADIX) * 4, s));
     {
-        int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 4));
-        double bytes = (double)n * (from_cols ? 12 : 8);
-        if (from_cols)
-            PM4G_LAUNCH("k_hist", bytes, s, k_hist<true><<<g, 256, 0, s>>>(nullptr, cs, ts, n, kp, passes, hist));
-        else
-            PM4G_LAUNCH("k_hist", bytes, s, k_hist<false><<<g, 256, 0, s>>>(keys_in, nullptr, nullptr, n, kp, passes, hist));
+        const int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 4));
+        PM4G_LAUNCH("k_hist", n * (double)sizeof(K), s,
+                    (k_hist<K><<<g, 256, 0, s>>>(key_in, n, sub, bits, passes, hist)));
         PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(hist, off, passes));
     }
-    // ping-pong so that the last pass lands in the output buffers
-    const size_t per = (size_t)n * (8 + sizeof(P) + (WI ? 4 : 0));
-    PM4G_TRY(tmp.alloc(per));
-    // layout keeps every array naturally aligned: keys (8n) | idx (4n) | act
-    uint64_t* tkey = tmp.as<uint64_t>();
-    uint32_t* tidx = (uint32_t*)((char*)tmp.p + (size_t)n * 8);
-    P* tact = (P*)((char*)tmp.p + (size_t)n * (8 + (WI ? 4 : 0)));
-    const uint64_t* ck = keys_in;
+    const size_t per = (size_t)n * (sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P));
+    PM4G_TRY(tmp.alloc(per + 64));
+    // aligned sub-arrays: ts (8) | key | idx | act
+    char* tp = (char*)tmp.p;
+    int64_t* tts = (int64_t*)tp;
+    K* tkey = (K*)(tp + (TS ? (size_t)n * 8 : 0));
+    uint32_t* tidx = (uint32_t*)((char*)tkey + (size_t)n * sizeof(K));
+    P* tact = (P*)((char*)tidx + (WI ? (size_t)n * 4 : 0));
+    const K* ck = key_in;
+    const int64_t* ct = ts_in;
     const P* ca = act_in;
     const uint32_t* ci = idx_in;
+    K csub = sub;
+    const double row = (double)sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P);
     for (int p = 0; p < passes; ++p) {
-        bool to_out = ((passes - 1 - p) % 2) == 0;
-        uint64_t* ok = to_out ? key_out : tkey;
-        P* oa = to_out ? act_out : tact;
-        uint32_t* oi = to_out ? idx_out : tidx;
-        double rd = (p == 0 && from_cols) ? 12.0 + sizeof(P) : 8.0 + sizeof(P) + (WI ? 4 : 0);
-        double bytes = (double)n * (rd + 8 + sizeof(P) + (WI ? 4 : 0));
-        if (p == 0 && from_cols) {
-            PassArgs<P, true, WI> a{nullptr, cs, ts, act_in, nullptr, ok, oa, oi, n, 0,
-                                    off, status, counters, kp};
-            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", bytes));
-        } else {
-            PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, 8 * p,
-                                     off + p * RADIX, status + (size_t)p * tiles * RADIX,
-                                     counters + p, kp};
-            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", bytes));
-        }
-        ck = ok;
-        ca = oa;
-        ci = oi;
+        const bool to_out = ((passes - 1 - p) % 2) == 0;
+        PassArgs<K, P, TS, WI> a{ck, ct, ca, ci,
+                                 to_out ? key_out : tkey, to_out ? ts_out : tts,
+                                 to_out ? act_out : tact, to_out ? idx_out : tidx,
+                                 n, csub, p * bits, bits, off + p * RADIX,
+                                 status + (size_t)p * tiles * RADIX, counters + p};
+        const double bytes = (double)n * (row - ((WI && !ci) ? 4 : 0) + row);
+        PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", bytes));
+        ck = a.out_key;
+        ct = a.out_ts;
+        ca = a.out_act;
+        ci = a.out_idx;
+        csub = 0;
     }
     return PM4G_OK;
+}
+
+// ------------------------------------------------------------------ A4 + format
+// Input: events grouped by case (stable), case_rel = gcase[i] - case_sub.
+// Per tile of 4096 positions: heads (case starts) -> ranks via look-back ->
+// case offsets; each case owned by this tile (head inside it) is sorted by
+// timestamp in shared memory and written as composite keys.  A case may run up
+// to FMT_EXT positions past the tile end; longer ones are "big" cases handled
+// by format_big().
+constexpr int FMT_THREADS = 256, FMT_IPT = 16, FMT_TILE = FMT_THREADS * FMT_IPT;
+constexpr int FMT_EXT = 1024, FMT_BUF = FMT_TILE + FMT_EXT;
+constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
+
+template <class P>
+struct FmtArgs {
+    const uint32_t* gcase;
+    const int64_t* gts;
+    const P* gact;
+    const uint32_t* gidx;      // nullptr: ingest row = position (no LSD passes ran)
+    int64_t n;
+    uint32_t case_sub;
+    uint32_t case_min;
+    int64_t ts_min;
+    int ts_bits;
+    uint64_t* key_out;
+    P* act_out;
+    uint32_t* perm_out;        // nullptr: no extra columns
+    uint32_t* off;
+    uint32_t* case_code;
+    uint64_t* n_cases;
+    uint32_t* status;
+    uint32_t* counter;
+    uint32_t* big;             // [cap] ranks of big cases
+    uint32_t* big_count;
+};
+
+template <class P, bool WI>
+__global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    uint64_t* s_key = (uint64_t*)fsm;                              // [FMT_BUF]
+    uint16_t* s_dst = (uint16_t*)(s_key + FMT_BUF);                // [FMT_BUF]
+    uint16_t* s_ci = s_dst + FMT_BUF;                              // [FMT_BUF] case of each row
+    uint16_t* s_head = s_ci + FMT_BUF;                             // [FMT_TILE + 8]
+    P* s_act = (P*)(s_head + FMT_TILE + 8);                        // [FMT_BUF]
+    uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
+    __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
+    __shared__ uint32_t s_prefix, s_H;
+    __shared__ int s_ext;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * FMT_TILE;
+    const int tn = (int)min((int64_t)FMT_TILE, a.n - base);
+    const int64_t wbase = base + warp * (32 * FMT_IPT);
+
+    // ---- heads: case(i) != case(i-1)
+    uint32_t ball[FMT_IPT], wc = 0;
+    {
+        uint32_t prev = 0;
+        const int64_t pi = wbase - 1;
+        if (pi >= 0 && pi < a.n) prev = a.gcase[pi];
+#pragma unroll
+        for (int j = 0; j < FMT_IPT; ++j) {
+            const int64_t i = wbase + j * 32 + lane;
+            const bool ok = i < a.n;
+            const uint32_t c = ok ? a.gcase[i] : 0u;
+            uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+            if (lane == 0) pc = prev;
+            prev = __shfl_sync(0xffffffffu, c, 31);
+            ball[j] = __ballot_sync(0xffffffffu, ok && (i == 0 || c != pc));
+            wc += __popc(ball[j]);
+        }
+    }
+    if (lane == 0) s_wt[warp] = wc;
+    __syncthreads();
+    uint32_t H;
+    const uint32_t wex = block_excl_scan<FMT_THREADS>(tid < FMT_THREADS / 32 ? s_wt[tid] : 0u, s_scan, &H);
+    if (tid < FMT_THREADS / 32) s_wt[tid] = wex;
+    if (warp == 0) {
+        const uint32_t pf = lookback_warp(a.status, tile, H);
+        if (lane == 0) s_prefix = pf;
+    }
+    __syncthreads();
+    {
+        const uint32_t lt = lanemask_lt();
+        uint32_t r = s_wt[warp];
+#pragma unroll
+        for (int j = 0; j < FMT_IPT; ++j) {
+            if (ball[j] & (1u << lane)) s_head[r + __popc(ball[j] & lt)] = (uint16_t)(warp * 32 * FMT_IPT + j * 32 + lane);
+            r += __popc(ball[j]);
+        }
+    }
+    __syncthreads();
+    const uint32_t R0 = s_prefix;
+
+    // ---- extent of the last owned case past the tile end
+    if (warp == 0) {
+        int ext = 0;
+        if (H > 0 && base + tn < a.n) {
+            const uint32_t last = a.gcase[base + s_head[H - 1]];
+            ext = -1;
+            for (int o = 0; o <= FMT_EXT; o += 32) {
+                const int64_t i = base + tn + o + lane;
+                const bool stop = i >= a.n || a.gcase[i] != last;
+                const uint32_t b = __ballot_sync(0xffffffffu, stop);
+                if (b) {
+                    const int e = o + __ffs(b) - 1;
+                    ext = e <= FMT_EXT ? e : -1;
+                    break;
+                }
+            }
+        }
+        if (lane == 0) {
+            s_ext = ext;
+            s_H = H;
+        }
+    }
+    // case offsets and codes of every head in the tile
+    for (uint32_t h = tid; h < H; h += FMT_THREADS) {
+        const int64_t i = base + s_head[h];
+        a.off[R0 + h] = (uint32_t)i;
+        a.case_code[R0 + h] = a.case_min + (a.gcase[i] - a.case_sub);
+    }
+    if (tid == 0 && base + tn >= a.n) {
+        a.off[R0 + H] = (uint32_t)a.n;
+        *a.n_cases = R0 + H;
+    }
+    __syncthreads();
+    if (H == 0) return;
+    int ext = s_ext;
+    uint32_t Hown = H;                 // cases this tile sorts here
+    if (ext < 0) {                     // last case is big: exact fallback after the kernel
+        if (tid == 0) a.big[atomicAdd(a.big_count, 1u)] = R0 + H - 1;
+        Hown = H - 1;
+        ext = 0;
+    }
+    const int h0 = s_head[0];
+    const int oend = Hown == H ? tn + ext : (int)s_head[H - 1];   // owned local range [h0, oend)
+
+    // ---- stage the owned range: composite keys, activities, ingest rows
+    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
+        const int64_t i = base + p;
+        const uint64_t cr = a.gcase[i] - a.case_sub;
+        s_key[p] = make_key(cr, a.gts[i], a.ts_min, a.ts_bits);
+        s_act[p] = a.gact[i];
+        if (WI) s_idx[p] = a.gidx ? a.gidx[i] : (uint32_t)i;
+    }
+    __syncthreads();
+
+    // ---- rank every event inside its case: #(key_j < key_i or (== and j < i)).
+    // Event-parallel: each thread ranks one row against its own case, so work
+    // is balanced across threads and a warp (mostly one case) reads s_key[j]
+    // as a broadcast.  Cases longer than FMT_WARP_MAX go to the exact fallback.
+    for (uint32_t h = tid; h < Hown; h += FMT_THREADS) {
+        const int s0 = s_head[h], e0 = (h + 1 < Hown) ? s_head[h + 1] : oend;
+        const bool big = e0 - s0 > FMT_WARP_MAX;
+        if (big) a.big[atomicAdd(a.big_count, 1u)] = R0 + h;
+        for (int p = s0; p < e0; ++p) s_ci[p] = big ? (uint16_t)0xffff : (uint16_t)h;
+    }
+    __syncthreads();
+    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
+        const uint32_t h = s_ci[p];
+        if (h == 0xffff) {
+            s_dst[p] = 0xffff;
+            continue;
+        }
+        const int s0 = s_head[h], e0 = (h + 1 < Hown) ? s_head[h + 1] : oend;
+        const uint64_t ki = s_key[p];
+        int r = 0;
+        for (int j = s0; j < e0; ++j) {
+            const uint64_t kj = s_key[j];
+            r += (kj < ki) || (kj == ki && j < p);
+        }
+        s_dst[p] = (uint16_t)(s0 + r);
+    }
+    __syncthreads();
+
+    // ---- write the formatted rows of the owned range
+    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
+        if (s_dst[p] == 0xffff) continue;   // rows of a fallback case
+        const int64_t g = base + s_dst[p];
+        a.key_out[g] = s_key[p];
+        a.act_out[g] = s_act[p];
+        if (WI) a.perm_out[g] = s_idx[p];
+    }
+}
+
+// big cases: stable radix sort of the case's timestamps, then gather
+template <class P>
+__global__ void k_big_keys(const int64_t* __restrict__ gts, int64_t start, int64_t len, int64_t ts_min,
+                           uint64_t* __restrict__ k, uint32_t* __restrict__ v) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
+        k[q] = (uint64_t)gts[start + q] - (uint64_t)ts_min;
+        v[q] = (uint32_t)q;
+    }
+}
+template <class P>
+__global__ void k_big_gather(FmtArgs<P> a, int64_t start, int64_t len, uint64_t case_rel,
+                             const uint32_t* __restrict__ v) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t src = start + v[q];
+        a.key_out[start + q] = make_key(case_rel, a.gts[src], a.ts_min, a.ts_bits);
+        a.act_out[start + q] = a.gact[src];
+        if (a.perm_out) a.perm_out[start + q] = a.gidx ? a.gidx[src] : (uint32_t)src;
+    }
+}
+
+template <class P>
+static pm4g_status format_log(pm4g_log* L, const FmtArgs<P>& fa0, cudaStream_t s) {
+    FmtArgs<P> fa = fa0;
+    const int64_t n = fa.n;
+    const int64_t tiles = (n + FMT_TILE - 1) / FMT_TILE;
+    Scratch st(s);
+    const size_t words = 2 + (size_t)tiles + ((size_t)n / FMT_WARP_MAX + tiles + 2);
+    PM4G_TRY(st.alloc(words * 4));
+    PM4G_CK(cudaMemsetAsync(st.p, 0, (2 + tiles) * 4, s));
+    fa.counter = st.as<uint32_t>();
+    fa.big_count = fa.counter + 1;
+    fa.status = fa.counter + 2;
+    fa.big = fa.status + tiles;
+    const bool wi = fa.perm_out != nullptr;
+    const size_t smem = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + 16 +
+                        (wi ? (size_t)FMT_BUF * 4 : 0);
+    static bool attr = false;
+    if (!attr) {
+        PM4G_CK(cudaFuncSetAttribute(k_format<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(smem + (wi ? 0 : (size_t)FMT_BUF * 4))));
+        PM4G_CK(cudaFuncSetAttribute(k_format<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(smem + (wi ? 0 : (size_t)FMT_BUF * 4))));
+        attr = true;
+    }
+    const double bytes = (double)n * (4 + 8 + sizeof(P) + (fa.gidx ? 4 : 0) + 8 + sizeof(P) +
+                                      (fa.perm_out ? 4 : 0));
+    if (wi)
+        PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
+    else
+        PM4G_LAUNCH("k_format", bytes, s, (k_format<P, false><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
+    uint32_t nbig = 0;
+    PM4G_CK(cudaMemcpyAsync(&nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    if (nbig == 0) return PM4G_OK;
+    std::vector<uint32_t> ranks(nbig);
+    PM4G_CK(cudaMemcpyAsync(ranks.data(), fa.big, nbig * 4, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    for (uint32_t r : ranks) {
+        uint32_t se[2];
+        uint32_t code = 0;
+        PM4G_CK(cudaMemcpyAsync(se, fa.off + r, 8, cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaMemcpyAsync(&code, fa.case_code + r, 4, cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaStreamSynchronize(s));
+        const int64_t start = se[0], len = (int64_t)se[1] - se[0];
+        Scratch kv(s);
+        PM4G_TRY(kv.alloc((size_t)len * 12 + 16));
+        uint64_t* k = kv.as<uint64_t>();
+        uint32_t* v = (uint32_t*)(k + len);
+        const int g = std::max(1, std::min<int>((int)((len + 255) / 256), num_sms() * 4));
+        PM4G_LAUNCH("k_big_keys", len * 20.0, s, (k_big_keys<P><<<g, 256, 0, s>>>(fa.gts, start, len, fa.ts_min, k, v)));
+        PM4G_TRY(radix_sort_u64(k, v, len, std::min(64, std::max(1, fa.ts_bits)), s));
+        PM4G_LAUNCH("k_big_gather", len * 30.0, s,
+                    (k_big_gather<P><<<g, 256, 0, s>>>(fa, start, len, (uint64_t)(code - fa.case_min), v)));
+    }
+    (void)L;
+    return PM4G_OK;
+}
+
+template <class P>
+static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
+    const int64_t n = L->n;
+    const bool wi = !L->extra.empty();
+    FmtArgs<P> fa{};
+    fa.n = n;
+    fa.case_min = L->case_min;
+    fa.ts_min = L->ts_min;
+    fa.ts_bits = L->ts_bits;
+    fa.key_out = L->key;
+    fa.act_out = (P*)L->s_act;
+    fa.perm_out = wi ? L->perm : nullptr;
+    fa.off = L->off;
+    fa.case_code = L->s_case_code;
+    fa.n_cases = L->d_n_cases;
+    Scratch grp(s);
+    if (L->case_bits == 0) {           // a single case code: already grouped
+        fa.gcase = L->case_;
+        fa.gts = L->ts;
+        fa.gact = (const P*)L->act;
+        fa.gidx = nullptr;
+        fa.case_sub = L->case_min;
+        return format_log<P>(L, fa, s);
+    }
+    // stable LSD passes on the case code; ts / act (/ ingest row) ride along
+    const size_t per = (size_t)n * (4 + 8 + (wi ? 4 : 0) + sizeof(P));
+    PM4G_TRY(grp.alloc(per + 64));
+    char* gp = (char*)grp.p;
+    int64_t* gts = (int64_t*)gp;
+    uint32_t* gcase = (uint32_t*)(gp + (size_t)n * 8);
+    uint32_t* gidx = gcase + n;
+    P* gact = (P*)((char*)gidx + (wi ? (size_t)n * 4 : 0));
+    if (wi)
+        PM4G_TRY((lsd_sort<uint32_t, P, true, true>(L->case_, L->ts, (const P*)L->act, nullptr, gcase, gts,
+                                                     gact, gidx, n, L->case_min, L->case_bits, s)));
+    else
+        PM4G_TRY((lsd_sort<uint32_t, P, true, false>(L->case_, L->ts, (const P*)L->act, nullptr, gcase, gts,
+                                                      gact, nullptr, n, L->case_min, L->case_bits, s)));
+    fa.gcase = gcase;
+    fa.gts = gts;
+    fa.gact = gact;
+    fa.gidx = wi ? gidx : nullptr;
+    fa.case_sub = 0;
+    return format_log<P>(L, fa, s);
 }
 
 // ------------------------------------------------------------------ A4 segments
@@ -454,37 +763,36 @@ pm4g_status sort_log(pm4g_log* L, cudaStream_t s) {
     PM4G_TRY(dalloc_t(&L->key, std::max<int64_t>(n, 1), s));
     PM4G_TRY(dalloc(&L->s_act, std::max<int64_t>(n, 1) * L->act_bytes, s));
     if (wi) PM4G_TRY(dalloc_t(&L->perm, std::max<int64_t>(n, 1), s));
-    if (n == 0) return PM4G_OK;
-    KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
-    int passes = std::max(1, L->passes);
-#define PM4G_SORT_CASE(P)                                                                  \
-    if (wi)                                                                                \
-        PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr,   \
-                                    L->key, (P*)L->s_act, L->perm, n, passes, kp, s)));    \
-    else                                                                                   \
-        PM4G_TRY((lsd_sort<P, false>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr,  \
-                                     L->key, (P*)L->s_act, nullptr, n, passes, kp, s)));
-    switch (L->act_bytes) {
-        case 1: PM4G_SORT_CASE(uint8_t) break;
-        case 2: PM4G_SORT_CASE(uint16_t) break;
-        default: PM4G_SORT_CASE(uint32_t) break;
+    // offsets: number of cases <= min(n, case range)
+    dfree(L->off, s);
+    dfree(L->s_case_code, s);
+    const uint64_t cap = std::min<uint64_t>((uint64_t)n, (uint64_t)(L->case_max - L->case_min) + 1);
+    PM4G_TRY(dalloc_t(&L->off, cap + 1, s));
+    PM4G_TRY(dalloc_t(&L->s_case_code, std::max<uint64_t>(cap, 1), s));
+    L->n_cases = -1;
+    if (n == 0) {
+        PM4G_LAUNCH("k_zero_cases", 0, s, k_zero_cases<<<1, 1, 0, s>>>(L->off, L->d_n_cases));
+        L->n_cases = 0;
+        return PM4G_OK;
     }
-#undef PM4G_SORT_CASE
+    switch (L->act_bytes) {
+        case 1: PM4G_TRY(sort_log_t<uint8_t>(L, s)); break;
+        case 2: PM4G_TRY(sort_log_t<uint16_t>(L, s)); break;
+        default: PM4G_TRY(sort_log_t<uint32_t>(L, s)); break;
+    }
     if (wi) PM4G_TRY(gather_extras(L, s));
     return PM4G_OK;
 }
 
-// generic (u64 key, u32 value) sort on `bits` low key bits, result in place
+// generic (u64 key, u32 value) stable sort on `bits` low key bits, in place
 pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, cudaStream_t s) {
     if (n <= 1) return PM4G_OK;
-    int passes = std::max(1, (std::min(bits, 64) + 7) / 8);
     Scratch out(s);
-    PM4G_TRY(out.alloc((size_t)n * 12));
+    PM4G_TRY(out.alloc((size_t)n * 12 + 16));
     uint64_t* ok = out.as<uint64_t>();
-    uint32_t* ov = (uint32_t*)((char*)out.p + (size_t)n * 8);
-    KeyParams kp{0, 0, 0};
-    PM4G_TRY((lsd_sort<uint32_t, false>(nullptr, nullptr, keys, vals, nullptr, ok, ov, nullptr, n,
-                                        passes, kp, s)));
+    uint32_t* ov = (uint32_t*)(ok + n);
+    PM4G_TRY((lsd_sort<uint64_t, uint32_t, false, false>(keys, nullptr, vals, nullptr, ok, nullptr, ov,
+                                                          nullptr, n, 0, std::max(1, std::min(bits, 64)), s)));
     PM4G_CK(cudaMemcpyAsync(keys, ok, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
     PM4G_CK(cudaMemcpyAsync(vals, ov, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
     return PM4G_OK;
