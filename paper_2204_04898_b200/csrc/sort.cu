@@ -8,20 +8,23 @@
 // in sorted order, the activity (and, with extra columns, the ingest row)
 // alongside, and the case offsets (CSR) of the cases dataframe.
 //
-// B200 design: a radix pass on B200 is instruction-issue bound
-// (6.5 TB/s over 148 SMs is 23 B per SM clock), so the number of passes is
-// what matters.  Instead of ceil(key_bits / 8) passes over the 60-bit
-// composite key we do
-//   1. a stable LSD "onesweep" radix sort on the CASE code only
-//      (ceil(case_bits / 8) passes, 4-byte keys, ts/act carried as payload):
-//      events end up grouped by case, in ingest order inside each case;
-//   2. one fused "format" kernel: per tile it finds case heads, ranks them
-//      with a decoupled look-back (-> case offsets), sorts every case by
-//      timestamp in shared memory (rank = #earlier-or-smaller, ties by
-//      position => stable) and writes the composite key.  Cases longer than a
-//      tile extension go to an exact fallback (a stable radix sort of that
-//      case's timestamps).
-// HBM bytes per event (u8 act, P case passes): hist 4 + P * 26 + format 22.
+// B200 design.  A radix pass on B200 is instruction-issue bound
+// (6.5 TB/s over 148 SMs is 23 B per SM clock), so the number of passes and
+// the number of arrays each pass moves are what matter:
+//   1. the composite key is built once, on the fly, by the first pass;
+//   2. a stable LSD "onesweep" radix sort runs over the CASE bits of the key
+//      only (digit shift = ts_bits + p * bits, ceil(case_bits / 8) passes):
+//      events end up grouped by case, in ingest order inside each case.  Each
+//      pass moves 8 B of key + the activity; tiles are fetched with TMA bulk
+//      copies (cp.async.bulk + mbarrier), ranked with ballots, published with
+//      a decoupled look-back, and written out in digit runs;
+//   3. one fused "format" kernel finds case heads, ranks them (look-back ->
+//      case offsets), and sorts every case by timestamp in shared memory
+//      (rank = #smaller-or-equal-earlier, so ties keep ingest order).  Cases
+//      longer than FMT_WARP_MAX (or running too far past a tile) go to an
+//      exact fallback: a stable radix sort of that case's keys.
+// HBM bytes per event (u8 act, P case passes): hist 4 + (13 + 9) + (P-1) * 18
+// + format 18 (+ 8 per case).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,20 +35,28 @@
 namespace pm4g {
 
 constexpr int RADIX = 256;
-constexpr int SORT_THREADS = 256;
+constexpr int SORT_THREADS = 512;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_IPT = 16;
+constexpr int SORT_IPT = 8;
 constexpr int SORT_TILE = SORT_THREADS * SORT_IPT;  // 4096
 constexpr int MAX_PASSES = 8;
+
+struct KeyParams {
+    uint32_t case_min;
+    int64_t ts_min;
+    int ts_bits;
+};
 
 __host__ __device__ inline uint64_t make_key(uint64_t case_rel, int64_t t, int64_t ts_min, int ts_bits) {
     return (ts_bits >= 64 ? 0 : (case_rel << ts_bits)) | ((uint64_t)t - (uint64_t)ts_min);
 }
 
 // ------------------------------------------------------------------ histograms
-// digit p of a key = ((key - sub) >> (p * bits)) & ((1 << bits) - 1)
-template <class K>
-__global__ __launch_bounds__(256) void k_hist(const K* __restrict__ keys, int64_t n, K sub, int bits,
+// digit p of an item = (field >> (p * bits)) & mask, where field = case - case_min
+// (FROM_COLS: read from the case column) or key >> shift0.
+template <bool FROM_COLS>
+__global__ __launch_bounds__(256) void k_hist(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ cs,
+                                              int64_t n, uint32_t case_min, int shift0, int bits,
                                               int passes, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[MAX_PASSES][RADIX];
     for (int i = threadIdx.x; i < MAX_PASSES * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
@@ -53,8 +64,8 @@ __global__ __launch_bounds__(256) void k_hist(const K* __restrict__ keys, int64_
     const uint32_t mask = (1u << bits) - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        K k = keys[i] - sub;
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(k >> (p * bits)) & mask], 1u);
+        const uint64_t f = FROM_COLS ? (uint64_t)(cs[i] - case_min) : shr64(keys[i], shift0);
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(f >> (p * bits)) & mask], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * RADIX; i += blockDim.x) {
@@ -76,69 +87,123 @@ __global__ void k_hist_scan(const uint32_t* __restrict__ hist, uint32_t* __restr
 }
 
 // ------------------------------------------------------------------ one onesweep pass
-// Stable scatter of (key, [ts], act-like payload, [idx]) by one digit.
-template <class K, class P, bool HAS_TS, bool WITH_IDX>
+// Stable scatter of (u64 key, payload P [, u32 ingest row]) by one digit of
+// the key.  FROM_COLS: the key is built from the raw (case, ts) columns.
+template <class P, bool FROM_COLS, bool WITH_IDX>
 struct PassArgs {
-    const K* in_key;
+    const uint64_t* in_key;
+    const uint32_t* in_case;
     const int64_t* in_ts;
     const P* in_act;
     const uint32_t* in_idx;   // nullptr with WITH_IDX: generate the ingest row
-    K* out_key;
-    int64_t* out_ts;
+    uint64_t* out_key;
     P* out_act;
     uint32_t* out_idx;
     int64_t n;
-    K sub;                    // subtracted from every input key (case_min in pass 0)
     int shift, bits;
+    KeyParams kp;
     const uint32_t* bucket_off;  // [256]
     uint32_t* status;            // [tiles * 256]
     uint32_t* tile_counter;
+    bool aligned;                // every input array 16-byte aligned (TMA bulk path)
 };
 
-template <class K, class P, bool HAS_TS, bool WITH_IDX>
-__global__ __launch_bounds__(SORT_THREADS, 3) void k_onesweep(PassArgs<K, P, HAS_TS, WITH_IDX> a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    K* s_key = (K*)smem;
-    int64_t* s_ts = (int64_t*)(smem + SORT_TILE * sizeof(K));
-    uint32_t* s_idx = (uint32_t*)(smem + SORT_TILE * (sizeof(K) + (HAS_TS ? 8 : 0)));
-    P* s_act = (P*)(smem + SORT_TILE * (sizeof(K) + (HAS_TS ? 8 : 0) + (WITH_IDX ? 4 : 0)));
+// Shared-memory layout of one tile (all offsets multiples of 16):
+//   u_case[T] u_ts[T] (FROM_COLS) | u_key[T];  u_idx[T];  u_act[T]  -- as loaded
+//   s_src[T]                      -- slot (in the loaded tile) of the i-th key in digit order
+// (FROM_COLS keeps the built keys in u_key over the consumed u_ts.)
+template <class P, bool FROM_COLS, bool WITH_IDX>
+struct OsLayout {
+    static constexpr size_t T = SORT_TILE;
+    static constexpr size_t o_in = 0;                                   // u_key or u_ts
+    static constexpr size_t o_case = o_in + T * 8;                      // FROM_COLS only
+    static constexpr size_t o_idx = o_case + (FROM_COLS ? T * 4 : 0);
+    static constexpr size_t o_act = o_idx + (WITH_IDX ? T * 4 : 0);
+    static constexpr size_t o_src = (o_act + T * sizeof(P) + 15) / 16 * 16;
+    static constexpr size_t bytes = o_src + T * 2;
+};
+
+template <class P, bool FROM_COLS, bool WITH_IDX>
+__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
+    using Lay = OsLayout<P, FROM_COLS, WITH_IDX>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* u_key = (uint64_t*)(smem + Lay::o_in);
+    int64_t* u_ts = (int64_t*)(smem + Lay::o_in);
+    uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
+    uint32_t* u_idx = (uint32_t*)(smem + Lay::o_idx);
+    P* u_act = (P*)(smem + Lay::o_act);
+    uint16_t* s_src = (uint16_t*)(smem + Lay::o_src);
     __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
     __shared__ uint32_t s_start[RADIX];
     __shared__ long long s_gbase[RADIX];
     __shared__ uint32_t s_scan[SORT_WARPS + 1];
     __shared__ uint32_t s_tile;
+    __shared__ __align__(8) uint64_t s_bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+    if (tid == 0) {
+        s_tile = atomicAdd(a.tile_counter, 1u);
+        mbar_init(&s_bar, 1);
+    }
     for (int i = tid; i < SORT_WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const int64_t base = (int64_t)tile * SORT_TILE;
-    const int64_t wbase = base + warp * (32 * SORT_IPT);
+    const int64_t nv64 = a.n - base;
+    const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
     const uint32_t dmask = (1u << a.bits) - 1;
+    const bool gen_idx = WITH_IDX && a.in_idx == nullptr;
 
-    K k[SORT_IPT];
-#pragma unroll
-    for (int j = 0; j < SORT_IPT; ++j) {
-        int64_t i = wbase + j * 32 + lane;
-        k[j] = i < a.n ? (K)(a.in_key[i] - a.sub) : (K)~(K)0;
+    // ---- tile load: TMA bulk copies for full aligned tiles, plain loads otherwise
+    if (nvalid == SORT_TILE && a.aligned) {
+        if (tid == 0) {
+            const uint32_t bytes = SORT_TILE * (uint32_t)(8 + sizeof(P) + (FROM_COLS ? 4 : 0) +
+                                                          ((WITH_IDX && !gen_idx) ? 4 : 0));
+            mbar_expect_tx(&s_bar, bytes);
+            if (FROM_COLS) {
+                tma_load_1d(u_ts, a.in_ts + base, SORT_TILE * 8, &s_bar);
+                tma_load_1d(u_case, a.in_case + base, SORT_TILE * 4, &s_bar);
+            } else {
+                tma_load_1d(u_key, a.in_key + base, SORT_TILE * 8, &s_bar);
+            }
+            if (WITH_IDX && !gen_idx) tma_load_1d(u_idx, a.in_idx + base, SORT_TILE * 4, &s_bar);
+            tma_load_1d(u_act, a.in_act + base, SORT_TILE * sizeof(P), &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
+    } else {
+        for (uint32_t i = tid; i < nvalid; i += SORT_THREADS) {
+            if (FROM_COLS) {
+                u_ts[i] = a.in_ts[base + i];
+                u_case[i] = a.in_case[base + i];
+            } else {
+                u_key[i] = a.in_key[base + i];
+            }
+            if (WITH_IDX && !gen_idx) u_idx[i] = a.in_idx[base + i];
+            u_act[i] = a.in_act[base + i];
+        }
+        __syncthreads();
     }
 
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
     // Peers (lanes holding the same digit) from one ballot per digit bit.
+    uint64_t k[SORT_IPT];
     uint32_t pos[SORT_IPT];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
-        const uint32_t d = (uint32_t)(k[j] >> a.shift) & dmask;
+        const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
+        if (li < nvalid)
+            k[j] = FROM_COLS ? make_key(u_case[li] - a.kp.case_min, u_ts[li], a.kp.ts_min, a.kp.ts_bits)
+                             : u_key[li];
+        else
+            k[j] = ~0ull;
+        const uint32_t d = li < nvalid ? (uint32_t)shr64(k[j], a.shift) & dmask : dmask;
         uint32_t peers = 0xffffffffu;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            if (b < a.bits) {
-                const bool bit = (d >> b) & 1u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bal : ~bal;
-            }
+        for (int b = 0; b < 8; ++b) {   // bits above a.bits are 0 in every lane: no-ops
+            const bool bit = (d >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
         }
         const int leader = __ffs(peers) - 1;
         uint32_t bse = 0;
@@ -150,52 +215,51 @@ __global__ __launch_bounds__(SORT_THREADS, 3) void k_onesweep(PassArgs<K, P, HAS
         pos[j] = bse + __popc(peers & lt);
         __syncwarp();
     }
+    // FROM_COLS: the built keys replace the consumed timestamps in smem
+    if (FROM_COLS) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < SORT_IPT; ++j) u_key[warp * (32 * SORT_IPT) + j * 32 + lane] = k[j];
+    }
     __syncthreads();
 
-    // ---- per-digit totals and warp-exclusive prefixes (thread == digit)
+    // ---- per-digit totals and warp-exclusive prefixes (thread == digit, tid < 256)
     const int d = tid;
+    const bool dig = tid < RADIX && d <= (int)dmask;
     uint32_t tot = 0;
-#pragma unroll
-    for (int w = 0; w < SORT_WARPS; ++w) {
-        uint32_t c = s_whist[w][d];
-        s_whist[w][d] = tot;
-        tot += c;
-    }
-    // invalid items (only in the last tile) carry the all-ones digit and rank
-    // last; they are not part of the published counts
-    const int64_t nv64 = a.n - base;
-    const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
-    uint32_t pub = tot;
-    if (d == (int)dmask) pub -= (SORT_TILE - nvalid);
     uint32_t* st = a.status + (size_t)tile * RADIX + d;
-    if (d <= (int)dmask) {
-        if (tile == 0) st_volatile(st, ST_INC | pub);
-        else st_volatile(st, ST_AGG | pub);
+    uint32_t pub = 0;
+    if (tid < RADIX) {
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; ++w) {
+            uint32_t c = s_whist[w][d];
+            s_whist[w][d] = tot;
+            tot += c;
+        }
+        // invalid items (only in the last tile) carry the all-ones digit and
+        // rank last; they are not part of the published counts
+        pub = tot;
+        if (d == (int)dmask) pub -= (SORT_TILE - nvalid);
+        if (dig) {
+            if (tile == 0) st_volatile(st, ST_INC | pub);
+            else st_volatile(st, ST_AGG | pub);
+        }
     }
     const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, nullptr);
-    s_start[d] = start;
+    if (tid < RADIX) s_start[d] = start;
     __syncthreads();
 
-    // ---- scatter keys and payloads into smem in digit order (payload loads
-    // are issued here, after ranking, so they never occupy registers earlier)
+    // ---- keys (and their source slot) into smem in digit order
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
-        const uint32_t dd = (uint32_t)(k[j] >> a.shift) & dmask;
-        pos[j] += s_start[dd] + s_whist[warp][dd];
-        s_key[pos[j]] = k[j];
-    }
-#pragma unroll
-    for (int j = 0; j < SORT_IPT; ++j) {
-        const int64_t i = wbase + j * 32 + lane;
-        if (i < a.n) {
-            if (HAS_TS) s_ts[pos[j]] = a.in_ts[i];
-            s_act[pos[j]] = a.in_act[i];
-            if (WITH_IDX) s_idx[pos[j]] = a.in_idx ? a.in_idx[i] : (uint32_t)i;
-        }
+        const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
+        const uint32_t dd = li < nvalid ? (uint32_t)shr64(k[j], a.shift) & dmask : dmask;
+        const uint32_t p = pos[j] + s_start[dd] + s_whist[warp][dd];
+        s_src[p] = (uint16_t)li;
     }
 
     // ---- decoupled look-back for this digit, 4 predecessors per round trip
-    if (d <= (int)dmask) {
+    if (dig) {
         uint32_t prefix = 0;
         if (tile > 0) {
             int64_t p = (int64_t)tile - 1;
@@ -220,43 +284,50 @@ __global__ __launch_bounds__(SORT_THREADS, 3) void k_onesweep(PassArgs<K, P, HAS
     }
     __syncthreads();
 
-    // ---- coalesced write-out: consecutive threads, consecutive positions
-#pragma unroll
+    // ---- coalesced write-out: consecutive threads, consecutive positions;
+    // payloads are gathered from the loaded tile through s_src
+#pragma unroll 4
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t sidx = j * SORT_THREADS + tid;
         if (sidx < nvalid) {
-            const K kk = s_key[sidx];
-            const long long g = s_gbase[(uint32_t)(kk >> a.shift) & dmask] + sidx;
+            const uint32_t src = s_src[sidx];
+            const uint64_t kk = u_key[src];
+            const long long g = s_gbase[(uint32_t)shr64(kk, a.shift) & dmask] + sidx;
             a.out_key[g] = kk;
-            if (HAS_TS) a.out_ts[g] = s_ts[sidx];
-            a.out_act[g] = s_act[sidx];
-            if (WITH_IDX) a.out_idx[g] = s_idx[sidx];
+            a.out_act[g] = u_act[src];
+            if (WITH_IDX) a.out_idx[g] = gen_idx ? (uint32_t)(base + src) : u_idx[src];
         }
     }
 }
 
-template <class K, class P, bool TS, bool WI>
-static pm4g_status launch_pass(const PassArgs<K, P, TS, WI>& args, int64_t tiles, cudaStream_t s,
+template <class P, bool FC, bool WI>
+static pm4g_status launch_pass(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                const char* name, double bytes) {
-    const size_t smem = (size_t)SORT_TILE * (sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P));
+    const size_t smem = OsLayout<P, FC, WI>::bytes;
     static bool attr = false;
     if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_onesweep<K, P, TS, WI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PM4G_CK(cudaFuncSetAttribute(k_onesweep<P, FC, WI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
         attr = true;
     }
-    PM4G_LAUNCH(name, bytes, s, (k_onesweep<K, P, TS, WI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
+    PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
     return PM4G_OK;
 }
 
-// Stable LSD sort of `bits_total` low bits of (key - sub), payloads carried.
-// Result lands in the *_out buffers; tmp holds the ping-pong copy.
-template <class K, class P, bool TS, bool WI>
-static pm4g_status lsd_sort(const K* key_in, const int64_t* ts_in, const P* act_in,
-                            const uint32_t* idx_in, K* key_out, int64_t* ts_out, P* act_out,
-                            uint32_t* idx_out, int64_t n, K sub, int bits_total, cudaStream_t s) {
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// Stable LSD sort on `bits_total` bits of the key starting at bit `shift0`.
+// Input: either raw columns (in_case/in_ts, key built on the fly) or keys.
+// Result lands in the *_out buffers.
+template <class P, bool WI>
+static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const uint64_t* in_key,
+                            const P* in_act, const uint32_t* in_idx, uint64_t* key_out, P* act_out,
+                            uint32_t* idx_out, int64_t n, int shift0, int bits_total, KeyParams kp,
+                            cudaStream_t s) {
+    const bool from_cols = in_case != nullptr;
+    bits_total = std::max(1, bits_total);
     const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
-    const int bits = std::max(1, (bits_total + passes - 1) / passes);
+    const int bits = (bits_total + passes - 1) / passes;
     const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
     Scratch aux(s), tmp(s);
     const size_t status_words = (size_t)tiles * RADIX * passes;
@@ -268,64 +339,66 @@ static pm4g_status lsd_sort(const K* key_in, const int64_t* ts_in, const P* act_
     PM4G_CK(cudaMemsetAsync(status, 0, (status_words + passes + MAX_PASSES * RADIX) * 4, s));
     {
         const int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 4));
-        PM4G_LAUNCH("k_hist", n * (double)sizeof(K), s,
-                    (k_hist<K><<<g, 256, 0, s>>>(key_in, n, sub, bits, passes, hist)));
+        if (from_cols)
+            PM4G_LAUNCH("k_hist", n * 4.0, s,
+                        (k_hist<true><<<g, 256, 0, s>>>(nullptr, in_case, n, kp.case_min, 0, bits, passes, hist)));
+        else
+            PM4G_LAUNCH("k_hist", n * 8.0, s,
+                        (k_hist<false><<<g, 256, 0, s>>>(in_key, nullptr, n, 0, shift0, bits, passes, hist)));
         PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(hist, off, passes));
     }
-    const size_t per = (size_t)n * (sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P));
-    PM4G_TRY(tmp.alloc(per + 64));
-    // aligned sub-arrays: ts (8) | key | idx | act
-    char* tp = (char*)tmp.p;
-    int64_t* tts = (int64_t*)tp;
-    K* tkey = (K*)(tp + (TS ? (size_t)n * 8 : 0));
-    uint32_t* tidx = (uint32_t*)((char*)tkey + (size_t)n * sizeof(K));
+    // ping-pong buffer: key (8n) | idx (4n) | act
+    PM4G_TRY(tmp.alloc((size_t)n * (8 + (WI ? 4 : 0) + sizeof(P)) + 64));
+    uint64_t* tkey = tmp.as<uint64_t>();
+    uint32_t* tidx = (uint32_t*)(tkey + n);
     P* tact = (P*)((char*)tidx + (WI ? (size_t)n * 4 : 0));
-    const K* ck = key_in;
-    const int64_t* ct = ts_in;
-    const P* ca = act_in;
-    const uint32_t* ci = idx_in;
-    K csub = sub;
-    const double row = (double)sizeof(K) + (TS ? 8 : 0) + (WI ? 4 : 0) + sizeof(P);
+    const uint64_t* ck = in_key;
+    const P* ca = in_act;
+    const uint32_t* ci = in_idx;
     for (int p = 0; p < passes; ++p) {
         const bool to_out = ((passes - 1 - p) % 2) == 0;
-        PassArgs<K, P, TS, WI> a{ck, ct, ca, ci,
-                                 to_out ? key_out : tkey, to_out ? ts_out : tts,
-                                 to_out ? act_out : tact, to_out ? idx_out : tidx,
-                                 n, csub, p * bits, bits, off + p * RADIX,
-                                 status + (size_t)p * tiles * RADIX, counters + p};
-        const double bytes = (double)n * (row - ((WI && !ci) ? 4 : 0) + row);
-        PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", bytes));
-        ck = a.out_key;
-        ct = a.out_ts;
-        ca = a.out_act;
-        ci = a.out_idx;
-        csub = 0;
+        uint64_t* ok = to_out ? key_out : tkey;
+        P* oa = to_out ? act_out : tact;
+        uint32_t* oi = to_out ? idx_out : tidx;
+        const int shift = shift0 + p * bits;
+        const double wr = 8.0 + sizeof(P) + (WI ? 4 : 0);
+        if (p == 0 && from_cols) {
+            PassArgs<P, true, WI> a{nullptr, in_case, in_ts, ca, ci, ok, oa, oi, n, shift, bits, kp,
+                                    off, status, counters,
+                                    aligned16(in_case) && aligned16(in_ts) && aligned16(ca) &&
+                                        (!ci || aligned16(ci))};
+            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
+        } else {
+            PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, shift, bits, kp,
+                                     off + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p,
+                                     aligned16(ck) && aligned16(ca) && (!ci || aligned16(ci))};
+            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr)));
+        }
+        ck = ok;
+        ca = oa;
+        ci = oi;
     }
     return PM4G_OK;
 }
 
 // ------------------------------------------------------------------ A4 + format
-// Input: events grouped by case (stable), case_rel = gcase[i] - case_sub.
+// Input: composite keys grouped by case (stable), activity (+ ingest row).
 // Per tile of 4096 positions: heads (case starts) -> ranks via look-back ->
-// case offsets; each case owned by this tile (head inside it) is sorted by
-// timestamp in shared memory and written as composite keys.  A case may run up
-// to FMT_EXT positions past the tile end; longer ones are "big" cases handled
-// by format_big().
+// case offsets; each case owned by this tile (head inside it) is sorted by key
+// in shared memory.  A case may run up to FMT_EXT positions past the tile end;
+// longer ones (and cases over FMT_WARP_MAX rows) go to the exact fallback.
 constexpr int FMT_THREADS = 256, FMT_IPT = 16, FMT_TILE = FMT_THREADS * FMT_IPT;
 constexpr int FMT_EXT = 1024, FMT_BUF = FMT_TILE + FMT_EXT;
 constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
 
 template <class P>
 struct FmtArgs {
-    const uint32_t* gcase;
-    const int64_t* gts;
+    const uint64_t* gkey;
     const P* gact;
-    const uint32_t* gidx;      // nullptr: ingest row = position (no LSD passes ran)
+    const uint32_t* gidx;
     int64_t n;
-    uint32_t case_sub;
-    uint32_t case_min;
-    int64_t ts_min;
     int ts_bits;
+    uint32_t case_min;
     uint64_t* key_out;
     P* act_out;
     uint32_t* perm_out;        // nullptr: no extra columns
@@ -334,7 +407,7 @@ struct FmtArgs {
     uint64_t* n_cases;
     uint32_t* status;
     uint32_t* counter;
-    uint32_t* big;             // [cap] ranks of big cases
+    uint32_t* big;             // ranks of fallback cases
     uint32_t* big_count;
 };
 
@@ -348,7 +421,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     P* s_act = (P*)(s_head + FMT_TILE + 8);                        // [FMT_BUF]
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
-    __shared__ uint32_t s_prefix, s_H;
+    __shared__ uint32_t s_prefix;
     __shared__ int s_ext;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -358,19 +431,23 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     const int64_t base = (int64_t)tile * FMT_TILE;
     const int tn = (int)min((int64_t)FMT_TILE, a.n - base);
     const int64_t wbase = base + warp * (32 * FMT_IPT);
+    const int tb = a.ts_bits;
 
-    // ---- heads: case(i) != case(i-1)
+    // ---- load the tile's keys (coalesced, warp-striped) and find the heads
     uint32_t ball[FMT_IPT], wc = 0;
     {
-        uint32_t prev = 0;
+        uint64_t prev = 0;
         const int64_t pi = wbase - 1;
-        if (pi >= 0 && pi < a.n) prev = a.gcase[pi];
+        if (pi >= 0 && pi < a.n) prev = shr64(a.gkey[pi], tb);
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
-            const int64_t i = wbase + j * 32 + lane;
+            const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
+            const int64_t i = base + li;
             const bool ok = i < a.n;
-            const uint32_t c = ok ? a.gcase[i] : 0u;
-            uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+            const uint64_t kk = ok ? a.gkey[i] : 0ull;
+            if (ok) s_key[li] = kk;
+            const uint64_t c = shr64(kk, tb);
+            uint64_t pc = __shfl_up_sync(0xffffffffu, c, 1);
             if (lane == 0) pc = prev;
             prev = __shfl_sync(0xffffffffu, c, 31);
             ball[j] = __ballot_sync(0xffffffffu, ok && (i == 0 || c != pc));
@@ -399,15 +476,16 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     __syncthreads();
     const uint32_t R0 = s_prefix;
 
-    // ---- extent of the last owned case past the tile end
+    // ---- extent of the last owned case past the tile end (warp 0), while the
+    // other warps publish the case offsets and codes of every head
     if (warp == 0) {
         int ext = 0;
         if (H > 0 && base + tn < a.n) {
-            const uint32_t last = a.gcase[base + s_head[H - 1]];
+            const uint64_t last = shr64(s_key[s_head[H - 1]], tb);
             ext = -1;
             for (int o = 0; o <= FMT_EXT; o += 32) {
                 const int64_t i = base + tn + o + lane;
-                const bool stop = i >= a.n || a.gcase[i] != last;
+                const bool stop = i >= a.n || shr64(a.gkey[i], tb) != last;
                 const uint32_t b = __ballot_sync(0xffffffffu, stop);
                 if (b) {
                     const int e = o + __ffs(b) - 1;
@@ -416,16 +494,13 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
                 }
             }
         }
-        if (lane == 0) {
-            s_ext = ext;
-            s_H = H;
+        if (lane == 0) s_ext = ext;
+    } else {
+        for (uint32_t h = tid - 32; h < H; h += FMT_THREADS - 32) {
+            const int hp = s_head[h];
+            a.off[R0 + h] = (uint32_t)(base + hp);
+            a.case_code[R0 + h] = a.case_min + (uint32_t)shr64(s_key[hp], tb);
         }
-    }
-    // case offsets and codes of every head in the tile
-    for (uint32_t h = tid; h < H; h += FMT_THREADS) {
-        const int64_t i = base + s_head[h];
-        a.off[R0 + h] = (uint32_t)i;
-        a.case_code[R0 + h] = a.case_min + (a.gcase[i] - a.case_sub);
     }
     if (tid == 0 && base + tn >= a.n) {
         a.off[R0 + H] = (uint32_t)a.n;
@@ -435,7 +510,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     if (H == 0) return;
     int ext = s_ext;
     uint32_t Hown = H;                 // cases this tile sorts here
-    if (ext < 0) {                     // last case is big: exact fallback after the kernel
+    if (ext < 0) {                     // last case runs far past the tile: fallback
         if (tid == 0) a.big[atomicAdd(a.big_count, 1u)] = R0 + H - 1;
         Hown = H - 1;
         ext = 0;
@@ -443,20 +518,14 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     const int h0 = s_head[0];
     const int oend = Hown == H ? tn + ext : (int)s_head[H - 1];   // owned local range [h0, oend)
 
-    // ---- stage the owned range: composite keys, activities, ingest rows
+    // ---- stage the owned range (keys of the tile are already in smem)
     for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
         const int64_t i = base + p;
-        const uint64_t cr = a.gcase[i] - a.case_sub;
-        s_key[p] = make_key(cr, a.gts[i], a.ts_min, a.ts_bits);
+        if (p >= tn) s_key[p] = a.gkey[i];
         s_act[p] = a.gact[i];
-        if (WI) s_idx[p] = a.gidx ? a.gidx[i] : (uint32_t)i;
+        if (WI) s_idx[p] = a.gidx[i];
     }
-    __syncthreads();
-
-    // ---- rank every event inside its case: #(key_j < key_i or (== and j < i)).
-    // Event-parallel: each thread ranks one row against its own case, so work
-    // is balanced across threads and a warp (mostly one case) reads s_key[j]
-    // as a broadcast.  Cases longer than FMT_WARP_MAX go to the exact fallback.
+    // case index of every owned row; long cases -> fallback
     for (uint32_t h = tid; h < Hown; h += FMT_THREADS) {
         const int s0 = s_head[h], e0 = (h + 1 < Hown) ? s_head[h + 1] : oend;
         const bool big = e0 - s0 > FMT_WARP_MAX;
@@ -464,6 +533,10 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         for (int p = s0; p < e0; ++p) s_ci[p] = big ? (uint16_t)0xffff : (uint16_t)h;
     }
     __syncthreads();
+
+    // ---- rank every row inside its case: #(key_j < key_i or (== and j < i)).
+    // Event-parallel, so work is balanced and a warp (mostly one case) reads
+    // s_key[j] as a broadcast.
     for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
         const uint32_t h = s_ci[p];
         if (h == 0xffff) {
@@ -491,28 +564,27 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     }
 }
 
-// big cases: stable radix sort of the case's timestamps, then gather
-template <class P>
-__global__ void k_big_keys(const int64_t* __restrict__ gts, int64_t start, int64_t len, int64_t ts_min,
+// fallback cases: stable radix sort of the case's keys, then gather payloads
+__global__ void k_big_keys(const uint64_t* __restrict__ gkey, int64_t start, int64_t len,
                            uint64_t* __restrict__ k, uint32_t* __restrict__ v) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
-        k[q] = (uint64_t)gts[start + q] - (uint64_t)ts_min;
+        k[q] = gkey[start + q];
         v[q] = (uint32_t)q;
     }
 }
 template <class P>
-__global__ void k_big_gather(FmtArgs<P> a, int64_t start, int64_t len, uint64_t case_rel,
+__global__ void k_big_gather(FmtArgs<P> a, int64_t start, int64_t len, const uint64_t* __restrict__ k,
                              const uint32_t* __restrict__ v) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t src = start + v[q];
-        a.key_out[start + q] = make_key(case_rel, a.gts[src], a.ts_min, a.ts_bits);
+        a.key_out[start + q] = k[q];
         a.act_out[start + q] = a.gact[src];
-        if (a.perm_out) a.perm_out[start + q] = a.gidx ? a.gidx[src] : (uint32_t)src;
+        if (a.perm_out) a.perm_out[start + q] = a.gidx[src];
     }
 }
 
 template <class P>
-static pm4g_status format_log(pm4g_log* L, const FmtArgs<P>& fa0, cudaStream_t s) {
+static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
     FmtArgs<P> fa = fa0;
     const int64_t n = fa.n;
     const int64_t tiles = (n + FMT_TILE - 1) / FMT_TILE;
@@ -525,18 +597,16 @@ static pm4g_status format_log(pm4g_log* L, const FmtArgs<P>& fa0, cudaStream_t s
     fa.status = fa.counter + 2;
     fa.big = fa.status + tiles;
     const bool wi = fa.perm_out != nullptr;
-    const size_t smem = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + 16 +
-                        (wi ? (size_t)FMT_BUF * 4 : 0);
+    const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + 16;
+    const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0);
     static bool attr = false;
     if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_format<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(smem + (wi ? 0 : (size_t)FMT_BUF * 4))));
+        PM4G_CK(cudaFuncSetAttribute(k_format<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_base));
         PM4G_CK(cudaFuncSetAttribute(k_format<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(smem + (wi ? 0 : (size_t)FMT_BUF * 4))));
+                                     (int)(smem_base + (size_t)FMT_BUF * 4)));
         attr = true;
     }
-    const double bytes = (double)n * (4 + 8 + sizeof(P) + (fa.gidx ? 4 : 0) + 8 + sizeof(P) +
-                                      (fa.perm_out ? 4 : 0));
+    const double bytes = (double)n * (2.0 * (8 + sizeof(P) + (wi ? 4 : 0)));
     if (wi)
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
     else
@@ -550,9 +620,7 @@ static pm4g_status format_log(pm4g_log* L, const FmtArgs<P>& fa0, cudaStream_t s
     PM4G_CK(cudaStreamSynchronize(s));
     for (uint32_t r : ranks) {
         uint32_t se[2];
-        uint32_t code = 0;
         PM4G_CK(cudaMemcpyAsync(se, fa.off + r, 8, cudaMemcpyDeviceToHost, s));
-        PM4G_CK(cudaMemcpyAsync(&code, fa.case_code + r, 4, cudaMemcpyDeviceToHost, s));
         PM4G_CK(cudaStreamSynchronize(s));
         const int64_t start = se[0], len = (int64_t)se[1] - se[0];
         Scratch kv(s);
@@ -560,12 +628,10 @@ static pm4g_status format_log(pm4g_log* L, const FmtArgs<P>& fa0, cudaStream_t s
         uint64_t* k = kv.as<uint64_t>();
         uint32_t* v = (uint32_t*)(k + len);
         const int g = std::max(1, std::min<int>((int)((len + 255) / 256), num_sms() * 4));
-        PM4G_LAUNCH("k_big_keys", len * 20.0, s, (k_big_keys<P><<<g, 256, 0, s>>>(fa.gts, start, len, fa.ts_min, k, v)));
+        PM4G_LAUNCH("k_big_keys", len * 20.0, s, (k_big_keys<<<g, 256, 0, s>>>(fa.gkey, start, len, k, v)));
         PM4G_TRY(radix_sort_u64(k, v, len, std::min(64, std::max(1, fa.ts_bits)), s));
-        PM4G_LAUNCH("k_big_gather", len * 30.0, s,
-                    (k_big_gather<P><<<g, 256, 0, s>>>(fa, start, len, (uint64_t)(code - fa.case_min), v)));
+        PM4G_LAUNCH("k_big_gather", len * 30.0, s, (k_big_gather<P><<<g, 256, 0, s>>>(fa, start, len, k, v)));
     }
-    (void)L;
     return PM4G_OK;
 }
 
@@ -573,46 +639,34 @@ template <class P>
 static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
     const int64_t n = L->n;
     const bool wi = !L->extra.empty();
+    KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
+    // 1. stable LSD passes over the case bits of the composite key (built on the fly)
+    Scratch grp(s);
+    PM4G_TRY(grp.alloc((size_t)n * (8 + (wi ? 4 : 0) + sizeof(P)) + 64));
+    uint64_t* gkey = grp.as<uint64_t>();
+    uint32_t* gidx = (uint32_t*)(gkey + n);
+    P* gact = (P*)((char*)gidx + (wi ? (size_t)n * 4 : 0));
+    if (wi)
+        PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, gidx, n,
+                                    L->ts_bits, L->case_bits, kp, s)));
+    else
+        PM4G_TRY((lsd_sort<P, false>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, nullptr,
+                                     n, L->ts_bits, L->case_bits, kp, s)));
+    // 2. per-case timestamp order + case offsets
     FmtArgs<P> fa{};
+    fa.gkey = gkey;
+    fa.gact = gact;
+    fa.gidx = wi ? gidx : nullptr;
     fa.n = n;
-    fa.case_min = L->case_min;
-    fa.ts_min = L->ts_min;
     fa.ts_bits = L->ts_bits;
+    fa.case_min = L->case_min;
     fa.key_out = L->key;
     fa.act_out = (P*)L->s_act;
     fa.perm_out = wi ? L->perm : nullptr;
     fa.off = L->off;
     fa.case_code = L->s_case_code;
     fa.n_cases = L->d_n_cases;
-    Scratch grp(s);
-    if (L->case_bits == 0) {           // a single case code: already grouped
-        fa.gcase = L->case_;
-        fa.gts = L->ts;
-        fa.gact = (const P*)L->act;
-        fa.gidx = nullptr;
-        fa.case_sub = L->case_min;
-        return format_log<P>(L, fa, s);
-    }
-    // stable LSD passes on the case code; ts / act (/ ingest row) ride along
-    const size_t per = (size_t)n * (4 + 8 + (wi ? 4 : 0) + sizeof(P));
-    PM4G_TRY(grp.alloc(per + 64));
-    char* gp = (char*)grp.p;
-    int64_t* gts = (int64_t*)gp;
-    uint32_t* gcase = (uint32_t*)(gp + (size_t)n * 8);
-    uint32_t* gidx = gcase + n;
-    P* gact = (P*)((char*)gidx + (wi ? (size_t)n * 4 : 0));
-    if (wi)
-        PM4G_TRY((lsd_sort<uint32_t, P, true, true>(L->case_, L->ts, (const P*)L->act, nullptr, gcase, gts,
-                                                     gact, gidx, n, L->case_min, L->case_bits, s)));
-    else
-        PM4G_TRY((lsd_sort<uint32_t, P, true, false>(L->case_, L->ts, (const P*)L->act, nullptr, gcase, gts,
-                                                      gact, nullptr, n, L->case_min, L->case_bits, s)));
-    fa.gcase = gcase;
-    fa.gts = gts;
-    fa.gact = gact;
-    fa.gidx = wi ? gidx : nullptr;
-    fa.case_sub = 0;
-    return format_log<P>(L, fa, s);
+    return format_log<P>(fa, s);
 }
 
 // ------------------------------------------------------------------ A4 segments
@@ -791,8 +845,9 @@ pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, 
     PM4G_TRY(out.alloc((size_t)n * 12 + 16));
     uint64_t* ok = out.as<uint64_t>();
     uint32_t* ov = (uint32_t*)(ok + n);
-    PM4G_TRY((lsd_sort<uint64_t, uint32_t, false, false>(keys, nullptr, vals, nullptr, ok, nullptr, ov,
-                                                          nullptr, n, 0, std::max(1, std::min(bits, 64)), s)));
+    KeyParams kp{0, 0, 0};
+    PM4G_TRY((lsd_sort<uint32_t, false>(nullptr, nullptr, keys, vals, nullptr, ok, ov, nullptr, n, 0,
+                                        std::max(1, std::min(bits, 64)), kp, s)));
     PM4G_CK(cudaMemcpyAsync(keys, ok, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
     PM4G_CK(cudaMemcpyAsync(vals, ov, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
     return PM4G_OK;
