@@ -242,6 +242,33 @@ __device__ __forceinline__ uint32_t lookback_warp(uint32_t* status, uint32_t til
     return prefix;
 }
 
+// Same walk for a tile that already published its aggregate (flag AGG, or INC
+// for tile 0): resolves the exclusive prefix and publishes INC.  All 32 lanes.
+__device__ __forceinline__ uint32_t lookback_warp_inc(uint32_t* status, uint32_t tile,
+                                                      uint32_t aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) return 0;
+    uint32_t prefix = 0;
+    int64_t end = (int64_t)tile - 1;
+    while (true) {
+        const int64_t idx = end - lane;
+        uint32_t v = idx >= 0 ? ld_volatile(&status[idx]) : ST_INC;
+        while (__any_sync(0xffffffffu, (v >> 30) == 0)) {
+            if ((v >> 30) == 0) v = ld_volatile(&status[idx]);
+        }
+        const uint32_t inc = __ballot_sync(0xffffffffu, (v >> 30) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        uint32_t x = lane <= stop ? (v & ST_VAL) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        prefix += x;
+        if (inc) break;
+        end -= 32;
+    }
+    if (lane == 0) st_volatile(&status[tile], ST_INC | (prefix + aggregate));
+    return prefix;
+}
+
 // Block-wide exclusive scan of one u32 per thread (BLOCK threads, multiple of 32).
 template <int BLOCK>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp, uint32_t* total) {

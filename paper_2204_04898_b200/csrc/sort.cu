@@ -388,7 +388,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
 // in shared memory.  A case may run up to FMT_EXT positions past the tile end;
 // longer ones (and cases over FMT_WARP_MAX rows) go to the exact fallback.
 constexpr int FMT_THREADS = 256, FMT_IPT = 16, FMT_TILE = FMT_THREADS * FMT_IPT;
-constexpr int FMT_EXT = 1024, FMT_BUF = FMT_TILE + FMT_EXT;
+constexpr int FMT_EXT = 512, FMT_BUF = FMT_TILE + FMT_EXT;
 constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
 
 template <class P>
@@ -430,20 +430,20 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     const uint32_t tile = s_tile;
     const int64_t base = (int64_t)tile * FMT_TILE;
     const int tn = (int)min((int64_t)FMT_TILE, a.n - base);
-    const int64_t wbase = base + warp * (32 * FMT_IPT);
     const int tb = a.ts_bits;
+    const uint32_t lt = lanemask_lt();
 
-    // ---- load the tile's keys (coalesced, warp-striped) and find the heads
+    // ---- 1. the tile's keys (coalesced, warp-striped) -> smem, head ballots
     uint32_t ball[FMT_IPT], wc = 0;
     {
         uint64_t prev = 0;
-        const int64_t pi = wbase - 1;
+        const int64_t pi = base + warp * (32 * FMT_IPT) - 1;
         if (pi >= 0 && pi < a.n) prev = shr64(a.gkey[pi], tb);
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
             const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
             const int64_t i = base + li;
-            const bool ok = i < a.n;
+            const bool ok = li < tn;
             const uint64_t kk = ok ? a.gkey[i] : 0ull;
             if (ok) s_key[li] = kk;
             const uint64_t c = shr64(kk, tb);
@@ -459,26 +459,26 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     uint32_t H;
     const uint32_t wex = block_excl_scan<FMT_THREADS>(tid < FMT_THREADS / 32 ? s_wt[tid] : 0u, s_scan, &H);
     if (tid < FMT_THREADS / 32) s_wt[tid] = wex;
-    if (warp == 0) {
-        const uint32_t pf = lookback_warp(a.status, tile, H);
-        if (lane == 0) s_prefix = pf;
-    }
     __syncthreads();
+
+    // ---- 2. head list and the case index of every row of the tile
     {
-        const uint32_t lt = lanemask_lt();
         uint32_t r = s_wt[warp];
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
-            if (ball[j] & (1u << lane)) s_head[r + __popc(ball[j] & lt)] = (uint16_t)(warp * 32 * FMT_IPT + j * 32 + lane);
-            r += __popc(ball[j]);
+            const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
+            const uint32_t b = ball[j];
+            const uint32_t incl = r + __popc(b & (lt | (1u << lane)));   // heads at positions <= li
+            if (b & (1u << lane)) s_head[incl - 1] = (uint16_t)li;
+            if (li < tn) s_ci[li] = incl ? (uint16_t)(incl - 1) : (uint16_t)0xffff;  // 0xffff: previous tile's case
+            r += __popc(b);
         }
     }
     __syncthreads();
-    const uint32_t R0 = s_prefix;
 
-    // ---- extent of the last owned case past the tile end (warp 0), while the
-    // other warps publish the case offsets and codes of every head
+    // ---- 3. case ranks (warp 0 look-back) and the extent of the last case
     if (warp == 0) {
+        const uint32_t pf = lookback_warp(a.status, tile, H);
         int ext = 0;
         if (H > 0 && base + tn < a.n) {
             const uint64_t last = shr64(s_key[s_head[H - 1]], tb);
@@ -486,78 +486,80 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             for (int o = 0; o <= FMT_EXT; o += 32) {
                 const int64_t i = base + tn + o + lane;
                 const bool stop = i >= a.n || shr64(a.gkey[i], tb) != last;
-                const uint32_t b = __ballot_sync(0xffffffffu, stop);
-                if (b) {
-                    const int e = o + __ffs(b) - 1;
+                const uint32_t bb = __ballot_sync(0xffffffffu, stop);
+                if (bb) {
+                    const int e = o + __ffs(bb) - 1;
                     ext = e <= FMT_EXT ? e : -1;
                     break;
                 }
             }
         }
-        if (lane == 0) s_ext = ext;
-    } else {
-        for (uint32_t h = tid - 32; h < H; h += FMT_THREADS - 32) {
-            const int hp = s_head[h];
-            a.off[R0 + h] = (uint32_t)(base + hp);
-            a.case_code[R0 + h] = a.case_min + (uint32_t)shr64(s_key[hp], tb);
+        if (lane == 0) {
+            s_prefix = pf;
+            s_ext = ext;
         }
+    } else if (H > 0) {   // meanwhile: stage the tile's payloads
+        for (int p = (int)s_head[0] + tid - 32; p < tn; p += FMT_THREADS - 32) {
+            s_act[p] = a.gact[base + p];
+            if (WI) s_idx[p] = a.gidx[base + p];
+        }
+    }
+    __syncthreads();
+    const uint32_t R0 = s_prefix;
+    for (uint32_t h = tid; h < H; h += FMT_THREADS) {
+        const int hp = s_head[h];
+        a.off[R0 + h] = (uint32_t)(base + hp);
+        a.case_code[R0 + h] = a.case_min + (uint32_t)shr64(s_key[hp], tb);
     }
     if (tid == 0 && base + tn >= a.n) {
         a.off[R0 + H] = (uint32_t)a.n;
         *a.n_cases = R0 + H;
     }
-    __syncthreads();
     if (H == 0) return;
     int ext = s_ext;
-    uint32_t Hown = H;                 // cases this tile sorts here
-    if (ext < 0) {                     // last case runs far past the tile: fallback
-        if (tid == 0) a.big[atomicAdd(a.big_count, 1u)] = R0 + H - 1;
-        Hown = H - 1;
+    int Hown = (int)H;
+    if (ext < 0) {   // the last case runs far past the tile: exact fallback, not owned here
+        Hown = (int)H - 1;
         ext = 0;
+        if (tid == 0) a.big[atomicAdd(a.big_count, 1u)] = R0 + H - 1;
     }
     const int h0 = s_head[0];
-    const int oend = Hown == H ? tn + ext : (int)s_head[H - 1];   // owned local range [h0, oend)
-
-    // ---- stage the owned range (keys of the tile are already in smem)
-    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
+    const int oend = Hown == (int)H ? tn + ext : (int)s_head[H - 1];   // owned rows [h0, oend)
+    for (int p = tn + tid; p < oend; p += FMT_THREADS) {                // extension rows
         const int64_t i = base + p;
-        if (p >= tn) s_key[p] = a.gkey[i];
+        s_key[p] = a.gkey[i];
         s_act[p] = a.gact[i];
         if (WI) s_idx[p] = a.gidx[i];
-    }
-    // case index of every owned row; long cases -> fallback
-    for (uint32_t h = tid; h < Hown; h += FMT_THREADS) {
-        const int s0 = s_head[h], e0 = (h + 1 < Hown) ? s_head[h + 1] : oend;
-        const bool big = e0 - s0 > FMT_WARP_MAX;
-        if (big) a.big[atomicAdd(a.big_count, 1u)] = R0 + h;
-        for (int p = s0; p < e0; ++p) s_ci[p] = big ? (uint16_t)0xffff : (uint16_t)h;
+        s_ci[p] = (uint16_t)(H - 1);
     }
     __syncthreads();
 
-    // ---- rank every row inside its case: #(key_j < key_i or (== and j < i)).
-    // Event-parallel, so work is balanced and a warp (mostly one case) reads
-    // s_key[j] as a broadcast.
+    // ---- 4. rank each row inside its case: #(key_j < key_p) + #(j < p with key_j == key_p).
+    // Event-parallel with one uniform loop per case (a warp mostly reads one
+    // case -> broadcast smem reads, equal trip counts).
     for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
         const uint32_t h = s_ci[p];
-        if (h == 0xffff) {
+        const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
+        if (e0 - s0 > FMT_WARP_MAX) {      // long case: exact fallback
             s_dst[p] = 0xffff;
+            if (p == s0) a.big[atomicAdd(a.big_count, 1u)] = R0 + h;
             continue;
         }
-        const int s0 = s_head[h], e0 = (h + 1 < Hown) ? s_head[h + 1] : oend;
-        const uint64_t ki = s_key[p];
         int r = 0;
+        const uint64_t ki = s_key[p];
         for (int j = s0; j < e0; ++j) {
             const uint64_t kj = s_key[j];
-            r += (kj < ki) || (kj == ki && j < p);
+            r += (kj < ki) | ((kj == ki) & (j < p));
         }
         s_dst[p] = (uint16_t)(s0 + r);
     }
     __syncthreads();
 
-    // ---- write the formatted rows of the owned range
+    // ---- 5. write the formatted rows of the owned range
     for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
-        if (s_dst[p] == 0xffff) continue;   // rows of a fallback case
-        const int64_t g = base + s_dst[p];
+        const uint32_t dp = s_dst[p];
+        if (dp == 0xffff) continue;   // rows of a fallback case
+        const int64_t g = base + dp;
         a.key_out[g] = s_key[p];
         a.act_out[g] = s_act[p];
         if (WI) a.perm_out[g] = s_idx[p];
