@@ -323,7 +323,7 @@ template <class P, bool WI>
 static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const uint64_t* in_key,
                             const P* in_act, const uint32_t* in_idx, uint64_t* key_out, P* act_out,
                             uint32_t* idx_out, int64_t n, int shift0, int bits_total, KeyParams kp,
-                            cudaStream_t s) {
+                            cudaStream_t s, const char* pass_name = "k_onesweep") {
     const bool from_cols = in_case != nullptr;
     bits_total = std::max(1, bits_total);
     const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
@@ -367,12 +367,12 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
                                     off, status, counters,
                                     aligned16(in_case) && aligned16(in_ts) && aligned16(ca) &&
                                         (!ci || aligned16(ci))};
-            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
+            PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
         } else {
             PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, shift, bits, kp,
                                      off + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p,
                                      aligned16(ck) && aligned16(ca) && (!ci || aligned16(ci))};
-            PM4G_TRY(launch_pass(a, tiles, s, "k_onesweep", n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr)));
+            PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr)));
         }
         ck = ok;
         ca = oa;
@@ -849,7 +849,7 @@ pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, 
     uint32_t* ov = (uint32_t*)(ok + n);
     KeyParams kp{0, 0, 0};
     PM4G_TRY((lsd_sort<uint32_t, false>(nullptr, nullptr, keys, vals, nullptr, ok, ov, nullptr, n, 0,
-                                        std::max(1, std::min(bits, 64)), kp, s)));
+                                        std::max(1, std::min(bits, 64)), kp, s, "k_onesweep_small")));
     PM4G_CK(cudaMemcpyAsync(keys, ok, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
     PM4G_CK(cudaMemcpyAsync(vals, ov, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
     return PM4G_OK;
