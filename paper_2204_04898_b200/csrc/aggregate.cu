@@ -57,71 +57,117 @@ __device__ __forceinline__ void finish_key(uint64_t h1, uint64_t h2, uint32_t le
     k2 = fmix64(h2 + (uint64_t)len * 0xff51afd7ed558ccdull);
 }
 
-constexpr uint32_t AGG_STAGE = 4096;   // events of a case tile staged in smem
+constexpr uint32_t AGG_STAGE = 4096;   // rows of a case tile staged in smem (+ alignment slack)
+constexpr int AGG_CONSUMERS = 256;     // 8 consumer warps; + 1 producer warp
+constexpr int AGG_BLOCK = AGG_CONSUMERS + 32;
+constexpr int AGG_STAGES = 2;
+
+// One pipeline stage: the tile's case offsets and its rows (keys, activities).
+template <class P>
+struct alignas(128) AggStage {
+    uint32_t off[AGG_CASES + 4];
+    uint64_t key[AGG_STAGE + 16];
+    P act[AGG_STAGE + 32];
+    uint32_t nc, ka, aa, staged;
+    uint64_t c0;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 template <class P, bool SMEM>
-__global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
+__global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A,
     uint64_t* __restrict__ packed, uint32_t* __restrict__ n_events, int64_t* __restrict__ dur,
     uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
-    extern __shared__ __align__(16) uint32_t sm[];
+    extern __shared__ __align__(128) unsigned char agg_sm[];
+    __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
     const bool tables = packed != nullptr;
     const uint32_t AA = A * A;
-    const uint32_t tab_words = (SMEM && tables) ? 3 * AA + 2 * A : 0;
+    const uint32_t tab_words = (SMEM && tables) ? ((3 * AA + 2 * A + 31) & ~31u) : 0;
+    uint32_t* sm = (uint32_t*)agg_sm;
     uint32_t* s_cnt = sm;
     uint32_t* s_lo = sm + AA;
     uint32_t* s_hi = sm + 2 * AA;
     uint32_t* s_st = sm + 3 * AA;
     uint32_t* s_en = s_st + A;
-    uint32_t* s_off = sm + tab_words;                       // [AGG_CASES + 1]
-    P* s_act = (P*)(s_off + AGG_CASES + 4);                 // [AGG_STAGE]
+    AggStage<P>* stage = (AggStage<P>*)(agg_sm + (size_t)tab_words * 4);
     uint64_t* g_cnt = packed;
     uint64_t* g_sum = packed + AA;
     uint64_t* g_st = packed + 2 * (size_t)AA;
     uint64_t* g_en = g_st + A;
-    const int lane = threadIdx.x & 31;
-    for (uint32_t i = threadIdx.x; i < tab_words; i += AGG_THREADS) sm[i] = 0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (uint32_t i = tid; i < tab_words; i += AGG_BLOCK) sm[i] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < AGG_STAGES; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], AGG_CONSUMERS);
+        }
+    }
     __syncthreads();
     const uint64_t C = *d_n_cases;
     const uint64_t tiles = (C + AGG_CASES - 1) / AGG_CASES;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const uint64_t c0 = t * AGG_CASES;
-        const uint32_t nc = (uint32_t)min((uint64_t)AGG_CASES, C - c0);
-        for (uint32_t i = threadIdx.x; i <= nc; i += AGG_THREADS) s_off[i] = off[c0 + i];
-        __syncthreads();
-        const uint32_t e0 = s_off[0], e1 = s_off[nc], ne = e1 - e0;
-        const bool staged = ne <= AGG_STAGE;
-        if (staged)
-            for (uint32_t i = threadIdx.x; i < ne; i += AGG_THREADS) s_act[i] = act[e0 + i];
-        __syncthreads();
-        auto A_at = [&](uint32_t i) -> uint32_t { return staged ? (uint32_t)s_act[i - e0] : (uint32_t)act[i]; };
-        if (tables) {
-            // directly-follows pairs (i, i+1), 4 independent key loads in flight per thread;
-            // the successor's key comes from the next lane
-            for (uint32_t base = e0; base + 1 < e1; base += 4 * AGG_THREADS) {
-                uint64_t kk[4], kn[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
-                    kk[u] = i < e1 ? key[i] : 0ull;
+
+    if (warp == 0) {
+        // ---------------- producer warp: stream tiles into the ring with TMA
+        uint32_t i = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int s = i % AGG_STAGES;
+            if (i >= AGG_STAGES) mbar_wait(&s_empty[s], ((i / AGG_STAGES) - 1) & 1);
+            AggStage<P>& st = stage[s];
+            const uint64_t c0 = t * AGG_CASES;
+            const uint32_t nc = (uint32_t)min((uint64_t)AGG_CASES, C - c0);
+            for (uint32_t j = lane; j <= nc; j += 32) st.off[j] = off[c0 + j];
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t e0 = st.off[0], e1 = st.off[nc];
+                const uint32_t ka = e0 & ~1u, kb = (e1 + 1) & ~1u;                  // keys: 2 per 16 B
+                const uint32_t ea = (uint32_t)(16 / sizeof(P));
+                const uint32_t aa = e0 & ~(ea - 1), ab = (e1 + ea - 1) & ~(ea - 1);
+                const bool fit = kb - ka <= AGG_STAGE + 16 && ab - aa <= AGG_STAGE + 32;
+                st.nc = nc;
+                st.c0 = c0;
+                st.ka = ka;
+                st.aa = aa;
+                st.staged = fit ? 1u : 0u;
+                if (fit) {
+                    mbar_expect_tx(&s_full[s], (kb - ka) * 8 + (ab - aa) * (uint32_t)sizeof(P));
+                    tma_load_1d(st.key, key + ka, (kb - ka) * 8, &s_full[s]);
+                    tma_load_1d(st.act, act + aa, (ab - aa) * (uint32_t)sizeof(P), &s_full[s]);
+                } else {
+                    mbar_arrive(&s_full[s]);     // oversized tile: consumers read global memory
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
-                    kn[u] = __shfl_down_sync(0xffffffffu, kk[u], 1);
-                    if (lane == 31 && i + 1 < e1) kn[u] = key[i + 1];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t i = base + u * AGG_THREADS + threadIdx.x;
-                    if (i + 1 >= e1 || shr64(kk[u], ts_bits) != shr64(kn[u], ts_bits)) continue;
-                    uint32_t e = A_at(i) * A + A_at(i + 1);
-                    uint64_t d = kn[u] - kk[u];
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- consumer warps
+        const int ct = tid - 32;
+        uint32_t i = 0;
+        for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int s = i % AGG_STAGES;
+            mbar_wait(&s_full[s], (i / AGG_STAGES) & 1);
+            const AggStage<P>& st = stage[s];
+            const uint32_t nc = st.nc, ka = st.ka, aa = st.aa;
+            const bool staged = st.staged != 0;
+            const uint64_t c0 = st.c0;
+            const uint32_t e0 = st.off[0], e1 = st.off[nc];
+            auto K_at = [&](uint32_t r) -> uint64_t { return staged ? st.key[r - ka] : key[r]; };
+            auto A_at = [&](uint32_t r) -> uint32_t { return staged ? (uint32_t)st.act[r - aa] : (uint32_t)act[r]; };
+            if (tables) {
+                // directly-follows pairs (r, r+1) of one case
+                for (uint32_t r = e0 + ct; r + 1 < e1; r += AGG_CONSUMERS) {
+                    const uint64_t kk = K_at(r), kn = K_at(r + 1);
+                    if (shr64(kk, ts_bits) != shr64(kn, ts_bits)) continue;
+                    const uint32_t e = A_at(r) * A + A_at(r + 1);
+                    const uint64_t d = kn - kk;
                     if (SMEM) {
                         atomicAdd(&s_cnt[e], 1u);
-                        uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
-                        uint32_t old = atomicAdd(&s_lo[e], lo);
+                        const uint32_t lo = (uint32_t)d;
+                        uint32_t hi = (uint32_t)(d >> 32);
+                        const uint32_t old = atomicAdd(&s_lo[e], lo);
                         hi += (old + lo < old) ? 1u : 0u;   // carry out of the low word
                         if (hi) atomicAdd(&s_hi[e], hi);
                     } else {
@@ -130,47 +176,48 @@ __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
                     }
                 }
             }
-        }
-        if (threadIdx.x < nc) {
-            const uint64_t c = c0 + threadIdx.x;
-            const uint32_t f = s_off[threadIdx.x], l = s_off[threadIdx.x + 1] - 1;
-            if (tables) {
-                uint32_t as = A_at(f), ae = A_at(l);
-                if (SMEM) {
-                    atomicAdd(&s_st[as], 1u);
-                    atomicAdd(&s_en[ae], 1u);
-                } else {
-                    atomicAdd((unsigned long long*)&g_st[as], 1ull);
-                    atomicAdd((unsigned long long*)&g_en[ae], 1ull);
+            if ((uint32_t)ct < nc) {
+                const uint64_t c = c0 + ct;
+                const uint32_t f = st.off[ct], l = st.off[ct + 1] - 1;
+                if (tables) {
+                    const uint32_t as = A_at(f), ae = A_at(l);
+                    if (SMEM) {
+                        atomicAdd(&s_st[as], 1u);
+                        atomicAdd(&s_en[ae], 1u);
+                    } else {
+                        atomicAdd((unsigned long long*)&g_st[as], 1ull);
+                        atomicAdd((unsigned long long*)&g_en[ae], 1ull);
+                    }
+                }
+                if (n_events) n_events[c] = l - f + 1;
+                if (dur) dur[c] = (int64_t)(K_at(l) - K_at(f));
+                if (k1o) {
+                    uint64_t h1 = 0, h2 = 0;
+                    for (uint32_t r = f; r <= l; ++r) {
+                        const uint64_t a = (uint64_t)A_at(r) + 1;
+                        h1 = h1 * HB1 + a;
+                        h2 = h2 * HB2 + a;
+                    }
+                    uint64_t x1, x2;
+                    finish_key(h1, h2, l - f + 1, weak != 0, x1, x2);
+                    k1o[c] = x1;
+                    k2o[c] = x2;
                 }
             }
-            if (n_events) n_events[c] = l - f + 1;
-            if (dur) dur[c] = (int64_t)(key[l] - key[f]);
-            if (k1o) {
-                uint64_t h1 = 0, h2 = 0;
-                for (uint32_t i = f; i <= l; ++i) {
-                    uint64_t a = (uint64_t)A_at(i) + 1;
-                    h1 = h1 * HB1 + a;
-                    h2 = h2 * HB2 + a;
-                }
-                uint64_t x1, x2;
-                finish_key(h1, h2, l - f + 1, weak != 0, x1, x2);
-                k1o[c] = x1;
-                k2o[c] = x2;
-            }
+            mbar_arrive(&s_empty[s]);   // this thread is done reading the stage
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (SMEM && tables) {
-        for (uint32_t e = threadIdx.x; e < AA; e += AGG_THREADS) {
-            uint32_t cn = s_cnt[e];
+        for (uint32_t e = tid; e < AA; e += AGG_BLOCK) {
+            const uint32_t cn = s_cnt[e];
             if (cn) {
                 atomicAdd((unsigned long long*)&g_cnt[e], (unsigned long long)cn);
-                uint64_t sm64 = ((uint64_t)s_hi[e] << 32) | s_lo[e];
+                const uint64_t sm64 = ((uint64_t)s_hi[e] << 32) | s_lo[e];
                 if (sm64) atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)sm64);
             }
         }
-        for (uint32_t a = threadIdx.x; a < A; a += AGG_THREADS) {
+        for (uint32_t a = tid; a < A; a += AGG_BLOCK) {
             if (s_st[a]) atomicAdd((unsigned long long*)&g_st[a], (unsigned long long)s_st[a]);
             if (s_en[a]) atomicAdd((unsigned long long*)&g_en[a], (unsigned long long)s_en[a]);
         }
@@ -180,23 +227,23 @@ __global__ __launch_bounds__(AGG_THREADS) void k_aggregate(
 template <class P, bool SMEM>
 static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
-    size_t smem = ((SMEM && o.tables) ? ((size_t)3 * A * A + 2 * A) * 4 : 0) +
-                  (AGG_CASES + 4) * 4 + (size_t)AGG_STAGE * sizeof(P);
+    const size_t tab = (SMEM && o.tables) ? ((size_t)((3 * A * A + 2 * A + 31) & ~31u)) * 4 : 0;
+    const size_t smem = tab + AGG_STAGES * sizeof(AggStage<P>);
     static bool attr = false;
     if (!attr) {
         PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(AGG_SMEM_MAX + (AGG_CASES + 4) * 4 + AGG_STAGE * sizeof(P))));
+                                     (int)(AGG_SMEM_MAX + 128 + AGG_STAGES * sizeof(AggStage<P>))));
         attr = true;
     }
-    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
-    uint64_t tiles = std::max<uint64_t>(1, (cap + AGG_CASES - 1) / AGG_CASES);
-    int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (smem + 1024)));
-    uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
-    // algorithmic bytes: read key + act once per event, + per-case outputs
-    double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 +
-                   (o.n_events ? cap * 4.0 : 0) + (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
+    const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    const uint64_t tiles = std::max<uint64_t>(1, (cap + AGG_CASES - 1) / AGG_CASES);
+    const int per_sm = std::max(1, (int)std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
+    const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
+    // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
+    const double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
+                         (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, SMEM><<<(unsigned)grid, AGG_THREADS, smem, s>>>(
+                (k_aggregate<P, SMEM><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A,
                     o.tables ? o.packed : nullptr, o.n_events, o.dur, o.k1, o.k2,
                     debug_weak_hash() ? 1 : 0)));

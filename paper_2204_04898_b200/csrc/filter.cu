@@ -216,8 +216,8 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         cs.ncol++;
     };
     if (in->sorted) {
-        if ((st = dalloc((void**)&L->key, N * 8, s))) return bail(st);
-        if ((st = dalloc(&L->s_act, N * in->act_bytes, s))) return bail(st);
+        if ((st = dalloc((void**)&L->key, (N + 32) * 8, s))) return bail(st);
+        if ((st = dalloc(&L->s_act, (N + 32) * in->act_bytes, s))) return bail(st);
         add(in->key, L->key, 8);
         add(in->s_act, L->s_act, in->act_bytes);
         if (in->perm) {

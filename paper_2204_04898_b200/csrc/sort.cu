@@ -348,10 +348,12 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
         PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(hist, off, passes));
     }
     // ping-pong buffer: key (8n) | idx (4n) | act
-    PM4G_TRY(tmp.alloc((size_t)n * (8 + (WI ? 4 : 0) + sizeof(P)) + 64));
+    auto up16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    const size_t o_idx = up16((size_t)n * 8), o_act = up16(o_idx + (WI ? (size_t)n * 4 : 0));
+    PM4G_TRY(tmp.alloc(o_act + ((size_t)n + 32) * sizeof(P) + 64));
     uint64_t* tkey = tmp.as<uint64_t>();
-    uint32_t* tidx = (uint32_t*)(tkey + n);
-    P* tact = (P*)((char*)tidx + (WI ? (size_t)n * 4 : 0));
+    uint32_t* tidx = (uint32_t*)((char*)tmp.p + o_idx);
+    P* tact = (P*)((char*)tmp.p + o_act);
     const uint64_t* ck = in_key;
     const P* ca = in_act;
     const uint32_t* ci = in_idx;
@@ -409,6 +411,7 @@ struct FmtArgs {
     uint32_t* counter;
     uint32_t* big;             // ranks of fallback cases
     uint32_t* big_count;
+    bool aligned;              // gkey / gact / gidx 16-byte aligned (TMA bulk path)
 };
 
 template <class P, bool WI>
@@ -423,6 +426,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
     __shared__ uint32_t s_prefix;
     __shared__ int s_ext;
+    __shared__ __align__(8) uint64_t s_bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(a.counter, 1u);
@@ -433,20 +437,39 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     const int tb = a.ts_bits;
     const uint32_t lt = lanemask_lt();
 
-    // ---- 1. the tile's keys (coalesced, warp-striped) -> smem, head ballots
+    // ---- 1. the tile's rows -> smem (TMA bulk copies for full tiles), head ballots
+    const bool bulk = tn == FMT_TILE && a.aligned;
+    if (bulk) {
+        if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            mbar_expect_tx(&s_bar, FMT_TILE * (uint32_t)(8 + sizeof(P) + (WI ? 4 : 0)));
+            tma_load_1d(s_key, a.gkey + base, FMT_TILE * 8, &s_bar);
+            tma_load_1d(s_act, a.gact + base, FMT_TILE * (uint32_t)sizeof(P), &s_bar);
+            if (WI) tma_load_1d(s_idx, a.gidx + base, FMT_TILE * 4, &s_bar);
+        }
+    } else {
+        for (int p = tid; p < tn; p += FMT_THREADS) {
+            s_key[p] = a.gkey[base + p];
+            s_act[p] = a.gact[base + p];
+            if (WI) s_idx[p] = a.gidx[base + p];
+        }
+    }
+    uint64_t prev_case = 0;
+    {
+        const int64_t pi = base + warp * (32 * FMT_IPT) - 1;
+        if (pi >= 0 && pi < a.n) prev_case = shr64(a.gkey[pi], tb);
+    }
+    __syncthreads();
+    if (bulk) mbar_wait(&s_bar, 0);
     uint32_t ball[FMT_IPT], wc = 0;
     {
-        uint64_t prev = 0;
-        const int64_t pi = base + warp * (32 * FMT_IPT) - 1;
-        if (pi >= 0 && pi < a.n) prev = shr64(a.gkey[pi], tb);
+        uint64_t prev = prev_case;
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
             const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
             const int64_t i = base + li;
             const bool ok = li < tn;
-            const uint64_t kk = ok ? a.gkey[i] : 0ull;
-            if (ok) s_key[li] = kk;
-            const uint64_t c = shr64(kk, tb);
+            const uint64_t c = ok ? shr64(s_key[li], tb) : 0ull;
             uint64_t pc = __shfl_up_sync(0xffffffffu, c, 1);
             if (lane == 0) pc = prev;
             prev = __shfl_sync(0xffffffffu, c, 31);
@@ -497,11 +520,6 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         if (lane == 0) {
             s_prefix = pf;
             s_ext = ext;
-        }
-    } else if (H > 0) {   // meanwhile: stage the tile's payloads
-        for (int p = (int)s_head[0] + tid - 32; p < tn; p += FMT_THREADS - 32) {
-            s_act[p] = a.gact[base + p];
-            if (WI) s_idx[p] = a.gidx[base + p];
         }
     }
     __syncthreads();
@@ -599,6 +617,7 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
     fa.status = fa.counter + 2;
     fa.big = fa.status + tiles;
     const bool wi = fa.perm_out != nullptr;
+    fa.aligned = aligned16(fa.gkey) && aligned16(fa.gact) && (!wi || aligned16(fa.gidx));
     const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + 16;
     const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0);
     static bool attr = false;
@@ -644,10 +663,12 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
     KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
     // 1. stable LSD passes over the case bits of the composite key (built on the fly)
     Scratch grp(s);
-    PM4G_TRY(grp.alloc((size_t)n * (8 + (wi ? 4 : 0) + sizeof(P)) + 64));
+    auto up16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    const size_t o_idx = up16((size_t)n * 8), o_act = up16(o_idx + (wi ? (size_t)n * 4 : 0));
+    PM4G_TRY(grp.alloc(o_act + ((size_t)n + 32) * sizeof(P) + 64));
     uint64_t* gkey = grp.as<uint64_t>();
-    uint32_t* gidx = (uint32_t*)(gkey + n);
-    P* gact = (P*)((char*)gidx + (wi ? (size_t)n * 4 : 0));
+    uint32_t* gidx = (uint32_t*)((char*)grp.p + o_idx);
+    P* gact = (P*)((char*)grp.p + o_act);
     if (wi)
         PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, gidx, n,
                                     L->ts_bits, L->case_bits, kp, s)));
@@ -816,8 +837,9 @@ static pm4g_status gather_extras(pm4g_log* L, cudaStream_t s) {
 pm4g_status sort_log(pm4g_log* L, cudaStream_t s) {
     const int64_t n = L->n;
     const bool wi = !L->extra.empty();
-    PM4G_TRY(dalloc_t(&L->key, std::max<int64_t>(n, 1), s));
-    PM4G_TRY(dalloc(&L->s_act, std::max<int64_t>(n, 1) * L->act_bytes, s));
+    // +32 rows: 16-byte aligned TMA reads of the formatted log may run one vector past n
+    PM4G_TRY(dalloc_t(&L->key, (size_t)n + 32, s));
+    PM4G_TRY(dalloc(&L->s_act, ((size_t)n + 32) * L->act_bytes, s));
     if (wi) PM4G_TRY(dalloc_t(&L->perm, std::max<int64_t>(n, 1), s));
     // offsets: number of cases <= min(n, case range)
     dfree(L->off, s);
