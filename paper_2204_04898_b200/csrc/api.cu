@@ -185,25 +185,46 @@ struct Meta {
     unsigned long long bad_case, bad_act, bad_extra;
 };
 
+// One pass over the ingested columns: metadata (ts / case ranges), the first
+// invalid row, and -- since the case column is being read anyway -- the
+// histograms of the case digits the sort's LSD passes will use (digit p of
+// case - case_lo, `bits` per digit, layout derived from [case_lo, case_hi)).
+// Vectorised: 4 rows per thread per iteration (16-byte loads of case and ts).
 template <class P>
-__global__ void k_validate(const uint32_t* __restrict__ cs, const P* __restrict__ act,
-                           const int64_t* __restrict__ ts, int64_t n, uint32_t lo, uint32_t hi,
-                           uint32_t A, Meta* m) {
+__global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ cs, const P* __restrict__ act,
+                                                  const int64_t* __restrict__ ts, int64_t n, uint32_t lo,
+                                                  uint32_t hi, uint32_t A, Meta* m, int hpasses, int hbits,
+                                                  uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[4][256];
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
     long long tmin = LLONG_MAX, tmax = LLONG_MIN;
     unsigned cmin = 0xffffffffu, cmax = 0;
     unsigned long long bc = ~0ull, ba = ~0ull;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t c = cs[i];
-        long long t = ts[i];
-        uint32_t a = (uint32_t)act[i];
+    const uint32_t hmask = (1u << hbits) - 1;
+    auto row = [&](int64_t i, uint32_t c, long long t, uint32_t a) {
         tmin = min(tmin, t);
         tmax = max(tmax, t);
         cmin = min(cmin, c);
         cmax = max(cmax, c);
         if ((c < lo || c >= hi) && (unsigned long long)i < bc) bc = i;
         if (a >= A && (unsigned long long)i < ba) ba = i;
+        const uint32_t f = c - lo;
+        for (int p = 0; p < hpasses; ++p) atomicAdd(&sh[p][(f >> (p * hbits)) & hmask], 1u);
+    };
+    const bool vec = (((uintptr_t)cs | (uintptr_t)ts) & 15) == 0;
+    const int64_t nq = vec ? n / 4 : 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 c4 = ((const uint4*)cs)[q];
+        const longlong2 t01 = ((const longlong2*)ts)[2 * q], t23 = ((const longlong2*)ts)[2 * q + 1];
+        const int64_t i = 4 * q;
+        row(i, c4.x, t01.x, (uint32_t)act[i]);
+        row(i + 1, c4.y, t01.y, (uint32_t)act[i + 1]);
+        row(i + 2, c4.z, t23.x, (uint32_t)act[i + 2]);
+        row(i + 3, c4.w, t23.y, (uint32_t)act[i + 3]);
     }
+    for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        row(i, cs[i], ts[i], (uint32_t)act[i]);
     for (int o = 16; o; o >>= 1) {
         tmin = min(tmin, __shfl_xor_sync(~0u, tmin, o));
         tmax = max(tmax, __shfl_xor_sync(~0u, tmax, o));
@@ -219,6 +240,11 @@ __global__ void k_validate(const uint32_t* __restrict__ cs, const P* __restrict_
         atomicMax(&m->case_max, cmax);
         if (bc != ~0ull) atomicMin(&m->bad_case, bc);
         if (ba != ~0ull) atomicMin(&m->bad_act, ba);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < hpasses * 256; i += blockDim.x) {
+        const uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
     }
 }
 
@@ -248,13 +274,20 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
     PM4G_CK(cudaMemcpyAsync(dm, &h, sizeof(Meta), cudaMemcpyHostToDevice, s));
     const int64_t n = L->n;
     uint32_t hi = L->case_hi;
+    // case-digit histograms for the sort, laid out for the range [case_lo, case_hi)
+    const int rbits = bit_width_u64((uint64_t)(hi > L->case_lo ? hi - 1 - L->case_lo : 0));
+    const int hpasses = std::max(1, std::min(4, (std::max(rbits, 1) + 7) / 8));
+    const int hbits = (std::max(rbits, 1) + hpasses - 1) / hpasses;
+    L->hist_passes = 0;
+    if (!L->hist) PM4G_TRY(dalloc_t(&L->hist, 4 * 256, s));
+    PM4G_CK(cudaMemsetAsync(L->hist, 0, 4 * 256 * 4, s));
     if (n > 0) {
-        int g = grid_for(n, 256);
+        int g = grid_for((n + 3) / 4, 256);
         double bytes = (double)n * (12 + L->act_bytes);
         switch (L->act_bytes) {
-            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
-            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
-            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm)); break;
+            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
+            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
+            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
         }
         for (auto& c : L->extra)
             if (c.kind == PM4G_KIND_CODES)
@@ -283,6 +316,15 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
     L->ts_bits = bit_width_u64(ts_span);
     L->key_bits = L->case_bits + L->ts_bits;
     L->passes = (std::min(L->key_bits, 64) + 7) / 8;
+    // the sort can reuse the histograms iff its digit layout is the same
+    {
+        const int cb = std::max(L->case_bits, 1);
+        const int sp = (cb + 7) / 8, sb = (cb + sp - 1) / sp;
+        if (n > 0 && L->case_min == L->case_lo && sp == hpasses && sb == hbits) {
+            L->hist_passes = hpasses;
+            L->hist_bits = hbits;
+        }
+    }
     return PM4G_OK;
 }
 
@@ -477,6 +519,7 @@ pm4g_status pm4g_log_destroy(pm4g_log* L) {
     dfree(L->off, s);
     dfree(L->s_case_code, s);
     dfree(L->d_n_cases, s);
+    dfree(L->hist, s);
     for (auto& x : L->extra)
         if (x.owned) {
             dfree(x.data, s);

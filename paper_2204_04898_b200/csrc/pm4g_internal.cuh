@@ -108,6 +108,10 @@ struct pm4g_log {
     uint32_t* s_case_code = nullptr;  // [n_cases] case code of each case
     uint64_t* d_n_cases = nullptr;    // device scalar
     int64_t n_cases = -1;             // host copy (-1 until fetched)
+    // case-digit histograms computed during validation (reused by the sort
+    // when hist_passes > 0: digit p of case - case_lo, hist_bits per digit)
+    uint32_t* hist = nullptr;         // [4][256]
+    int hist_passes = 0, hist_bits = 0;
     std::vector<pm4g::ExtraCol> extra;
     cudaStream_t stream = nullptr;
 };

@@ -323,7 +323,8 @@ template <class P, bool WI>
 static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const uint64_t* in_key,
                             const P* in_act, const uint32_t* in_idx, uint64_t* key_out, P* act_out,
                             uint32_t* idx_out, int64_t n, int shift0, int bits_total, KeyParams kp,
-                            cudaStream_t s, const char* pass_name = "k_onesweep") {
+                            cudaStream_t s, const char* pass_name = "k_onesweep",
+                            const uint32_t* pre_hist = nullptr) {
     const bool from_cols = in_case != nullptr;
     bits_total = std::max(1, bits_total);
     const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
@@ -337,7 +338,9 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
     uint32_t* hist = counters + passes;
     uint32_t* off = hist + MAX_PASSES * RADIX;
     PM4G_CK(cudaMemsetAsync(status, 0, (status_words + passes + MAX_PASSES * RADIX) * 4, s));
-    {
+    if (pre_hist) {   // histograms already built (by the validation pass)
+        PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(pre_hist, off, passes));
+    } else {
         const int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 4));
         if (from_cols)
             PM4G_LAUNCH("k_hist", n * 4.0, s,
@@ -669,12 +672,13 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
     uint64_t* gkey = grp.as<uint64_t>();
     uint32_t* gidx = (uint32_t*)((char*)grp.p + o_idx);
     P* gact = (P*)((char*)grp.p + o_act);
+    const uint32_t* pre = L->hist_passes > 0 ? L->hist : nullptr;
     if (wi)
         PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, gidx, n,
-                                    L->ts_bits, L->case_bits, kp, s)));
+                                    L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre)));
     else
         PM4G_TRY((lsd_sort<P, false>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, nullptr,
-                                     n, L->ts_bits, L->case_bits, kp, s)));
+                                     n, L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre)));
     // 2. per-case timestamp order + case offsets
     FmtArgs<P> fa{};
     fa.gkey = gkey;
