@@ -215,11 +215,24 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
         const uint32_t it = list ? list[t] : (uint32_t)t;
         const uint32_t sl = item_slot[it];
         const uint32_t ord = order ? order[it] : it;
-        if (table[sl].rep == ord) continue;             // the representative itself
-        const uint32_t rep_it = item_of_rep_slot[sl];
+        const uint32_t rep = table[sl].rep;
+        if (rep == ord) continue;                       // the representative itself
+        // with the identity order the representative item IS the slot's rep
+        const uint32_t rep_it = order ? item_of_rep_slot[sl] : rep;
         const OFF f = off[it], l = off[it + 1], rf = off[rep_it], rl = off[rep_it + 1];
         bool same = (l - f) == (rl - rf);
-        for (OFF i = 0; same && i < l - f; ++i) same = acts[f + i] == acts[rf + i];
+        if (same) {   // branch-free compare: independent loads, no early exit
+            uint32_t diff = 0;
+            const OFF len = l - f;
+            OFF i = 0;
+            for (; i + 4 <= len; i += 4)
+                diff |= ((uint32_t)acts[f + i] ^ (uint32_t)acts[rf + i]) |
+                        ((uint32_t)acts[f + i + 1] ^ (uint32_t)acts[rf + i + 1]) |
+                        ((uint32_t)acts[f + i + 2] ^ (uint32_t)acts[rf + i + 2]) |
+                        ((uint32_t)acts[f + i + 3] ^ (uint32_t)acts[rf + i + 3]);
+            for (; i < len; ++i) diff |= (uint32_t)acts[f + i] ^ (uint32_t)acts[rf + i];
+            same = diff == 0;
+        }
         if (!same) {
             atomicAdd(&table[sl].weight, (unsigned long long)(0ull - (weight ? weight[it] : 1ull)));
             pending[it] = 1;
@@ -252,7 +265,7 @@ __global__ void k_compact(const Slot* __restrict__ table, uint64_t cap,
         if ((s.k1 | s.k2) == 0 || s.weight == 0) continue;
         uint32_t g = atomicAdd(n_groups, 1u);
         g_weight[g] = s.weight;
-        g_rep_item[g] = item_of_rep_slot[sl];
+        g_rep_item[g] = item_of_rep_slot ? item_of_rep_slot[sl] : s.rep;
         g_order[g] = s.rep;
         slot_group[sl] = g;
     }
@@ -378,38 +391,39 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                                 list, n_active, k1, k2, off, weight, order, table, cap - 1, salt,
                                 item_slot, pending, counters + 1)));
             }
-            PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
-                        (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot)));
+            uint32_t* ior = order ? item_of_rep_slot : nullptr;   // identity order: rep item = slot.rep
+            if (order)
+                PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
+                            (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot)));
             PM4G_LAUNCH("k_variant_verify", n_active * 16.0, s,
                         (k_verify<OFF, ACT><<<gs, 256, 0, s>>>(list, n_active, off, acts, weight, order,
-                                                               item_of_rep_slot, table, item_slot,
+                                                               ior, table, item_slot,
                                                                pending, next_list, counters)));
-            uint32_t h[2] = {0, 0};
-            PM4G_CK(cudaMemcpyAsync(h, counters, 8, cudaMemcpyDeviceToHost, s));
-            PM4G_CK(cudaStreamSynchronize(s));
-            if (h[1]) {  // table overflow: retry this round with a full-size table
-                if (attempt == 1) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
-                cap = pow2_at_least(2 * n_active + 1024);
-                continue;
-            }
             PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
-                        (k_compact<<<gsz(cap), 256, 0, s>>>(table, cap, item_of_rep_slot, slot_group,
+                        (k_compact<<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
                                                             g.weight, g.rep_item, g.order,
                                                             counters + 2)));
             PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
                         (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
                                                          g.item_group)));
+            // one host round trip per round: next_count, overflow, n_groups
+            uint32_t h[3] = {0, 0, 0};
+            PM4G_CK(cudaMemcpyAsync(h, counters, 12, cudaMemcpyDeviceToHost, s));
+            PM4G_CK(cudaStreamSynchronize(s));
+            if (h[1]) {  // table overflow: discard this round's groups, retry with a full-size table
+                if (attempt == 1) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
+                const uint32_t gb = (uint32_t)G;
+                PM4G_CK(cudaMemcpyAsync(counters + 2, &gb, 4, cudaMemcpyHostToDevice, s));
+                PM4G_CK(cudaStreamSynchronize(s));
+                cap = pow2_at_least(2 * n_active + 1024);
+                continue;
+            }
+            G = h[2];
             n_active = h[0];
             list = next_list;
             if (round > 64 * 1024) return bail(fail(PM4G_ECUDA, "variant grouping did not converge"));
             break;
         }
-    }
-    {   // total groups over all rounds (counters[2] accumulates across rounds)
-        uint32_t ng = 0;
-        PM4G_CK(cudaMemcpyAsync(&ng, counters + 2, 4, cudaMemcpyDeviceToHost, s));
-        PM4G_CK(cudaStreamSynchronize(s));
-        G = ng;
     }
     g.G = G;
     // sort groups: count desc, order asc
