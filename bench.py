@@ -135,6 +135,15 @@ def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=
     return res, v
 
 
+def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt: bool) -> dict:
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": f"synthetic-{cfg}: {n_local:,} events / {cases:,} cases / {A} activities per GPU, "
+                        f"fully shuffled rows (full radix sort)" + (", events-mode time filter" if filt else ""),
+            "events_per_gpu": n_local, "global_events": n_local * world, "parallelism": f"case-sharded x{world}",
+            "l2": "inputs (13 B/event) larger than L2; no flush needed",
+            "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")}
+
+
 def cpu_baseline(cfg, cases: int, device):
     """O1 on a bounded sample (the first `cases` cases of the workload), 1 core."""
     import oracle
@@ -171,11 +180,12 @@ def reference_arm(args):
         oracle.run(c, a, t, spec.n_activities)
     dt = time.perf_counter() - t0
     v = c.size * args.steps / dt
+    full_n = spec.n_events if spec.n_events is not None else int(c.size)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic",
-            "config": {"workload": f"synthetic-{args.config} (sample)", "events_per_step": int(c.size)},
+            "config": workload_config(args.config, full_n, spec.n_cases, spec.n_activities, 1, args.filter),
             "cpu_baseline": {"value": v, "unit": "events/s", "cores": 1, "kind": "oracle",
                              "sample": f"first {min(cases, spec.n_cases):,} cases ({c.size:,} events) of "
                                        f"the {args.config} workload per step; single-threaded O1"},
@@ -360,12 +370,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"synthetic-{args.config}: {n_local:,} events / {meta['case_hi'] - meta['case_lo']:,} "
-                                   f"cases / {meta['A']} activities per GPU, fully shuffled rows (full radix sort)"
-                                   + (", events-mode time filter" if filt else ""),
-                       "events_per_gpu": n_local, "global_events": n_total, "parallelism": f"case-sharded x{world}",
-                       "l2": "inputs (13 B/event) larger than L2; no flush needed",
-                       "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")},
+            "config": workload_config(args.config, n_local, meta["case_hi"] - meta["case_lo"], meta["A"], world,
+                                      filt is not None),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
             "hbm_pipeline": {"algorithmic_GB_per_step": step_bytes / args.steps / 1e9,
