@@ -427,8 +427,8 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     P* s_act = (P*)(s_head + FMT_TILE + 8);                        // [FMT_BUF]
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
-    __shared__ uint32_t s_prefix;
-    __shared__ int s_ext;
+    __shared__ uint32_t s_prefix, s_nbig, s_bigh[16];
+    __shared__ int s_ext, s_wlast[FMT_THREADS / 32];
     __shared__ __align__(8) uint64_t s_bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -480,16 +480,31 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             wc += __popc(ball[j]);
         }
     }
-    if (lane == 0) s_wt[warp] = wc;
+    // last head of this warp (for the tile-extension scan)
+    int lasth = -1;
+#pragma unroll
+    for (int j = 0; j < FMT_IPT; ++j)
+        if (ball[j]) lasth = warp * (32 * FMT_IPT) + j * 32 + (31 - __clz(ball[j]));
+    if (lane == 0) {
+        s_wt[warp] = wc;
+        s_wlast[warp] = lasth;
+    }
     __syncthreads();
-    uint32_t H;
-    const uint32_t wex = block_excl_scan<FMT_THREADS>(tid < FMT_THREADS / 32 ? s_wt[tid] : 0u, s_scan, &H);
-    if (tid < FMT_THREADS / 32) s_wt[tid] = wex;
-    __syncthreads();
+    uint32_t H = 0, wex = 0;
+    int lastp = -1;
+#pragma unroll
+    for (int w = 0; w < FMT_THREADS / 32; ++w) {
+        const uint32_t c = s_wt[w];
+        wex += (w < warp) ? c : 0u;
+        H += c;
+        lastp = max(lastp, s_wlast[w]);
+    }
 
-    // ---- 2. head list and the case index of every row of the tile
+    // ---- 2. concurrently: every warp writes its heads and row->case indices;
+    // warp 0 then runs the case-rank look-back, warp 1 finds how far the last
+    // case runs past the tile end
     {
-        uint32_t r = s_wt[warp];
+        uint32_t r = wex;
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
             const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
@@ -500,90 +515,100 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             r += __popc(b);
         }
     }
+    if (tid < 16) s_bigh[tid] = 0;
+    if (tid == 0) s_nbig = 0;
     __syncthreads();
 
-    // ---- 3. case ranks (warp 0 look-back) and the extent of the last case
+    // ---- 3. warp 0 resolves the case ranks (decoupled look-back) while warps
+    // 1..7 sort the tile; the workers synchronise on named barrier 1
     if (warp == 0) {
         const uint32_t pf = lookback_warp(a.status, tile, H);
-        int ext = 0;
-        if (H > 0 && base + tn < a.n) {
-            const uint64_t last = shr64(s_key[s_head[H - 1]], tb);
-            ext = -1;
-            for (int o = 0; o <= FMT_EXT; o += 32) {
-                const int64_t i = base + tn + o + lane;
-                const bool stop = i >= a.n || shr64(a.gkey[i], tb) != last;
-                const uint32_t bb = __ballot_sync(0xffffffffu, stop);
-                if (bb) {
-                    const int e = o + __ffs(bb) - 1;
-                    ext = e <= FMT_EXT ? e : -1;
-                    break;
+        if (lane == 0) s_prefix = pf;
+    } else if (H > 0) {
+        constexpr int NW = FMT_THREADS - 32;
+        const int wt = tid - 32;
+        auto wsync = [] { asm volatile("bar.sync 1, %0;" ::"n"(FMT_THREADS - 32) : "memory"); };
+        if (warp == 1) {   // how far the last case runs past the tile end
+            int ext = 0;
+            if (base + tn < a.n) {
+                const uint64_t last = shr64(s_key[lastp], tb);
+                ext = -1;
+                for (int o = 0; o <= FMT_EXT; o += 32) {
+                    const int64_t i = base + tn + o + lane;
+                    const bool stop = i >= a.n || shr64(a.gkey[i], tb) != last;
+                    const uint32_t bb = __ballot_sync(0xffffffffu, stop);
+                    if (bb) {
+                        const int e = o + __ffs(bb) - 1;
+                        ext = e <= FMT_EXT ? e : -1;
+                        break;
+                    }
                 }
             }
+            if (lane == 0) s_ext = ext;
         }
-        if (lane == 0) {
-            s_prefix = pf;
-            s_ext = ext;
+        wsync();
+        int ext = s_ext;
+        int Hown = (int)H;
+        if (ext < 0) {   // the last case runs far past the tile: exact fallback, not owned here
+            Hown = (int)H - 1;
+            ext = 0;
+            if (wt == 0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = H - 1;
+        }
+        const int h0 = s_head[0];
+        const int oend = Hown == (int)H ? tn + ext : (int)s_head[H - 1];   // owned rows [h0, oend)
+        for (int p = tn + wt; p < oend; p += NW) {                          // extension rows
+            const int64_t i = base + p;
+            s_key[p] = a.gkey[i];
+            s_act[p] = a.gact[i];
+            if (WI) s_idx[p] = a.gidx[i];
+            s_ci[p] = (uint16_t)(H - 1);
+        }
+        wsync();
+
+        // ---- 4. rank each row inside its case: #(key_j < key_p) + #(j < p with key_j == key_p).
+        // Event-parallel with one uniform loop per case (a warp mostly reads one
+        // case -> broadcast smem reads, equal trip counts).
+        for (int p = h0 + wt; p < oend; p += NW) {
+            const uint32_t h = s_ci[p];
+            const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
+            if (e0 - s0 > FMT_WARP_MAX) {      // long case: exact fallback
+                s_dst[p] = 0xffff;
+                if (p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
+                continue;
+            }
+            int r = 0;
+            const uint64_t ki = s_key[p];
+            for (int j = s0; j < e0; ++j) {
+                const uint64_t kj = s_key[j];
+                r += (kj < ki) | ((kj == ki) & (j < p));
+            }
+            s_dst[p] = (uint16_t)(s0 + r);
+        }
+        wsync();
+
+        // ---- 5. write the formatted rows of the owned range
+        for (int p = h0 + wt; p < oend; p += NW) {
+            const uint32_t dp = s_dst[p];
+            if (dp == 0xffff) continue;   // rows of a fallback case
+            const int64_t g = base + dp;
+            a.key_out[g] = s_key[p];
+            a.act_out[g] = s_act[p];
+            if (WI) a.perm_out[g] = s_idx[p];
         }
     }
     __syncthreads();
+
+    // ---- 6. case offsets and codes (ranks known now)
     const uint32_t R0 = s_prefix;
     for (uint32_t h = tid; h < H; h += FMT_THREADS) {
         const int hp = s_head[h];
         a.off[R0 + h] = (uint32_t)(base + hp);
         a.case_code[R0 + h] = a.case_min + (uint32_t)shr64(s_key[hp], tb);
     }
+    if (tid < min(s_nbig, 16u)) a.big[atomicAdd(a.big_count, 1u)] = R0 + s_bigh[tid];
     if (tid == 0 && base + tn >= a.n) {
         a.off[R0 + H] = (uint32_t)a.n;
         *a.n_cases = R0 + H;
-    }
-    if (H == 0) return;
-    int ext = s_ext;
-    int Hown = (int)H;
-    if (ext < 0) {   // the last case runs far past the tile: exact fallback, not owned here
-        Hown = (int)H - 1;
-        ext = 0;
-        if (tid == 0) a.big[atomicAdd(a.big_count, 1u)] = R0 + H - 1;
-    }
-    const int h0 = s_head[0];
-    const int oend = Hown == (int)H ? tn + ext : (int)s_head[H - 1];   // owned rows [h0, oend)
-    for (int p = tn + tid; p < oend; p += FMT_THREADS) {                // extension rows
-        const int64_t i = base + p;
-        s_key[p] = a.gkey[i];
-        s_act[p] = a.gact[i];
-        if (WI) s_idx[p] = a.gidx[i];
-        s_ci[p] = (uint16_t)(H - 1);
-    }
-    __syncthreads();
-
-    // ---- 4. rank each row inside its case: #(key_j < key_p) + #(j < p with key_j == key_p).
-    // Event-parallel with one uniform loop per case (a warp mostly reads one
-    // case -> broadcast smem reads, equal trip counts).
-    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
-        const uint32_t h = s_ci[p];
-        const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
-        if (e0 - s0 > FMT_WARP_MAX) {      // long case: exact fallback
-            s_dst[p] = 0xffff;
-            if (p == s0) a.big[atomicAdd(a.big_count, 1u)] = R0 + h;
-            continue;
-        }
-        int r = 0;
-        const uint64_t ki = s_key[p];
-        for (int j = s0; j < e0; ++j) {
-            const uint64_t kj = s_key[j];
-            r += (kj < ki) | ((kj == ki) & (j < p));
-        }
-        s_dst[p] = (uint16_t)(s0 + r);
-    }
-    __syncthreads();
-
-    // ---- 5. write the formatted rows of the owned range
-    for (int p = h0 + tid; p < oend; p += FMT_THREADS) {
-        const uint32_t dp = s_dst[p];
-        if (dp == 0xffff) continue;   // rows of a fallback case
-        const int64_t g = base + dp;
-        a.key_out[g] = s_key[p];
-        a.act_out[g] = s_act[p];
-        if (WI) a.perm_out[g] = s_idx[p];
     }
 }
 
