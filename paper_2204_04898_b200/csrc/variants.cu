@@ -94,7 +94,7 @@ __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint6
 // (Zipf head) costs one global atomic per CTA, not one per case -- then
 // publishes every distinct key of the chunk to the global table.
 constexpr int INS_THREADS = 256, INS_IPT = 4, INS_CHUNK = INS_THREADS * INS_IPT, INS_SLOTS = 2048;
-constexpr size_t INS_SMEM = (size_t)INS_SLOTS * (8 + 8 + 4 + 4 + 8);
+constexpr size_t INS_SMEM = (size_t)INS_SLOTS * (8 + 8 + 4 + 4 + 8 + 2);
 
 template <class OFF>
 __global__ __launch_bounds__(INS_THREADS) void k_insert(
@@ -108,6 +108,8 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     unsigned long long* s_g = s_k2 + INS_SLOTS;
     uint32_t* s_w = (uint32_t*)(s_g + INS_SLOTS);
     uint32_t* s_rep = s_w + INS_SLOTS;
+    uint16_t* s_list = (uint16_t*)(s_rep + INS_SLOTS);
+    __shared__ uint32_t s_scan[INS_THREADS / 32 + 1];
     (void)off;
     for (uint64_t chunk = blockIdx.x; chunk * INS_CHUNK < n_items; chunk += gridDim.x) {
         for (int i = threadIdx.x; i < INS_SLOTS; i += INS_THREADS) {
@@ -169,9 +171,26 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
             }
         }
         __syncthreads();
-        // phase C: publish each distinct local key once
-        for (int sl = threadIdx.x; sl < INS_SLOTS; sl += INS_THREADS) {
-            if (s_k1[sl] == 0 || s_w[sl] == 0) continue;
+        // phase C: compact the occupied local slots (so every thread probes ~2
+        // keys, not 8 mostly-empty slots in sequence), then publish each
+        // distinct local key once
+        uint32_t nocc;
+        {
+            constexpr int PER = INS_SLOTS / INS_THREADS;
+            uint32_t occ = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int sl = threadIdx.x + j * INS_THREADS;
+                occ |= (s_k1[sl] != 0 && s_w[sl] != 0) ? (1u << j) : 0u;
+            }
+            uint32_t pos = block_excl_scan<INS_THREADS>(__popc(occ), s_scan, &nocc);
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+                if (occ & (1u << j)) s_list[pos++] = (uint16_t)(threadIdx.x + j * INS_THREADS);
+            __syncthreads();
+        }
+        for (uint32_t q = threadIdx.x; q < nocc; q += INS_THREADS) {
+            const int sl = s_list[q];
             uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], overflow);
             s_g[sl] = g;
             if (g == ~0ull) continue;
@@ -200,6 +219,34 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     }
 }
 
+// 8 bytes starting at an arbitrary byte offset, from two aligned 8-byte loads
+// (the activity arrays carry >= 16 bytes of tail padding).
+__device__ __forceinline__ uint64_t load8_at(const uint8_t* b, uint64_t off) {
+    const uint64_t* w = (const uint64_t*)(b + (off & ~7ull));
+    const uint32_t sh = (uint32_t)(off & 7) * 8;
+    const uint64_t w0 = w[0];
+    return sh ? (w0 >> sh) | (w[1] << (64 - sh)) : w0;
+}
+
+// exact sequence equality of acts[f, f+len) and acts[rf, rf+len): 8 bytes per
+// step for byte-wide activities, branch-free (no early exit)
+template <class ACT>
+__device__ __forceinline__ bool seq_equal(const ACT* acts, uint64_t f, uint64_t rf, uint64_t len) {
+    if constexpr (sizeof(ACT) == 1) {
+        const uint8_t* b = (const uint8_t*)acts;
+        uint64_t diff = 0;
+        for (uint64_t i = 0; i < len; i += 8) {
+            const uint64_t m = (len - i >= 8) ? ~0ull : ((1ull << (8 * (len - i))) - 1);
+            diff |= (load8_at(b, f + i) ^ load8_at(b, rf + i)) & m;
+        }
+        return diff == 0;
+    } else {
+        uint32_t diff = 0;
+        for (uint64_t i = 0; i < len; ++i) diff |= (uint32_t)acts[f + i] ^ (uint32_t)acts[rf + i];
+        return diff == 0;
+    }
+}
+
 // Each item compares its sequence with its slot representative's; the rep is
 // the item whose order key equals slot.rep: item_of_order maps order -> item
 // (identity when order == nullptr).
@@ -221,18 +268,7 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
         const uint32_t rep_it = order ? item_of_rep_slot[sl] : rep;
         const OFF f = off[it], l = off[it + 1], rf = off[rep_it], rl = off[rep_it + 1];
         bool same = (l - f) == (rl - rf);
-        if (same) {   // branch-free compare: independent loads, no early exit
-            uint32_t diff = 0;
-            const OFF len = l - f;
-            OFF i = 0;
-            for (; i + 4 <= len; i += 4)
-                diff |= ((uint32_t)acts[f + i] ^ (uint32_t)acts[rf + i]) |
-                        ((uint32_t)acts[f + i + 1] ^ (uint32_t)acts[rf + i + 1]) |
-                        ((uint32_t)acts[f + i + 2] ^ (uint32_t)acts[rf + i + 2]) |
-                        ((uint32_t)acts[f + i + 3] ^ (uint32_t)acts[rf + i + 3]);
-            for (; i < len; ++i) diff |= (uint32_t)acts[f + i] ^ (uint32_t)acts[rf + i];
-            same = diff == 0;
-        }
+        if (same) same = seq_equal(acts, (uint64_t)f, (uint64_t)rf, (uint64_t)(l - f));
         if (!same) {
             atomicAdd(&table[sl].weight, (unsigned long long)(0ull - (weight ? weight[it] : 1ull)));
             pending[it] = 1;
