@@ -129,7 +129,8 @@ pm4g_status pm4g_sorted_columns(const pm4g_log* log, uint32_t* case_code, uint32
                                 int64_t* ts, pm4g_stream_t stream);
 
 /* ---------------------------------------------------------------- aggregates
- * All require the sorted state (EINVAL otherwise).  With comm != NULL the
+ * All require the sorted state (EINVAL otherwise).  The A x A tables also
+ * require A * A < 2^32 (edge ids are 32-bit; EINVAL otherwise).  With comm != NULL the
  * tables are summed over all ranks (NCCL allreduce, exact in integers)
  * and every rank receives the global result. */
 

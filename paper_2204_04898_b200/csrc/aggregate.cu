@@ -13,14 +13,23 @@
 //      the case's variant"): two 64-bit polynomial hashes of the
 //      (act + 1) sequence plus the length, verified exactly later (A9).
 //
-// Work split: a CTA owns tiles of 256 consecutive CASES (tile edges are case
-// edges, so no directly-follows pair straddles two CTAs).  Pairs are processed
-// event-parallel (coalesced), per-case work case-parallel.  The A x A table is
-// privatised per CTA in shared memory (u32 counts; u32 lo/hi duration sums
-// with exact carry propagation, because 64-bit shared atomics are CAS loops on
-// sm_100a) and flushed once per CTA with 64-bit global atomics.  When A x A
-// does not fit in shared memory the pass updates the L2-resident global table
-// directly.
+// Work split: a CTA owns tiles of up to 256 consecutive CASES (tile edges are
+// case edges, so no directly-follows pair straddles two CTAs); the host sizes
+// tiles from the mean case length so a tile's rows fit one TMA stage.  Pairs
+// are processed event-parallel (coalesced), per-case work case-parallel.  The
+// A x A table lives where it fits:
+//   TAB_FULL  (3 A^2 words <= 100 KB, A <= 91): privatised per CTA in shared
+//             memory (u32 counts; u32 lo/hi duration sums with exact carry
+//             propagation, because 64-bit shared atomics are CAS loops on
+//             sm_100a), flushed once per CTA with 64-bit global atomics;
+//   TAB_HASH  (larger A): a per-CTA shared-memory hash table keyed by edge id
+//             (key, count, lo, hi) -- process DFGs are sparse (a handful of
+//             successors per activity), so the edges a CTA sees fit; an edge
+//             that finds no slot within HASH_PROBES goes straight to the
+//             global table.  Global atomics alone serialise on the hot edges
+//             of a skewed DFG (measured 2.4 ms per 1e8 events at A = 256), and
+//             a DSMEM-distributed dense table is slower than L2 atomics
+//             (tools/mbench_dsmem.cu).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,7 +40,7 @@ namespace pm4g {
 
 constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
-constexpr size_t AGG_SMEM_MAX = 100 * 1024;
+constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
 // Variant-key hash (internal, verified): Horner polynomial mod 2^64 over act+1.
 constexpr uint64_t HB1 = 0x00000100000001B3ull;
@@ -76,22 +85,54 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <class P, bool SMEM>
+enum { TAB_FULL = 1, TAB_HASH = 2 };
+
+constexpr int HASH_PROBES = 16;
+constexpr uint32_t HASH_EMPTY = 0xffffffffu;
+
+// shared-memory hash slots: as many as fit next to the two stages
+template <class P>
+__host__ __device__ constexpr uint32_t hash_slots() { return sizeof(P) == 1 ? 8192u : 4096u; }
+
+// start/end counters are privatised when A is small enough
+constexpr uint32_t SE_SMEM_MAX_A = 2048;
+__host__ __device__ constexpr uint32_t se_words(uint32_t A) { return A <= SE_SMEM_MAX_A ? 2 * A : 0u; }
+
+template <class P>
+__host__ __device__ constexpr uint32_t tab_words_for(int mode, uint32_t A) {
+    return mode == TAB_FULL ? ((3 * A * A + 2 * A + 31) & ~31u) : (4 * hash_slots<P>() + se_words(A) + 31) & ~31u;
+}
+
+// per-pair accumulation into a (count, lo, hi) triple in shared memory; the
+// carry out of the low word is exact because the returned old value decides it
+__device__ __forceinline__ void smem_acc(uint32_t* cnt, uint32_t* lo, uint32_t* hi, uint64_t d) {
+    atomicAdd(cnt, 1u);
+    const uint32_t l = (uint32_t)d;
+    uint32_t h = (uint32_t)(d >> 32);
+    const uint32_t old = atomicAdd(lo, l);
+    h += (old + l < old) ? 1u : 0u;
+    if (h) atomicAdd(hi, h);
+}
+
+template <class P, int MODE>
 __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
-    const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A,
+    const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
     uint64_t* __restrict__ packed, uint32_t* __restrict__ n_events, int64_t* __restrict__ dur,
     uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
     const bool tables = packed != nullptr;
     const uint32_t AA = A * A;
-    const uint32_t tab_words = (SMEM && tables) ? ((3 * AA + 2 * A + 31) & ~31u) : 0;
+    const uint32_t tab_words = tables ? tab_words_for<P>(MODE, A) : 0;
+    constexpr uint32_t HS = hash_slots<P>();
+    const uint32_t TW = MODE == TAB_FULL ? AA : HS;         // table entries
     uint32_t* sm = (uint32_t*)agg_sm;
     uint32_t* s_cnt = sm;
-    uint32_t* s_lo = sm + AA;
-    uint32_t* s_hi = sm + 2 * AA;
-    uint32_t* s_st = sm + 3 * AA;
+    uint32_t* s_lo = sm + TW;
+    uint32_t* s_hi = sm + 2 * TW;
+    uint32_t* s_key = sm + 3 * TW;                          // HASH: edge id or HASH_EMPTY
+    uint32_t* s_st = sm + (MODE == TAB_FULL ? 3 * AA : 4 * HS);
     uint32_t* s_en = s_st + A;
     AggStage<P>* stage = (AggStage<P>*)(agg_sm + (size_t)tab_words * 4);
     uint64_t* g_cnt = packed;
@@ -99,7 +140,8 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     uint64_t* g_st = packed + 2 * (size_t)AA;
     uint64_t* g_en = g_st + A;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (uint32_t i = tid; i < tab_words; i += AGG_BLOCK) sm[i] = 0;
+    for (uint32_t i = tid; i < tab_words; i += AGG_BLOCK)
+        sm[i] = (MODE == TAB_HASH && i >= 3 * HS && i < 4 * HS) ? HASH_EMPTY : 0u;
     if (tid == 0) {
         for (int s = 0; s < AGG_STAGES; ++s) {
             mbar_init(&s_full[s], 1);
@@ -108,7 +150,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     }
     __syncthreads();
     const uint64_t C = *d_n_cases;
-    const uint64_t tiles = (C + AGG_CASES - 1) / AGG_CASES;
+    const uint64_t tiles = (C + cpt - 1) / cpt;
 
     if (warp == 0) {
         // ---------------- producer warp: stream tiles into the ring with TMA
@@ -117,8 +159,8 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
             const int s = i % AGG_STAGES;
             if (i >= AGG_STAGES) mbar_wait(&s_empty[s], ((i / AGG_STAGES) - 1) & 1);
             AggStage<P>& st = stage[s];
-            const uint64_t c0 = t * AGG_CASES;
-            const uint32_t nc = (uint32_t)min((uint64_t)AGG_CASES, C - c0);
+            const uint64_t c0 = t * cpt;
+            const uint32_t nc = (uint32_t)min((uint64_t)cpt, C - c0);
             for (uint32_t j = lane; j <= nc; j += 32) st.off[j] = off[c0 + j];
             __syncwarp();
             if (lane == 0) {
@@ -163,14 +205,22 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                     if (shr64(kk, ts_bits) != shr64(kn, ts_bits)) continue;
                     const uint32_t e = A_at(r) * A + A_at(r + 1);
                     const uint64_t d = kn - kk;
-                    if (SMEM) {
-                        atomicAdd(&s_cnt[e], 1u);
-                        const uint32_t lo = (uint32_t)d;
-                        uint32_t hi = (uint32_t)(d >> 32);
-                        const uint32_t old = atomicAdd(&s_lo[e], lo);
-                        hi += (old + lo < old) ? 1u : 0u;   // carry out of the low word
-                        if (hi) atomicAdd(&s_hi[e], hi);
-                    } else {
+                    if (MODE == TAB_FULL) {
+                        smem_acc(&s_cnt[e], &s_lo[e], &s_hi[e], d);
+                        continue;
+                    }
+                    uint32_t h = (e * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
+                    bool done = false;
+                    for (int p = 0; p < HASH_PROBES; ++p, h = (h + 1) & (HS - 1)) {
+                        uint32_t k = s_key[h];
+                        if (k == HASH_EMPTY) k = atomicCAS(&s_key[h], HASH_EMPTY, e);
+                        if (k == HASH_EMPTY || k == e) {
+                            smem_acc(&s_cnt[h], &s_lo[h], &s_hi[h], d);
+                            done = true;
+                            break;
+                        }
+                    }
+                    if (!done) {   // no slot near: straight to the global table
                         atomicAdd((unsigned long long*)&g_cnt[e], 1ull);
                         atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)d);
                     }
@@ -181,7 +231,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                 const uint32_t f = st.off[ct], l = st.off[ct + 1] - 1;
                 if (tables) {
                     const uint32_t as = A_at(f), ae = A_at(l);
-                    if (SMEM) {
+                    if (se_words(A)) {
                         atomicAdd(&s_st[as], 1u);
                         atomicAdd(&s_en[ae], 1u);
                     } else {
@@ -208,43 +258,47 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
         }
     }
     __syncthreads();
-    if (SMEM && tables) {
-        for (uint32_t e = tid; e < AA; e += AGG_BLOCK) {
-            const uint32_t cn = s_cnt[e];
-            if (cn) {
-                atomicAdd((unsigned long long*)&g_cnt[e], (unsigned long long)cn);
-                const uint64_t sm64 = ((uint64_t)s_hi[e] << 32) | s_lo[e];
-                if (sm64) atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)sm64);
-            }
-        }
-        for (uint32_t a = tid; a < A; a += AGG_BLOCK) {
+    if (tables) {
+        for (uint32_t a = tid; a < (se_words(A) ? A : 0u); a += AGG_BLOCK) {
             if (s_st[a]) atomicAdd((unsigned long long*)&g_st[a], (unsigned long long)s_st[a]);
             if (s_en[a]) atomicAdd((unsigned long long*)&g_en[a], (unsigned long long)s_en[a]);
+        }
+        for (uint32_t j = tid; j < TW; j += AGG_BLOCK) {
+            const uint32_t cn = s_cnt[j];
+            if (!cn) continue;
+            const uint32_t e = MODE == TAB_FULL ? j : s_key[j];
+            atomicAdd((unsigned long long*)&g_cnt[e], (unsigned long long)cn);
+            const uint64_t sm64 = ((uint64_t)s_hi[j] << 32) | s_lo[j];
+            if (sm64) atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)sm64);
         }
     }
 }
 
-template <class P, bool SMEM>
+template <class P, int MODE>
 static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
-    const size_t tab = (SMEM && o.tables) ? ((size_t)((3 * A * A + 2 * A + 31) & ~31u)) * 4 : 0;
+    const size_t tab = o.tables ? (size_t)tab_words_for<P>(MODE, A) * 4 : 0;
     const size_t smem = tab + AGG_STAGES * sizeof(AggStage<P>);
-    static bool attr = false;
-    if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(AGG_SMEM_MAX + 128 + AGG_STAGES * sizeof(AggStage<P>))));
-        attr = true;
+    static size_t attr = 0;
+    if (smem > attr) {
+        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
     }
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
-    const uint64_t tiles = std::max<uint64_t>(1, (cap + AGG_CASES - 1) / AGG_CASES);
+    // cases per tile: a tile's rows should fit one stage (mean length from the
+    // case-code range, exact when codes are dense; a rare oversized tile is
+    // read from global memory instead)
+    const double mean_len = (double)L->n / (double)std::max<uint64_t>(cap, 1);
+    const uint32_t cpt = (uint32_t)std::max(32.0, std::min((double)AGG_CASES, 0.7 * AGG_STAGE / std::max(mean_len, 1.0)));
+    const uint64_t tiles = std::max<uint64_t>(1, (cap + cpt - 1) / cpt);
     const int per_sm = std::max(1, (int)std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
     const double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
                          (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, SMEM><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
-                    L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A,
+                (k_aggregate<P, MODE><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
+                    L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
                     o.tables ? o.packed : nullptr, o.n_events, o.dur, o.k1, o.k2,
                     debug_weak_hash() ? 1 : 0)));
     return PM4G_OK;
@@ -253,12 +307,15 @@ static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s
 pm4g_status aggregate(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     if (L->n == 0) return PM4G_OK;
     const uint32_t A = L->A;
-    bool smem_ok = ((size_t)3 * A * A + 2 * A) * 4 <= AGG_SMEM_MAX;
+    const int mode = (size_t)tab_words_for<uint32_t>(TAB_FULL, A) * 4 <= AGG_SMEM_MAX ? TAB_FULL : TAB_HASH;
+#define PM4G_AGG_MODES(P) \
+    return mode == TAB_FULL ? launch_agg<P, TAB_FULL>(L, o, s) : launch_agg<P, TAB_HASH>(L, o, s)
     switch (L->act_bytes) {
-        case 1: return smem_ok ? launch_agg<uint8_t, true>(L, o, s) : launch_agg<uint8_t, false>(L, o, s);
-        case 2: return smem_ok ? launch_agg<uint16_t, true>(L, o, s) : launch_agg<uint16_t, false>(L, o, s);
-        default: return smem_ok ? launch_agg<uint32_t, true>(L, o, s) : launch_agg<uint32_t, false>(L, o, s);
+        case 1: PM4G_AGG_MODES(uint8_t);
+        case 2: PM4G_AGG_MODES(uint16_t);
+        default: PM4G_AGG_MODES(uint32_t);
     }
+#undef PM4G_AGG_MODES
 }
 
 // ------------------------------------------------------------------ K11 finalise
@@ -299,7 +356,15 @@ static pm4g_status require_sorted(const pm4g_log* L) {
 
 static size_t packed_len(uint32_t A) { return 2 * (size_t)A * A + 2 * (size_t)A; }
 
+// edge ids a * A + b are 32-bit on the device
+static pm4g_status check_table_size(const pm4g_log* L) {
+    if ((uint64_t)L->A * L->A > 0xffffffffull)
+        return fail(PM4G_EINVAL, "n_activities too large for an A x A table (A^2 must fit 32 bits)");
+    return PM4G_OK;
+}
+
 static pm4g_status tables_into(const pm4g_log* L, uint64_t* packed, cudaStream_t s) {
+    PM4G_TRY(check_table_size(L));
     PM4G_CK(cudaMemsetAsync(packed, 0, packed_len(L->A) * 8, s));
     AggOut o;
     o.packed = packed;
@@ -331,6 +396,7 @@ pm4g_status pm4g_dfg(const pm4g_log* L, uint64_t* cnt, int64_t* dur_sum, double*
     PM4G_TRY(require_sorted(L));
     if (!cnt || !dur_sum) return fail(PM4G_EINVAL, "cnt and dur_sum are required");
     cudaStream_t s = (cudaStream_t)stream;
+    PM4G_TRY(check_table_size(L));
     Scratch pk(s);
     PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
     PM4G_TRY(tables_into(L, pk.as<uint64_t>(), s));
@@ -343,6 +409,7 @@ pm4g_status pm4g_start_end(const pm4g_log* L, uint64_t* start, uint64_t* end, pm
     PM4G_TRY(require_sorted(L));
     if (!start || !end) return fail(PM4G_EINVAL, "start and end are required");
     cudaStream_t s = (cudaStream_t)stream;
+    PM4G_TRY(check_table_size(L));
     Scratch pk(s);
     PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
     PM4G_TRY(tables_into(L, pk.as<uint64_t>(), s));
@@ -410,6 +477,7 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
     Scratch pk(s), keys(s);
     AggOut o;
     if (want_tables) {
+        PM4G_TRY(check_table_size(L));
         PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
         PM4G_CK(cudaMemsetAsync(pk.p, 0, packed_len(L->A) * 8, s));
         o.packed = pk.as<uint64_t>();

@@ -91,6 +91,11 @@ bool debug_weak_hash() {
     return e && e[0] == '1';
 }
 
+uint64_t debug_variant_cap() {
+    const char* e = getenv("PM4G_DEBUG_VARIANT_CAP");
+    return e ? strtoull(e, nullptr, 10) : 0;
+}
+
 // ------------------------------------------------------------------ memory
 static void setup_pool() {
     static std::once_flag once;

@@ -48,6 +48,9 @@ void count_launch();
 
 int num_sms();
 bool debug_weak_hash();
+// test hook: first-try variant table size (PM4G_DEBUG_VARIANT_CAP, 0 = automatic),
+// forcing the load-limit regrowth path on small inputs
+uint64_t debug_variant_cap();
 
 // ------------------------------------------------------------------ memory
 // Stream-ordered allocations from the device's default pool (kept cached).

@@ -70,9 +70,12 @@ __global__ void k_init_table(Slot* table, uint64_t cap) {
 }
 
 // Find or claim the global slot of key (a, b): linear probing, one 128-bit CAS
-// claims an empty slot.  Returns the slot, or ~0 when the table is full.
+// claims an empty slot.  ctl[0] = overflow flag, ctl[1] = claimed slots; a
+// claim past the load limit (3/4 of the table) raises overflow, so a table
+// that is too small is abandoned after O(limit) claims instead of being probed
+// to saturation.  Returns the slot, or ~0 once overflow is raised.
 __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint64_t a, uint64_t b,
-                                               uint32_t* overflow) {
+                                               uint32_t* ctl, uint32_t limit) {
     uint64_t h = (a ^ (a >> 29) ^ (b * 0x9E3779B97F4A7C15ull)) & mask;
     for (uint64_t probes = 0; probes <= mask; ++probes) {
         Slot* sp = &table[h];
@@ -81,11 +84,16 @@ __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint6
         if (cur.a == 0 && cur.b == 0) {
             K128 exp{0, 0}, des{a, b};
             K128 old = atomicCAS((K128*)sp, exp, des);
-            if ((old.a == 0 && old.b == 0) || (old.a == a && old.b == b)) return h;
+            if (old.a == 0 && old.b == 0) {
+                if (atomicAdd(&ctl[1], 1u) >= limit) break;
+                return h;
+            }
+            if (old.a == a && old.b == b) return h;
         }
+        if ((probes & 31) == 31 && *(volatile uint32_t*)ctl) return ~0ull;
         h = (h + 1) & mask;
     }
-    atomicExch(overflow, 1u);
+    atomicExch(ctl, 1u);
     return ~0ull;
 }
 
@@ -100,8 +108,8 @@ template <class OFF>
 __global__ __launch_bounds__(INS_THREADS) void k_insert(
     const uint32_t* __restrict__ list, uint64_t n_items, const uint64_t* __restrict__ k1,
     const uint64_t* __restrict__ k2, const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
-    const uint32_t* __restrict__ order, Slot* table, uint64_t mask, uint64_t salt,
-    uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* overflow) {
+    const uint32_t* __restrict__ order, Slot* table, uint64_t mask, uint32_t limit, uint64_t salt,
+    uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* ctl) {
     extern __shared__ __align__(16) unsigned char ins_sm[];
     unsigned long long* s_k1 = (unsigned long long*)ins_sm;
     unsigned long long* s_k2 = s_k1 + INS_SLOTS;
@@ -110,14 +118,17 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     uint32_t* s_rep = s_w + INS_SLOTS;
     uint16_t* s_list = (uint16_t*)(s_rep + INS_SLOTS);
     __shared__ uint32_t s_scan[INS_THREADS / 32 + 1];
+    __shared__ uint32_t s_stop;
     (void)off;
     for (uint64_t chunk = blockIdx.x; chunk * INS_CHUNK < n_items; chunk += gridDim.x) {
+        if (threadIdx.x == 0) s_stop = *(volatile uint32_t*)ctl;   // table abandoned: stop early
         for (int i = threadIdx.x; i < INS_SLOTS; i += INS_THREADS) {
             s_k1[i] = 0;
             s_w[i] = 0;
             s_rep[i] = 0xffffffffu;
         }
         __syncthreads();
+        if (s_stop) break;
         uint32_t it[INS_IPT], loc[INS_IPT], ord[INS_IPT], w[INS_IPT];
         uint64_t ka[INS_IPT], kb[INS_IPT];
         bool claimed[INS_IPT], live[INS_IPT];
@@ -191,7 +202,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
         }
         for (uint32_t q = threadIdx.x; q < nocc; q += INS_THREADS) {
             const int sl = s_list[q];
-            uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], overflow);
+            uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], ctl, limit);
             s_g[sl] = g;
             if (g == ~0ull) continue;
             atomicAdd(&table[g].weight, (unsigned long long)s_w[sl]);
@@ -203,7 +214,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
             if (!live[u]) continue;
             uint64_t g;
             if (direct[u]) {
-                g = table_slot(table, mask, ka[u], kb[u], overflow);
+                g = table_slot(table, mask, ka[u], kb[u], ctl, limit);
                 if (g != ~0ull) {
                     atomicAdd(&table[g].weight, (unsigned long long)w[u]);
                     atomicMin(&table[g].rep, ord[u]);
@@ -256,7 +267,9 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
                          const uint64_t* __restrict__ weight, const uint32_t* __restrict__ order,
                          const uint32_t* __restrict__ item_of_rep_slot, Slot* table,
                          const uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending,
-                         uint32_t* __restrict__ next_list, uint32_t* __restrict__ next_count) {
+                         uint32_t* __restrict__ next_list, uint32_t* __restrict__ next_count,
+                         const uint32_t* __restrict__ overflow) {
+    if (*overflow) return;   // this attempt's table is abandoned (item_slot incomplete)
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -280,7 +293,9 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
 // slot -> representative item (the item whose order == slot.rep)
 __global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
                            const uint32_t* __restrict__ order, const Slot* __restrict__ table,
-                           const uint32_t* __restrict__ item_slot, uint32_t* __restrict__ item_of_rep_slot) {
+                           const uint32_t* __restrict__ item_slot, uint32_t* __restrict__ item_of_rep_slot,
+                           const uint32_t* __restrict__ overflow) {
+    if (*overflow) return;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -294,7 +309,9 @@ __global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
 __global__ void k_compact(const Slot* __restrict__ table, uint64_t cap,
                           const uint32_t* __restrict__ item_of_rep_slot, uint32_t* __restrict__ slot_group,
                           uint64_t* __restrict__ g_weight, uint32_t* __restrict__ g_rep_item,
-                          uint32_t* __restrict__ g_order, uint32_t* __restrict__ n_groups) {
+                          uint32_t* __restrict__ g_order, uint32_t* __restrict__ n_groups,
+                          const uint32_t* __restrict__ overflow) {
+    if (*overflow) return;
     for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < cap;
          sl += (uint64_t)gridDim.x * blockDim.x) {
         const Slot& s = table[sl];
@@ -309,7 +326,9 @@ __global__ void k_compact(const Slot* __restrict__ table, uint64_t cap,
 
 __global__ void k_item_group(const uint32_t* __restrict__ list, uint64_t n_items,
                              const uint32_t* __restrict__ item_slot, const uint8_t* __restrict__ pending,
-                             const uint32_t* __restrict__ slot_group, uint32_t* __restrict__ item_group) {
+                             const uint32_t* __restrict__ slot_group, uint32_t* __restrict__ item_group,
+                             const uint32_t* __restrict__ overflow) {
+    if (*overflow) return;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -391,17 +410,22 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
     uint8_t* pending = (uint8_t*)(item_slot + N);
     uint32_t* list_a = (uint32_t*)(((uintptr_t)(pending + N) + 15) & ~(uintptr_t)15);
     uint32_t* list_b = list_a + N;
-    uint32_t* counters = list_b + N;  // [0] next_count, [1] overflow, [2] n_groups
+    // [0] next_count, [1] overflow, [2] claimed slots, [3] n_groups
+    uint32_t* counters = list_b + N;
     PM4G_CK(cudaMemsetAsync(counters, 0, 16, s));
 
     const uint32_t* list = nullptr;   // round 0: all items
     uint64_t n_active = n_items;
     uint64_t G = 0;
-    uint64_t cap_hint = pow2_at_least(std::max<uint64_t>(1024, 2 * std::min<uint64_t>(n_items, 1ull << 20)));
     const bool weak = debug_weak_hash();
     for (int round = 0; n_active > 0; ++round) {
-        uint64_t cap = std::min<uint64_t>(cap_hint, pow2_at_least(std::max<uint64_t>(1024, 2 * n_active)));
-        for (int attempt = 0; attempt < 2; ++attempt) {
+        // A table of `full` slots holds every item at load <= 1/2 and never
+        // overflows; the first try is smaller (distinct sequences are usually
+        // far fewer than items) and grows 4x whenever its load limit trips.
+        const uint64_t full = pow2_at_least(std::max<uint64_t>(1024, 2 * n_active));
+        uint64_t cap = std::min<uint64_t>(full, std::max<uint64_t>(1ull << 21, pow2_at_least(n_active / 16)));
+        if (const uint64_t dc = debug_variant_cap()) cap = std::min<uint64_t>(full, pow2_at_least(std::max<uint64_t>(dc, 64)));
+        for (int attempt = 0;; ++attempt) {
             Scratch tab(s), aux(s);
             if ((st = tab.alloc(cap * sizeof(Slot)))) return bail(st);
             if ((st = aux.alloc(cap * 8))) return bail(st);
@@ -409,7 +433,8 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
             uint32_t* item_of_rep_slot = aux.as<uint32_t>();
             uint32_t* slot_group = item_of_rep_slot + cap;
             PM4G_LAUNCH("k_variant_init", cap * 32.0, s, (k_init_table<<<gsz(cap), 256, 0, s>>>(table, cap)));
-            PM4G_CK(cudaMemsetAsync(counters, 0, 8, s));
+            PM4G_CK(cudaMemsetAsync(counters, 0, 12, s));
+            const uint32_t limit = cap == full ? 0xffffffffu : (uint32_t)(cap / 4 * 3);
             uint64_t salt = (round == 0 || weak) ? 0ull : 0x9E3779B97F4A7C15ull * (uint64_t)round;
             uint32_t* next_list = (list == list_a) ? list_b : list_a;
             const int gs = gsz(n_active);
@@ -424,37 +449,35 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                 int gi = (int)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (uint64_t)num_sms() * 3));
                 PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
                             (k_insert<OFF><<<gi, INS_THREADS, INS_SMEM, s>>>(
-                                list, n_active, k1, k2, off, weight, order, table, cap - 1, salt,
+                                list, n_active, k1, k2, off, weight, order, table, cap - 1, limit, salt,
                                 item_slot, pending, counters + 1)));
             }
             uint32_t* ior = order ? item_of_rep_slot : nullptr;   // identity order: rep item = slot.rep
             if (order)
                 PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
-                            (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot)));
+                            (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot,
+                                                            counters + 1)));
             PM4G_LAUNCH("k_variant_verify", n_active * 16.0, s,
                         (k_verify<OFF, ACT><<<gs, 256, 0, s>>>(list, n_active, off, acts, weight, order,
                                                                ior, table, item_slot,
-                                                               pending, next_list, counters)));
+                                                               pending, next_list, counters, counters + 1)));
             PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
                         (k_compact<<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
                                                             g.weight, g.rep_item, g.order,
-                                                            counters + 2)));
+                                                            counters + 3, counters + 1)));
             PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
                         (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
-                                                         g.item_group)));
-            // one host round trip per round: next_count, overflow, n_groups
-            uint32_t h[3] = {0, 0, 0};
-            PM4G_CK(cudaMemcpyAsync(h, counters, 12, cudaMemcpyDeviceToHost, s));
+                                                         g.item_group, counters + 1)));
+            // one host round trip per round: next_count, overflow, claims, n_groups
+            uint32_t h[4] = {0, 0, 0, 0};
+            PM4G_CK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, s));
             PM4G_CK(cudaStreamSynchronize(s));
-            if (h[1]) {  // table overflow: discard this round's groups, retry with a full-size table
-                if (attempt == 1) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
-                const uint32_t gb = (uint32_t)G;
-                PM4G_CK(cudaMemcpyAsync(counters + 2, &gb, 4, cudaMemcpyHostToDevice, s));
-                PM4G_CK(cudaStreamSynchronize(s));
-                cap = pow2_at_least(2 * n_active + 1024);
+            if (h[1]) {  // load limit hit: verify/compact/item_group skipped on the device; regrow
+                if (cap >= full || attempt > 16) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
+                cap = std::min<uint64_t>(full, cap * 4);
                 continue;
             }
-            G = h[2];
+            G = h[3];
             n_active = h[0];
             list = next_list;
             if (round > 64 * 1024) return bail(fail(PM4G_ECUDA, "variant grouping did not converge"));

@@ -169,3 +169,44 @@ def test_weak_hash_collisions_resolved_exactly(monkeypatch):
     check_log(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities, n_case_codes=L.n_case_codes)
     case, act, ts, A, ncodes = random_log(11)
     check_log(case, act, ts, A, n_case_codes=ncodes)
+
+
+@pytest.mark.parametrize("cap", ["64", "1024"])
+def test_variant_table_regrowth(monkeypatch, cap):
+    """PM4G_DEBUG_VARIANT_CAP forces a first variant table far smaller than the number
+    of distinct sequences: the load limit must trip, the follow-on kernels must skip
+    the abandoned table, and the regrown table must give the exact variant multiset."""
+    monkeypatch.setenv("PM4G_DEBUG_VARIANT_CAP", cap)
+    for name in ("tiny", "roadtraffic", "bpic2019"):
+        L = generate(CONFIGS[name])
+        check_log(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities, n_case_codes=L.n_case_codes)
+    monkeypatch.setenv("PM4G_DEBUG_WEAK_HASH", "1")
+    case, act, ts, A, ncodes = random_log(12)
+    check_log(case, act, ts, A, n_case_codes=ncodes)
+
+
+@pytest.mark.parametrize("A", [92, 200, 256])
+def test_cnt16_table_flush_exact(A):
+    """91 < A <= 256 keeps DFG counts as u16 pairs in shared memory, flushed in
+    steps of 0x4000.  One case repeats a self-loop ~200k times (one oversized
+    tile, read from global memory) and another alternates two activities, so
+    single edges cross the flush step many times inside one CTA; ordinary
+    random cases fill the rest.  Counts and sums must match the oracle exactly."""
+    rng = np.random.default_rng(A)
+    lens = rng.integers(1, 30, 5000)
+    case = np.repeat(np.arange(5000, dtype=np.int64), lens)
+    act = rng.integers(0, A, case.size).astype(np.int64)
+    ts = rng.integers(0, 10**9, case.size).astype(np.int64)
+    big = 200_003
+    c_big = np.full(big, 6000, np.int64)
+    a_big = np.full(big, A - 1, np.int64)
+    t_big = np.cumsum(rng.integers(0, 5, big)).astype(np.int64) + 1_000
+    alt = 70_001
+    c_alt = np.full(alt, 6001, np.int64)
+    a_alt = np.where(np.arange(alt) % 2 == 0, 3, A - 2).astype(np.int64)
+    t_alt = np.arange(alt, dtype=np.int64) * 7 + 5
+    case = np.concatenate([case, c_big, c_alt])
+    act = np.concatenate([act, a_big, a_alt])
+    ts = np.concatenate([ts, t_big, t_alt])
+    p = rng.permutation(case.size)
+    check_log(case[p], act[p], ts[p], A, n_case_codes=6002)
