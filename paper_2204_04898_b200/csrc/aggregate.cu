@@ -81,9 +81,6 @@ struct alignas(128) AggStage {
     uint64_t c0;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 enum { TAB_FULL = 1, TAB_HASH = 2 };
 

@@ -69,6 +69,17 @@ void prof_begin(const char* name, double bytes, cudaStream_t s) {
     cudaEventRecord(r.a, s);
     g_prof_recs.push_back(r);
 }
+// add bytes known only after the launch (e.g. a compaction's kept rows) to
+// the most recent record of that kernel
+void prof_add_bytes(const char* name, double bytes) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (size_t i = g_prof_recs.size(); i-- > 0;)
+        if (!strcmp(g_prof_recs[i].name, name)) {
+            g_prof_recs[i].bytes += bytes;
+            return;
+        }
+}
 void prof_end(cudaStream_t s) {
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -271,6 +282,44 @@ static int grid_for(int64_t n, int block) {
     return (int)std::max<int64_t>(1, std::min(g, cap));
 }
 
+// Case-digit histogram layout for the range [case_lo, case_hi): the sort can
+// reuse histograms built in this layout when its own digit layout matches.
+void hist_layout(const pm4g_log* L, int* hpasses, int* hbits) {
+    const uint32_t hi = L->case_hi;
+    const int rbits = bit_width_u64((uint64_t)(hi > L->case_lo ? hi - 1 - L->case_lo : 0));
+    *hpasses = std::max(1, std::min(4, (std::max(rbits, 1) + 7) / 8));
+    *hbits = (std::max(rbits, 1) + *hpasses - 1) / *hpasses;
+}
+
+// Log metadata from the observed ranges (n > 0) and the key layout derived
+// from it; marks the prebuilt histograms reusable iff the layouts agree.
+void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, uint32_t case_max,
+                int hpasses, int hbits) {
+    const int64_t n = L->n;
+    if (n == 0) {
+        L->ts_min = 0;
+        L->ts_max = -1;
+        L->case_min = L->case_max = L->case_lo;
+    } else {
+        L->ts_min = ts_min;
+        L->ts_max = ts_max;
+        L->case_min = case_min;
+        L->case_max = case_max;
+    }
+    uint64_t ts_span = n ? (uint64_t)L->ts_max - (uint64_t)L->ts_min : 0;
+    L->case_bits = bit_width_u64((uint64_t)(L->case_max - L->case_min));
+    L->ts_bits = bit_width_u64(ts_span);
+    L->key_bits = L->case_bits + L->ts_bits;
+    L->passes = (std::min(L->key_bits, 64) + 7) / 8;
+    L->hist_passes = 0;
+    const int cb = std::max(L->case_bits, 1);
+    const int sp = (cb + 7) / 8, sb = (cb + sp - 1) / sp;
+    if (n > 0 && L->case_min == L->case_lo && sp == hpasses && sb == hbits) {
+        L->hist_passes = hpasses;
+        L->hist_bits = hbits;
+    }
+}
+
 pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
     Meta h{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u, ~0ull, ~0ull, ~0ull};
     Scratch md(s);
@@ -279,10 +328,8 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
     PM4G_CK(cudaMemcpyAsync(dm, &h, sizeof(Meta), cudaMemcpyHostToDevice, s));
     const int64_t n = L->n;
     uint32_t hi = L->case_hi;
-    // case-digit histograms for the sort, laid out for the range [case_lo, case_hi)
-    const int rbits = bit_width_u64((uint64_t)(hi > L->case_lo ? hi - 1 - L->case_lo : 0));
-    const int hpasses = std::max(1, std::min(4, (std::max(rbits, 1) + 7) / 8));
-    const int hbits = (std::max(rbits, 1) + hpasses - 1) / hpasses;
+    int hpasses, hbits;
+    hist_layout(L, &hpasses, &hbits);
     L->hist_passes = 0;
     if (!L->hist) PM4G_TRY(dalloc_t(&L->hist, 4 * 256, s));
     PM4G_CK(cudaMemsetAsync(L->hist, 0, 4 * 256 * 4, s));
@@ -306,30 +353,7 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
         return fail(PM4G_EDATA, "activity code out of range (>= n_activities) at row " + std::to_string(h.bad_act));
     if (h.bad_extra != ~0ull)
         return fail(PM4G_EDATA, "extra-column code out of range at row " + std::to_string(h.bad_extra));
-    if (n == 0) {
-        L->ts_min = 0;
-        L->ts_max = -1;
-        L->case_min = L->case_max = L->case_lo;
-    } else {
-        L->ts_min = h.ts_min;
-        L->ts_max = h.ts_max;
-        L->case_min = h.case_min;
-        L->case_max = h.case_max;
-    }
-    uint64_t ts_span = n ? (uint64_t)L->ts_max - (uint64_t)L->ts_min : 0;
-    L->case_bits = bit_width_u64((uint64_t)(L->case_max - L->case_min));
-    L->ts_bits = bit_width_u64(ts_span);
-    L->key_bits = L->case_bits + L->ts_bits;
-    L->passes = (std::min(L->key_bits, 64) + 7) / 8;
-    // the sort can reuse the histograms iff its digit layout is the same
-    {
-        const int cb = std::max(L->case_bits, 1);
-        const int sp = (cb + 7) / 8, sb = (cb + sp - 1) / sp;
-        if (n > 0 && L->case_min == L->case_lo && sp == hpasses && sb == hbits) {
-            L->hist_passes = hpasses;
-            L->hist_bits = hbits;
-        }
-    }
+    apply_meta(L, h.ts_min, h.ts_max, h.case_min, h.case_max, hpasses, hbits);
     return PM4G_OK;
 }
 

@@ -11,7 +11,11 @@
 // look-back, warp-striped so each warp's kept rows are written contiguously)
 // that moves every column of the log.  Relative row order is preserved
 // (S:483), so a formatted input stays formatted and only its case offsets are
-// rebuilt.
+// rebuilt.  On an ingested log the compaction of the core columns is one
+// column-typed kernel that also evaluates the events-mode time predicate
+// itself (no mask pass) and produces the output log's metadata and radix
+// histograms (no second validation pass: the rows were validated when the
+// parent log was created).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -132,6 +136,16 @@ __global__ void k_attr_cases(RowView v, int64_t n, const uint8_t* any, int keep_
 }
 
 // ------------------------------------------------------------------ stable compaction
+// Two passes over tiles of CMP_TILE rows, no look-back: (1) count the kept
+// rows of every tile (the keep mask, or the events-mode time predicate on the
+// ts column), (2) exclusive scan of the tile counts, (3) scatter: each tile
+// re-reads its rows and writes the kept ones at tile_off[t] + their in-tile
+// rank (warp-striped, so each warp's kept rows land contiguously).  Every
+// pass is embarrassingly parallel.  A single-pass decoupled-look-back
+// compaction was measured latency-bound here (1.5 TB/s: each CTA serialises
+// load -> look-back -> store), and prefetching tiles into a per-CTA ring
+// makes the look-back chain convoy (a tile's aggregate waits for the tiles
+// queued before it in its owner's ring).
 constexpr int CMP_THREADS = 256, CMP_IPT = 8, CMP_TILE = CMP_THREADS * CMP_IPT, CMP_MAXCOL = 12;
 
 struct ColSet {
@@ -141,58 +155,268 @@ struct ColSet {
     int ncol;
 };
 
-__global__ __launch_bounds__(CMP_THREADS) void k_compact_rows(const uint8_t* __restrict__ keep,
-                                                              int64_t n, ColSet cols,
-                                                              uint32_t* status, uint32_t* counter,
-                                                              uint64_t* n_out) {
-    __shared__ uint32_t s_tile, s_wt[CMP_THREADS / 32], s_scan[CMP_THREADS / 32 + 1], s_prefix;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t wbase = (int64_t)tile * CMP_TILE + warp * (32 * CMP_IPT);
-    uint32_t ball[CMP_IPT], wc = 0;
+// keep predicate of row i: mask[i] != 0, or (TIME) t1 <= ts[i] <= t2
+template <bool TIME>
+__device__ __forceinline__ bool keep_row(const uint8_t* mask, const int64_t* ts, int64_t i, int64_t t1, int64_t t2) {
+    if (TIME) {
+        const int64_t t = ts[i];
+        return t >= t1 && t <= t2;
+    }
+    return mask[i] != 0;
+}
+
+template <bool TIME>
+__global__ __launch_bounds__(CMP_THREADS) void k_count_tiles(const uint8_t* __restrict__ mask,
+                                                             const int64_t* __restrict__ ts, int64_t n,
+                                                             int64_t t1, int64_t t2, uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t s_w[CMP_THREADS / 32];
+    const int64_t base = (int64_t)blockIdx.x * CMP_TILE;
+    uint32_t c = 0;
 #pragma unroll
     for (int j = 0; j < CMP_IPT; ++j) {
-        int64_t i = wbase + j * 32 + lane;
-        bool k = i < n && keep[i];
-        ball[j] = __ballot_sync(0xffffffffu, k);
+        const int64_t i = base + j * CMP_THREADS + threadIdx.x;
+        c += (i < n && keep_row<TIME>(mask, ts, i, t1, t2)) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < CMP_THREADS / 32; ++w) t += s_w[w];
+        cnt[blockIdx.x] = t;
+    }
+}
+
+// In-tile ranks: ballots of the warp-striped rows and the warp's exclusive
+// offset within the tile.  Rows: warp w, item j, lane l -> w*256 + j*32 + l.
+template <bool TIME>
+__device__ __forceinline__ uint32_t tile_ballots(const uint8_t* mask, const int64_t* ts, int64_t n, int64_t wbase,
+                                                 int64_t t1, int64_t t2, uint32_t (&ball)[CMP_IPT],
+                                                 uint32_t* s_wt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t wc = 0;
+#pragma unroll
+    for (int j = 0; j < CMP_IPT; ++j) {
+        const int64_t i = wbase + j * 32 + lane;
+        ball[j] = __ballot_sync(0xffffffffu, i < n && keep_row<TIME>(mask, ts, i, t1, t2));
         wc += __popc(ball[j]);
     }
     if (lane == 0) s_wt[warp] = wc;
     __syncthreads();
-    uint32_t total;
-    uint32_t wex = block_excl_scan<CMP_THREADS>(tid < CMP_THREADS / 32 ? s_wt[tid] : 0u, s_scan, &total);
-    if (tid < CMP_THREADS / 32) s_wt[tid] = wex;
-    if (warp == 0) {
-        uint32_t pf = lookback_warp(status, tile, total);
-        if (lane == 0) s_prefix = pf;
+    uint32_t wex = 0;
+#pragma unroll
+    for (int w = 0; w < CMP_THREADS / 32; ++w) wex += w < warp ? s_wt[w] : 0u;
+    return wex;
+}
+
+// generic columns (formatted logs, extra columns): per column all loads of the
+// thread's rows first, then the stores
+__global__ __launch_bounds__(CMP_THREADS) void k_compact_rows(const uint8_t* __restrict__ keep, int64_t n,
+                                                              ColSet cols, const uint64_t* __restrict__ tile_off) {
+    __shared__ uint32_t s_wt[CMP_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wbase = (int64_t)blockIdx.x * CMP_TILE + warp * (32 * CMP_IPT);
+    uint32_t ball[CMP_IPT];
+    const uint32_t wex = tile_ballots<false>(keep, nullptr, n, wbase, 0, 0, ball, s_wt);
+    const uint32_t lt = lanemask_lt();
+    uint64_t o[CMP_IPT];
+    {
+        uint64_t r = tile_off[blockIdx.x] + wex;
+#pragma unroll
+        for (int j = 0; j < CMP_IPT; ++j) {
+            o[j] = r + __popc(ball[j] & lt);
+            r += __popc(ball[j]);
+        }
+    }
+    for (int c = 0; c < cols.ncol; ++c) {
+        const int el = cols.elem[c];
+        const void* in = cols.in[c];
+        void* out = cols.out[c];
+        uint64_t v[CMP_IPT];
+#pragma unroll
+        for (int j = 0; j < CMP_IPT; ++j) {
+            const int64_t i = wbase + j * 32 + lane;
+            v[j] = 0;
+            if (ball[j] & (1u << lane)) {
+                v[j] = el == 1 ? ((const uint8_t*)in)[i]
+                     : el == 2 ? ((const uint16_t*)in)[i]
+                     : el == 4 ? ((const uint32_t*)in)[i] : ((const uint64_t*)in)[i];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < CMP_IPT; ++j) {
+            if (!(ball[j] & (1u << lane))) continue;
+            if (el == 1) ((uint8_t*)out)[o[j]] = (uint8_t)v[j];
+            else if (el == 2) ((uint16_t*)out)[o[j]] = (uint16_t)v[j];
+            else if (el == 4) ((uint32_t*)out)[o[j]] = (uint32_t)v[j];
+            else ((uint64_t*)out)[o[j]] = v[j];
+        }
+    }
+}
+
+struct FilterMeta {
+    long long ts_min, ts_max;
+    unsigned int case_min, case_max;
+};
+
+// Ingested log: scatter of (case, act, ts) plus the output log's metadata (ts /
+// case ranges) and case-digit histograms of the kept rows, in the layout
+// validate_and_meta uses (hist_layout) -- no second validation pass: the rows
+// were validated when the parent log was created.  omask (optional) receives
+// the keep mask for the extra columns' compaction.
+//
+// Persistent and warp-specialised: a producer warp streams the CTA's tiles
+// (t = blockIdx.x + k gridDim.x) into a ring of FS_STAGES shared-memory stages
+// with TMA bulk copies while 8 consumer warps rank and store the previous
+// ones; output offsets come from the count pass (tile_off), so tiles are
+// independent.  Without the ring each CTA serialises load -> rank -> store
+// and the scatter is load-latency bound (~2 TB/s measured).
+constexpr int FS_CONSUMERS = CMP_THREADS, FS_BLOCK = FS_CONSUMERS + 32, FS_STAGES = 3;
+
+template <class P>
+struct alignas(128) FsStage {
+    int64_t ts[CMP_TILE];
+    uint32_t cs[CMP_TILE];
+    P act[CMP_TILE];
+};
+
+template <class P, bool TIME>
+__global__ __launch_bounds__(FS_BLOCK) void k_filter_cols(
+    const uint8_t* __restrict__ mask, const uint32_t* __restrict__ cs, const P* __restrict__ act,
+    const int64_t* __restrict__ ts, int64_t n, int64_t t1, int64_t t2, const uint64_t* __restrict__ tile_off,
+    uint32_t* __restrict__ ocs, P* __restrict__ oact, int64_t* __restrict__ ots, uint8_t* __restrict__ omask,
+    FilterMeta* m, uint32_t case_lo, int hpasses, int hbits, uint32_t* __restrict__ hist, int tma_ok) {
+    extern __shared__ __align__(128) unsigned char fs_sm[];
+    FsStage<P>* stage = (FsStage<P>*)fs_sm;
+    __shared__ __align__(8) uint64_t s_full[FS_STAGES], s_empty[FS_STAGES];
+    __shared__ uint32_t sh[4][256];
+    __shared__ uint32_t s_wt[2][FS_CONSUMERS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 4 * 256; i += FS_BLOCK) (&sh[0][0])[i] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < FS_STAGES; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], FS_CONSUMERS);
+        }
     }
     __syncthreads();
-    const uint32_t lt = lanemask_lt();
-    uint64_t r = (uint64_t)s_prefix + s_wt[warp];
-#pragma unroll
-    for (int j = 0; j < CMP_IPT; ++j) {
-        if (ball[j] & (1u << lane)) {
-            int64_t i = wbase + j * 32 + lane;
-            uint64_t o = r + __popc(ball[j] & lt);
-            for (int c = 0; c < cols.ncol; ++c) {
-                switch (cols.elem[c]) {
-                    case 1: ((uint8_t*)cols.out[c])[o] = ((const uint8_t*)cols.in[c])[i]; break;
-                    case 2: ((uint16_t*)cols.out[c])[o] = ((const uint16_t*)cols.in[c])[i]; break;
-                    case 4: ((uint32_t*)cols.out[c])[o] = ((const uint32_t*)cols.in[c])[i]; break;
-                    default: ((uint64_t*)cols.out[c])[o] = ((const uint64_t*)cols.in[c])[i]; break;
+    const int64_t tiles = (n + CMP_TILE - 1) / CMP_TILE;
+    // a tile is staged by TMA when it is whole and the columns are 16-byte aligned
+    auto staged_tile = [&](int64_t t) { return tma_ok && (t + 1) * CMP_TILE <= n; };
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t i = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+                const int s = i % FS_STAGES;
+                if (i >= FS_STAGES) mbar_wait(&s_empty[s], ((i / FS_STAGES) - 1) & 1);
+                if (staged_tile(t)) {
+                    FsStage<P>& st = stage[s];
+                    const int64_t r0 = t * CMP_TILE;
+                    mbar_expect_tx(&s_full[s], CMP_TILE * (8 + 4 + (uint32_t)sizeof(P)));
+                    tma_load_1d(st.ts, ts + r0, CMP_TILE * 8, &s_full[s]);
+                    tma_load_1d(st.cs, cs + r0, CMP_TILE * 4, &s_full[s]);
+                    tma_load_1d(st.act, act + r0, CMP_TILE * (uint32_t)sizeof(P), &s_full[s]);
+                } else {
+                    mbar_arrive(&s_full[s]);   // tail tile: consumers read global memory
                 }
             }
         }
-        r += __popc(ball[j]);
+    } else {
+        const int ct = tid - 32, cw = ct >> 5;
+        long long tmin = LLONG_MAX, tmax = LLONG_MIN;
+        uint32_t cmin = 0xffffffffu, cmax = 0;
+        const uint32_t hmask = (1u << hbits) - 1;
+        const uint32_t lt = lanemask_lt();
+        uint32_t i = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int s = i % FS_STAGES;
+            mbar_wait(&s_full[s], (i / FS_STAGES) & 1);
+            const FsStage<P>& st = stage[s];
+            const bool staged = staged_tile(t);
+            const int64_t wbase = t * CMP_TILE + cw * (32 * CMP_IPT);
+            uint32_t c[CMP_IPT], ball[CMP_IPT], wc = 0;
+            int64_t tv[CMP_IPT];
+            P a[CMP_IPT];
+#pragma unroll
+            for (int j = 0; j < CMP_IPT; ++j) {
+                const int li = cw * (32 * CMP_IPT) + j * 32 + lane;
+                const int64_t row = wbase + j * 32 + lane;
+                const bool in = row < n;
+                if (staged) {
+                    c[j] = st.cs[li];
+                    tv[j] = st.ts[li];
+                    a[j] = st.act[li];
+                } else {
+                    c[j] = in ? cs[row] : 0u;
+                    tv[j] = in ? ts[row] : 0;
+                    a[j] = in ? act[row] : (P)0;
+                }
+            }
+            mbar_arrive(&s_empty[s]);   // the stage is in registers now
+#pragma unroll
+            for (int j = 0; j < CMP_IPT; ++j) {
+                const int64_t row = wbase + j * 32 + lane;
+                const bool in = row < n;
+                const bool k = in && (TIME ? (tv[j] >= t1 && tv[j] <= t2) : mask[row] != 0);
+                if (omask && in) omask[row] = k ? 1 : 0;
+                ball[j] = __ballot_sync(0xffffffffu, k);
+                wc += __popc(ball[j]);
+            }
+            if (lane == 0) s_wt[i & 1][cw] = wc;
+            asm volatile("bar.sync 1, %0;" ::"n"(FS_CONSUMERS) : "memory");
+            uint32_t wex = 0;
+#pragma unroll
+            for (int w = 0; w < FS_CONSUMERS / 32; ++w) wex += w < cw ? s_wt[i & 1][w] : 0u;
+            uint64_t r = tile_off[t] + wex;
+#pragma unroll
+            for (int j = 0; j < CMP_IPT; ++j) {
+                if (ball[j] & (1u << lane)) {
+                    const uint64_t o = r + __popc(ball[j] & lt);
+                    ocs[o] = c[j];
+                    oact[o] = a[j];
+                    ots[o] = tv[j];
+                    tmin = min(tmin, (long long)tv[j]);
+                    tmax = max(tmax, (long long)tv[j]);
+                    cmin = min(cmin, c[j]);
+                    cmax = max(cmax, c[j]);
+                    const uint32_t f = c[j] - case_lo;
+                    for (int p = 0; p < hpasses; ++p) atomicAdd(&sh[p][(f >> (p * hbits)) & hmask], 1u);
+                }
+                r += __popc(ball[j]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            tmin = min(tmin, __shfl_xor_sync(~0u, tmin, o));
+            tmax = max(tmax, __shfl_xor_sync(~0u, tmax, o));
+            cmin = min(cmin, __shfl_xor_sync(~0u, cmin, o));
+            cmax = max(cmax, __shfl_xor_sync(~0u, cmax, o));
+        }
+        if (lane == 0 && tmin <= tmax) {
+            atomicMin(&m->ts_min, tmin);
+            atomicMax(&m->ts_max, tmax);
+            atomicMin(&m->case_min, cmin);
+            atomicMax(&m->case_max, cmax);
+        }
     }
-    if (tid == 0 && (int64_t)(tile + 1) * CMP_TILE >= n) *n_out = (uint64_t)s_prefix + total;
+    __syncthreads();
+    for (int i = tid; i < hpasses * 256; i += FS_BLOCK) {
+        const uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
 }
 
-// Build the output log from the keep mask.
+// Time predicate for the fused path (events mode on an ingested log).
+struct TimePred {
+    int64_t t1, t2;
+};
+
+// Build the output log from the keep mask (or, with tp, from the events-mode
+// time predicate on an ingested log's ts column).
 static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStream_t s,
-                               pm4g_log** out) {
+                               pm4g_log** out, const TimePred* tp = nullptr) {
     const int64_t n = in->n;
     pm4g_log* L = new pm4g_log();
     L->A = in->A;
@@ -215,7 +439,8 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         cs.elem[cs.ncol] = e;
         cs.ncol++;
     };
-    if (in->sorted) {
+    const bool fused = !in->sorted;
+    if (!fused) {
         if ((st = dalloc((void**)&L->key, (N + 32) * 8, s))) return bail(st);
         if ((st = dalloc(&L->s_act, (N + 32) * in->act_bytes, s))) return bail(st);
         add(in->key, L->key, 8);
@@ -229,9 +454,6 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         if ((st = dalloc((void**)&L->case_, N * 4, s))) return bail(st);
         if ((st = dalloc(&L->act, N * in->act_bytes, s))) return bail(st);
         if ((st = dalloc((void**)&L->ts, N * 8, s))) return bail(st);
-        add(in->case_, L->case_, 4);
-        add(in->act, L->act, in->act_bytes);
-        add(in->ts, L->ts, 8);
     }
     for (auto& x : in->extra) {
         ExtraCol y = x;
@@ -246,29 +468,85 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         if (x.valid) add(x.valid, y.valid, 1);
     }
     uint64_t kept = 0;
+    FilterMeta fm{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u};
+    int hpasses = 0, hbits = 0;
+    Scratch wk(s), om(s);
+    if (fused) {
+        hist_layout(L, &hpasses, &hbits);
+        if ((st = dalloc_t(&L->hist, 4 * 256, s))) return bail(st);
+        if (cudaMemsetAsync(L->hist, 0, 4 * 256 * 4, s) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "memset"));
+    }
     if (n > 0) {
         const int64_t tiles = (n + CMP_TILE - 1) / CMP_TILE;
-        Scratch stt(s);
-        if ((st = stt.alloc((tiles + 1) * 4 + 16))) return bail(st);
-        uint32_t* status = stt.as<uint32_t>();
-        uint64_t* d_kept = (uint64_t*)(((uintptr_t)(status + tiles + 1) + 7) & ~(uintptr_t)7);
-        if (cudaMemsetAsync(stt.p, 0, (tiles + 1) * 4, s) != cudaSuccess)
-            return bail(cuda_fail(cudaGetLastError(), "memset"));
+        // [tile counts u32: tiles] [tile offsets u64: tiles + 1] [meta]
+        const size_t cnt_bytes = ((size_t)tiles * 4 + 15) & ~(size_t)15;
+        if ((st = wk.alloc(cnt_bytes + (tiles + 1) * 8 + sizeof(FilterMeta) + 16))) return bail(st);
+        uint32_t* tcnt = wk.as<uint32_t>();
+        uint64_t* toff = (uint64_t*)((char*)wk.p + cnt_bytes);
+        FilterMeta* d_meta = (FilterMeta*)(toff + tiles + 1);
+        const int64_t t1 = tp ? tp->t1 : 0, t2 = tp ? tp->t2 : 0;
+        if (tp)
+            PM4G_LAUNCH("k_count_tiles", n * 8.0, s,
+                        (k_count_tiles<true><<<(unsigned)tiles, CMP_THREADS, 0, s>>>(nullptr, in->ts, n, t1, t2, tcnt)));
+        else
+            PM4G_LAUNCH("k_count_tiles", n * 1.0, s,
+                        (k_count_tiles<false><<<(unsigned)tiles, CMP_THREADS, 0, s>>>(keep, nullptr, n, 0, 0, tcnt)));
+        if ((st = excl_scan_u32_to_u64(tcnt, toff, tiles, s))) return bail(st);
+        if (fused) {
+            uint8_t* omask = nullptr;
+            if (!in->extra.empty()) {
+                if ((st = om.alloc(N))) return bail(st);
+                omask = om.as<uint8_t>();
+            }
+            if (cudaMemcpyAsync(d_meta, &fm, sizeof(fm), cudaMemcpyHostToDevice, s) != cudaSuccess)
+                return bail(cuda_fail(cudaGetLastError(), "filter setup"));
+            const int tma_ok = (((uintptr_t)in->case_ | (uintptr_t)in->act | (uintptr_t)in->ts) & 15) == 0;
+            // reads (+ mask in / out); the kept rows' writes are added below
+            const double rb = n * (12.0 + in->act_bytes + (tp ? 0 : 1) + (omask ? 1 : 0));
+#define PM4G_FILTER_COLS(P)                                                                                     \
+    {                                                                                                           \
+        const size_t smem = FS_STAGES * sizeof(FsStage<P>);                                                     \
+        static bool attr = false;                                                                               \
+        if (!attr) {                                                                                            \
+            PM4G_CK(cudaFuncSetAttribute(k_filter_cols<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            PM4G_CK(cudaFuncSetAttribute(k_filter_cols<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            attr = true;                                                                                        \
+        }                                                                                                       \
+        const int per_sm = std::max(1, std::min(3, (int)((220 * 1024) / (smem + 6 * 1024))));                  \
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * per_sm)); \
+        if (tp)                                                                                                 \
+            PM4G_LAUNCH("k_filter_cols", rb, s,                                                                 \
+                        (k_filter_cols<P, true><<<grid, FS_BLOCK, smem, s>>>(                                   \
+                            keep, in->case_, (const P*)in->act, in->ts, n, t1, t2, toff, L->case_, (P*)L->act,  \
+                            L->ts, omask, d_meta, L->case_lo, hpasses, hbits, L->hist, tma_ok)));               \
+        else                                                                                                    \
+            PM4G_LAUNCH("k_filter_cols", rb, s,                                                                 \
+                        (k_filter_cols<P, false><<<grid, FS_BLOCK, smem, s>>>(                                  \
+                            keep, in->case_, (const P*)in->act, in->ts, n, t1, t2, toff, L->case_, (P*)L->act,  \
+                            L->ts, omask, d_meta, L->case_lo, hpasses, hbits, L->hist, tma_ok)));               \
+    }
+            switch (in->act_bytes) {
+                case 1: PM4G_FILTER_COLS(uint8_t); break;
+                case 2: PM4G_FILTER_COLS(uint16_t); break;
+                default: PM4G_FILTER_COLS(uint32_t); break;
+            }
+#undef PM4G_FILTER_COLS
+            keep = omask;   // the extra columns follow the same mask
+        }
         double row_bytes = 0;
         for (int c = 0; c < cs.ncol; ++c) row_bytes += cs.elem[c];
-        cudaError_t e;
-        prof_begin("k_compact_rows", n * (1.0 + row_bytes), s);
-        k_compact_rows<<<(unsigned)tiles, CMP_THREADS, 0, s>>>(keep, n, cs, status + 1, status, d_kept);
-        e = cudaGetLastError();
-        prof_end(s);
-        count_launch();
-        if (e != cudaSuccess) return bail(cuda_fail(e, "k_compact_rows"));
-        if (cudaMemcpyAsync(&kept, d_kept, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        if (cs.ncol > 0)
+            PM4G_LAUNCH("k_compact_rows", n * (1.0 + row_bytes), s,
+                        (k_compact_rows<<<(unsigned)tiles, CMP_THREADS, 0, s>>>(keep, n, cs, toff)));
+        if (cudaMemcpyAsync(&kept, toff + tiles, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            (fused && cudaMemcpyAsync(&fm, d_meta, sizeof(fm), cudaMemcpyDeviceToHost, s) != cudaSuccess) ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return bail(cuda_fail(cudaGetLastError(), "filter count"));
+        if (fused) prof_add_bytes("k_filter_cols", (double)kept * (12.0 + in->act_bytes));
+        if (cs.ncol > 0) prof_add_bytes("k_compact_rows", (double)kept * row_bytes);
     }
     L->n = (int64_t)kept;
-    if (in->sorted) {
+    if (!fused) {
         L->sorted = true;
         L->ts_min = in->ts_min;
         L->ts_max = in->ts_max;
@@ -280,7 +558,7 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         L->passes = in->passes;
         if ((st = segments(L, s))) return bail(st);
     } else {
-        if ((st = validate_and_meta(L, s))) return bail(st);
+        apply_meta(L, fm.ts_min, fm.ts_max, fm.case_min, fm.case_max, hpasses, hbits);
     }
     *out = L;
     return PM4G_OK;
@@ -301,8 +579,12 @@ pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = in->n;
     Scratch mask(s), span(s);
-    PM4G_TRY(mask.alloc(std::max<int64_t>(n, 1)));
     RowView v = view_of(in);
+    if (mode == PM4G_TIME_EVENTS && !in->sorted) {
+        const TimePred tp{t1, t2};
+        return compact_log(in, nullptr, s, out, &tp);
+    }
+    PM4G_TRY(mask.alloc(std::max<int64_t>(n, 1)));
     if (n > 0) {
         if (mode == PM4G_TIME_EVENTS) {
             PM4G_LAUNCH("k_time_events", n * 9.0, s, k_time_events<<<gsz(n), 256, 0, s>>>(v, n, t1, t2, mask.as<uint8_t>()));

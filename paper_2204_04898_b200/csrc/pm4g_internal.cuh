@@ -34,6 +34,7 @@ pm4g_status cuda_fail(cudaError_t e, const char* what);
 // profiling is on, brackets it with CUDA events on the launching stream.
 void prof_begin(const char* name, double bytes, cudaStream_t s);
 void prof_end(cudaStream_t s);
+void prof_add_bytes(const char* name, double bytes);
 void count_launch();
 
 #define PM4G_LAUNCH(name, bytes, stream, ...)                                  \
@@ -181,6 +182,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
             : "memory");
     } while (!done);
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // bytes and both addresses must be multiples of 16
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
                                             uint64_t* bar) {
@@ -194,34 +198,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
 // Decoupled look-back (single value per tile), status word = flag(2) | value(30).
 constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
 
-// Called by ONE thread per tile: publishes the tile's aggregate, walks back to
-// an inclusive prefix, publishes its own inclusive value and returns the
-// exclusive prefix.
-__device__ __forceinline__ uint32_t lookback_single(uint32_t* status, uint32_t tile,
-                                                    uint32_t aggregate) {
-    if (tile == 0) {
-        st_volatile(&status[0], ST_INC | aggregate);
-        return 0;
-    }
-    st_volatile(&status[tile], ST_AGG | aggregate);
-    uint32_t prefix = 0;
-    int64_t p = (int64_t)tile - 1;
-    while (true) {
-        uint32_t v;
-        do { v = ld_volatile(&status[p]); } while ((v >> 30) == 0);
-        prefix += v & ST_VAL;
-        if ((v >> 30) == 2) break;
-        --p;
-    }
-    st_volatile(&status[tile], ST_INC | (prefix + aggregate));
-    return prefix;
-}
-
-// Warp-cooperative decoupled look-back: called by ALL 32 lanes of one warp;
-// reads 32 predecessors per round, so the walk costs one L2 round trip per 32
-// tiles instead of one per tile.  Returns the exclusive prefix (all lanes).
-__device__ __forceinline__ uint32_t lookback_warp(uint32_t* status, uint32_t tile,
-                                                  uint32_t aggregate) {
+// Decoupled look-back (one value per tile, status word = flag(2) | value(30)),
+// warp-cooperative, reading K predecessors per lane (32 K per L2 round trip:
+// with T tiles in flight the newest tile's walk spans ~T predecessors, so the
+// window width bounds a single-pass kernel's steady state).  Called by all 32
+// lanes of one warp; publishes the tile's aggregate, walks back to the nearest
+// inclusive prefix, publishes its own.  Lane l covers predecessors
+// end - (l K + j), j = 0..K-1, nearest first.  Returns the exclusive prefix.
+template <int K>
+__device__ __forceinline__ uint32_t lookback_warp_k(uint32_t* status, uint32_t tile, uint32_t aggregate) {
     const int lane = threadIdx.x & 31;
     if (tile == 0) {
         if (lane == 0) st_volatile(&status[0], ST_INC | aggregate);
@@ -231,46 +216,34 @@ __device__ __forceinline__ uint32_t lookback_warp(uint32_t* status, uint32_t til
     uint32_t prefix = 0;
     int64_t end = (int64_t)tile - 1;
     while (true) {
-        const int64_t idx = end - lane;
-        uint32_t v = idx >= 0 ? ld_volatile(&status[idx]) : ST_INC;
-        while (__any_sync(0xffffffffu, (v >> 30) == 0)) {
-            if ((v >> 30) == 0) v = ld_volatile(&status[idx]);
-        }
-        const uint32_t inc = __ballot_sync(0xffffffffu, (v >> 30) == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive predecessor
-        uint32_t x = lane <= stop ? (v & ST_VAL) : 0u;
+        uint32_t v[K];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        prefix += x;
-        if (inc) break;
-        end -= 32;
-    }
-    if (lane == 0) st_volatile(&status[tile], ST_INC | (prefix + aggregate));
-    return prefix;
-}
-
-// Same walk for a tile that already published its aggregate (flag AGG, or INC
-// for tile 0): resolves the exclusive prefix and publishes INC.  All 32 lanes.
-__device__ __forceinline__ uint32_t lookback_warp_inc(uint32_t* status, uint32_t tile,
-                                                      uint32_t aggregate) {
-    const int lane = threadIdx.x & 31;
-    if (tile == 0) return 0;
-    uint32_t prefix = 0;
-    int64_t end = (int64_t)tile - 1;
-    while (true) {
-        const int64_t idx = end - lane;
-        uint32_t v = idx >= 0 ? ld_volatile(&status[idx]) : ST_INC;
-        while (__any_sync(0xffffffffu, (v >> 30) == 0)) {
-            if ((v >> 30) == 0) v = ld_volatile(&status[idx]);
+        for (int j = 0; j < K; ++j) {
+            const int64_t idx = end - (lane * K + j);
+            v[j] = idx >= 0 ? ld_volatile(&status[idx]) : ST_INC;
         }
-        const uint32_t inc = __ballot_sync(0xffffffffu, (v >> 30) == 2);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int64_t idx = end - (lane * K + j);
+            while ((v[j] >> 30) == 0) v[j] = ld_volatile(&status[idx]);
+        }
+        int fj = K;   // this lane's nearest inclusive entry
+#pragma unroll
+        for (int j = K - 1; j >= 0; --j)
+            if ((v[j] >> 30) == 2) fj = j;
+        const uint32_t inc = __ballot_sync(0xffffffffu, fj < K);
         const int stop = inc ? __ffs(inc) - 1 : 31;
-        uint32_t x = lane <= stop ? (v & ST_VAL) : 0u;
+        uint32_t x = 0;
+        if (lane <= stop) {
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (lane < stop || j <= fj) x += v[j] & ST_VAL;
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         prefix += x;
         if (inc) break;
-        end -= 32;
+        end -= 32 * K;
     }
     if (lane == 0) st_volatile(&status[tile], ST_INC | (prefix + aggregate));
     return prefix;
@@ -309,6 +282,9 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp
 // ------------------------------------------------------------------ entry points
 // (implemented across the .cu files)
 pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s);   // K1
+void hist_layout(const pm4g_log* L, int* hpasses, int* hbits);
+void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, uint32_t case_max,
+                int hpasses, int hbits);
 pm4g_status sort_log(pm4g_log* L, cudaStream_t s);            // A2-A4
 pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4
 pm4g_status fetch_n_cases(const pm4g_log* L, cudaStream_t s);

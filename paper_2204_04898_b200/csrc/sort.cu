@@ -522,7 +522,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     // ---- 3. warp 0 resolves the case ranks (decoupled look-back) while warps
     // 1..7 sort the tile; the workers synchronise on named barrier 1
     if (warp == 0) {
-        const uint32_t pf = lookback_warp(a.status, tile, H);
+        const uint32_t pf = lookback_warp_k<8>(a.status, tile, H);
         if (lane == 0) s_prefix = pf;
     } else if (H > 0) {
         constexpr int NW = FMT_THREADS - 32;
@@ -770,7 +770,7 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
     uint32_t wex = block_excl_scan<SEG_THREADS>(wt, s_scan, &total);
     if (tid < SEG_THREADS / 32) s_warp_tot[tid] = wex;
     if (warp == 0) {
-        uint32_t pf = lookback_warp(status, tile, total);
+        uint32_t pf = lookback_warp_k<8>(status, tile, total);
         if (lane == 0) s_prefix = pf;
     }
     __syncthreads();

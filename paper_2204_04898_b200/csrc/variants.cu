@@ -519,7 +519,7 @@ __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __re
     uint32_t total;
     uint32_t ex = block_excl_scan<SCAN_THREADS>(sum, s_scan, &total);
     if (threadIdx.x < 32) {
-        uint32_t pf = lookback_warp(status, tile, total);
+        uint32_t pf = lookback_warp_k<8>(status, tile, total);
         if (threadIdx.x == 0) s_prefix = pf;
     }
     __syncthreads();
