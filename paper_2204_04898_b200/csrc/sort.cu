@@ -576,11 +576,15 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
                 if (p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
                 continue;
             }
+            // #(key_j < key_p) + #(j < p with key_j == key_p) = #(key_j < key_p + [j < p]):
+            // one 64-bit compare per element; the all-ones key (key_bits = 64)
+            // has no successor and takes the two-compare form
             int r = 0;
-            const uint64_t ki = s_key[p];
-            for (int j = s0; j < e0; ++j) {
-                const uint64_t kj = s_key[j];
-                r += (kj < ki) | ((kj == ki) & (j < p));
+            const uint64_t ki = s_key[p], ki1 = ki + 1;
+            if (ki1 != 0) {
+                for (int j = s0; j < e0; ++j) r += s_key[j] < (j < p ? ki1 : ki);
+            } else {
+                for (int j = s0; j < e0; ++j) r += (s_key[j] < ki) | ((s_key[j] == ki) & (j < p));
             }
             s_dst[p] = (uint16_t)(s0 + r);
         }

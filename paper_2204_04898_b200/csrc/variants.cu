@@ -70,12 +70,11 @@ __global__ void k_init_table(Slot* table, uint64_t cap) {
 }
 
 // Find or claim the global slot of key (a, b): linear probing, one 128-bit CAS
-// claims an empty slot.  ctl[0] = overflow flag, ctl[1] = claimed slots; a
-// claim past the load limit (3/4 of the table) raises overflow, so a table
-// that is too small is abandoned after O(limit) claims instead of being probed
-// to saturation.  Returns the slot, or ~0 once overflow is raised.
+// claims an empty slot (*claimed = true).  Returns the slot, or ~0 when the
+// table is full or abandoned (ctl[0] = overflow flag, raised here or by the
+// load-limit check in claim_count).
 __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint64_t a, uint64_t b,
-                                               uint32_t* ctl, uint32_t limit) {
+                                               uint32_t* ctl, bool* claimed) {
     uint64_t h = (a ^ (a >> 29) ^ (b * 0x9E3779B97F4A7C15ull)) & mask;
     for (uint64_t probes = 0; probes <= mask; ++probes) {
         Slot* sp = &table[h];
@@ -85,7 +84,7 @@ __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint6
             K128 exp{0, 0}, des{a, b};
             K128 old = atomicCAS((K128*)sp, exp, des);
             if (old.a == 0 && old.b == 0) {
-                if (atomicAdd(&ctl[1], 1u) >= limit) break;
+                *claimed = true;
                 return h;
             }
             if (old.a == a && old.b == b) return h;
@@ -95,6 +94,19 @@ __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint6
     }
     atomicExch(ctl, 1u);
     return ~0ull;
+}
+
+// Claimed slots, counted once per warp (ctl[1]); past the load limit (3/4 of
+// the table) the table is abandoned (ctl[0] = 1), so an undersized table costs
+// O(limit) claims instead of being probed to saturation.  Called by the active
+// lanes together.
+__device__ __forceinline__ void claim_count(bool claimed, uint32_t* ctl, uint32_t limit) {
+    const uint32_t m = __activemask();
+    const uint32_t b = __ballot_sync(m, claimed);
+    if (b && (threadIdx.x & 31) == __ffs(m) - 1) {
+        const uint32_t c = __popc(b);
+        if (atomicAdd(&ctl[1], c) + c > limit) atomicExch(ctl, 1u);
+    }
 }
 
 // Items: t in [0, n_items) -> item list[t] (or t).  Each CTA first aggregates a
@@ -202,7 +214,9 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
         }
         for (uint32_t q = threadIdx.x; q < nocc; q += INS_THREADS) {
             const int sl = s_list[q];
-            uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], ctl, limit);
+            bool claimed = false;
+            uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], ctl, &claimed);
+            claim_count(claimed, ctl, limit);
             s_g[sl] = g;
             if (g == ~0ull) continue;
             atomicAdd(&table[g].weight, (unsigned long long)s_w[sl]);
@@ -214,7 +228,9 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
             if (!live[u]) continue;
             uint64_t g;
             if (direct[u]) {
-                g = table_slot(table, mask, ka[u], kb[u], ctl, limit);
+                bool claimed = false;
+                g = table_slot(table, mask, ka[u], kb[u], ctl, &claimed);
+                claim_count(claimed, ctl, limit);
                 if (g != ~0ull) {
                     atomicAdd(&table[g].weight, (unsigned long long)w[u]);
                     atomicMin(&table[g].rep, ord[u]);

@@ -109,6 +109,15 @@ def test_extreme_timestamps_wide_span():
     check_log([1] * 6, [0, 1, 0, 1, 0, 1], ts, 2)
 
 
+def test_all_ones_key_ties():
+    """key_bits = 64 with rows on the all-ones key (max case, max ts), tied: the
+    format rank falls back to the two-compare form there (no key + 1)."""
+    big, small = 2**63 - 1, -(2**63)
+    check_log([1] * 7, [0, 1, 2, 1, 0, 2, 1], [big, small, big, 0, big, small, 5], 3)
+    m = 2**62 - 1   # 1 case bit + 63 ts bits; case 3 at ts m is the all-ones key
+    check_log([3, 2, 3, 3, 2, 3], [0, 1, 2, 1, 0, 2], [m, -(2**62), m, 0, m, m], 3)
+
+
 def test_key_too_wide_is_reported():
     """case_bits + ts_bits > 64 -> PM4G_EKEYWIDTH (wide-key path is future work)."""
     c, a, t = to_device_cols([0, 2**31, 5], [0, 0, 0], [-(2**62), 2**62, 0], 1)
