@@ -114,7 +114,7 @@ def make_shard(cfg: str, rank: int, world: int, device):
     return case.contiguous(), act.contiguous(), ts, meta, spec
 
 
-def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None):
+def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None, info=None):
     tick = (lambda nm: trace.append((nm, time.perf_counter()))) if trace is not None else (lambda nm: None)
     tick("start")
     log = pm4g.pm4g_log_create(case, act, ts, meta["A"], n_case_codes=meta["n_case_codes"],
@@ -129,10 +129,42 @@ def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=
     tick("sort (async)")
     res = log.analyze(comm=comm, out=out)
     tick("analyze")
+    if info is not None:
+        i = log.info()
+        info.update(n=int(i.n_events), C=int(i.n_cases))
     v = res["variants"]
     log.close()
     tick("close")
     return res, v
+
+
+def check_invariants(pm4g, case, act, ts, meta, comm, out, filt, dist, dev, keep=None) -> dict:
+    """One extra step outside the timed region, its outputs checked against
+    identities that hold for any log (S:282, S:332, S:359, S:422, S:206 and the
+    telescoping of duration sums): the bench reports whether they held."""
+    info = {}
+    res, v = run_step(pm4g, case, act, ts, meta, comm, out, filt, info=info)
+    n, C = info["n"], info["C"]
+    tab = v.get()
+    M = 1 << 64
+    vals = [n, C, int(res["n_events"][:C].to(torch.int64).sum()), int(res["dur"][:C].sum()) if C else 0]
+    if dist:
+        g = [None] * dist.get_world_size()
+        dist.all_gather_object(g, vals)
+        vals = [sum(x[k] for x in g) for k in range(4)]
+    N, Ct, ne, dsum = vals
+    ok = {
+        "sum_dfg_count_eq_events_minus_cases": int(res["cnt"].sum()) == N - Ct,
+        "sum_start_eq_cases": int(res["start"].sum()) == Ct,
+        "sum_end_eq_cases": int(res["end"].sum()) == Ct,
+        "sum_variant_counts_eq_cases": int(tab["count"].sum()) == Ct,
+        "sum_case_events_eq_events": ne == N,
+        "sum_dfg_durations_eq_sum_case_durations": int(res["dur_sum"].sum()) % M == dsum % M,
+    }
+    if keep is not None:
+        keep.update(n_events=res["n_events"][:C], dur=res["dur"][:C])
+    v.close()
+    return {"all": all(ok.values()), **ok}
 
 
 def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt: bool) -> dict:
@@ -144,20 +176,28 @@ def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt
             "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")}
 
 
-def cpu_baseline(cfg, cases: int, device):
-    """O1 on a bounded sample (the first `cases` cases of the workload), 1 core."""
+def cpu_baseline(cfg, cases: int, device, gpu_cases=None):
+    """O1 on a bounded sample (the first `cases` cases of the workload), 1 core.
+    gpu_cases: (n_events, dur) of the GPU run for the same case codes -- the
+    oracle's per-case results on the sample are compared with them."""
+    import numpy as np
     import oracle
     from gen.synth import CONFIGS, generate
     spec = CONFIGS[cfg]
-    L = generate(spec, 0, min(cases, spec.n_cases), device=device)
+    k = min(cases, spec.n_cases)
+    L = generate(spec, 0, k, device=device)
     c, a, t = L.case.cpu().numpy(), L.act.cpu().numpy(), L.ts.cpu().numpy()
     oracle.build()
     t0 = time.perf_counter()
-    oracle.run(c, a, t, spec.n_activities)
+    r = oracle.run(c, a, t, spec.n_activities)
     dt = time.perf_counter() - t0
-    return {"value": c.size / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {min(cases, spec.n_cases):,} cases ({c.size:,} events) of the {cfg} "
-                      f"workload; single-threaded O1 (stable sort + loop), {dt:.2f} s"}
+    out = {"value": c.size / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
+           "sample": f"first {k:,} cases ({c.size:,} events) of the {cfg} "
+                     f"workload; single-threaded O1 (stable sort + loop), {dt:.2f} s"}
+    if gpu_cases is not None:
+        ne, du = gpu_cases
+        out["per_case_parity_on_sample"] = bool(np.array_equal(ne[:k], r.n_events) and np.array_equal(du[:k], r.dur))
+    return out
 
 
 # ------------------------------------------------------------------ reference arm
@@ -204,7 +244,7 @@ def main():
     ap.add_argument("--impl", default="pm4g", choices=["pm4g", "reference"])
     ap.add_argument("--filter", action="store_true", help="events-mode time filter in the step (1B-style)")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-cases", type=int, default=1_000_000)
+    ap.add_argument("--cpu-cases", type=int, default=4_000_000)
     ap.add_argument("--ref-cases", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stages", action="store_true", help="print the per-kernel table to stderr")
@@ -361,9 +401,15 @@ def main():
                 print(f"  {t0 - t00:9.3f} gap {t0 - prev_end:8.3f}  {d:8.3f}  {nm}", file=sys.stderr)
                 prev_end = t0 + d
 
+    kept = {}
+    verified = check_invariants(pm4g, case, act, ts, meta, comm, out, filt, dist, dev, kept)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, args.cpu_cases, dev)
+        gpu_cases = None
+        if filt is None:
+            k = min(args.cpu_cases, meta["case_hi"] - meta["case_lo"])
+            gpu_cases = (kept["n_events"][:k].cpu().numpy(), kept["dur"][:k].cpu().numpy())
+        cpu = cpu_baseline(args.config, args.cpu_cases, dev, gpu_cases)
 
     if rank == 0:
         line = {
@@ -372,7 +418,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": workload_config(args.config, n_local, meta["case_hi"] - meta["case_lo"], meta["A"], world,
                                       filt is not None),
-            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "verified": verified,
             "cpu_baseline": cpu,
             "hbm_pipeline": {"algorithmic_GB_per_step": step_bytes / args.steps / 1e9,
                              "achieved_GB_per_s": step_bytes / (ms / 1e3) / 1e9,
