@@ -62,6 +62,11 @@ def _load():
         L.orc_filter_attr.argtypes = [I64, P, I32, P, P, P, I64, I64, I64,
                                       ctypes.c_double, ctypes.c_double, I32, I32, P]
         L.orc_filter_attr.restype = I32
+        L.orc_get_dfg_minmax.argtypes = [P, P, P]
+        L.orc_filter_cases.argtypes = [I64, P, P, P, I32, P, I64, I64, I64, I32, P]
+        L.orc_filter_cases.restype = I32
+        L.orc_filter_variants.argtypes = [I64, P, P, P, P, P, I64, I32, P]
+        L.orc_filter_variants.restype = I32
         _lib = L
     return _lib
 
@@ -187,4 +192,55 @@ def filter_attr(case, col, *, codes=None, lo=None, hi=None, valid=None, level: i
                            1 if keep else 0, _ptr(out))
     if st != 0:
         raise ValueError("EINVAL (S:449, S:458)")
+    return out.astype(bool)
+
+
+def dfg_minmax(case, act, ts, n_activities: int):
+    """NEXT-2: per-edge min / max pair duration (u64, R20),
+    0 where the edge never occurs.  Returns (min[A, A], max[A, A])."""
+    L = _load()
+    c, a, t = _u32(case), _u32(act), _i64(ts)
+    A = int(n_activities)
+    h = L.orc_run(c.size, _ptr(c), _ptr(a), _ptr(t), A)
+    try:
+        mn = np.zeros(A * A, np.uint64)
+        mx = np.zeros(A * A, np.uint64)
+        L.orc_get_dfg_minmax(h, _ptr(mn), _ptr(mx))
+    finally:
+        L.orc_free(h)
+    return mn.reshape(A, A), mx.reshape(A, A)
+
+
+CASE_START_IN, CASE_END_IN, CASE_SIZE, CASE_THROUGHPUT, CASE_PATHS = 0, 1, 2, 3, 4
+
+
+def filter_cases(case, act, ts, kind: int, *, codes=None, lo: int = 0, hi: int = 0,
+                 keep: bool = True) -> np.ndarray:
+    """NEXT-1 whole-case filters: keep mask (bool, input
+    order).  ``codes``: activity codes (START_IN / END_IN) or flattened pairs
+    a0, b0, a1, b1, ... (PATHS).  Raises on lo > hi or an odd pair list."""
+    L = _load()
+    c, a, t = _u32(case), _u32(act), _i64(ts)
+    cs = _u32([] if codes is None else codes)
+    out = np.zeros(c.size, np.uint8)
+    st = L.orc_filter_cases(c.size, _ptr(c), _ptr(a), _ptr(t), int(kind), _ptr(cs), cs.size,
+                            int(lo), int(hi), 1 if keep else 0, _ptr(out))
+    if st != 0:
+        raise ValueError("EINVAL (S:459)")
+    return out.astype(bool)
+
+
+def filter_variants(case, act, ts, seqs, keep: bool = True) -> np.ndarray:
+    """filter_by_variants (P:102-103; S:372-380): keep mask (bool, input order);
+    ``seqs``: iterable of activity-code sequences."""
+    L = _load()
+    c, a, t = _u32(case), _u32(act), _i64(ts)
+    seqs = [list(x) for x in seqs]
+    off = np.zeros(len(seqs) + 1, np.uint64)
+    for i, q in enumerate(seqs):
+        off[i + 1] = off[i] + len(q)
+    flat = _u32([x for q in seqs for x in q])
+    out = np.zeros(c.size, np.uint8)
+    L.orc_filter_variants(c.size, _ptr(c), _ptr(a), _ptr(t), _ptr(off), _ptr(flat), len(seqs),
+                          1 if keep else 0, _ptr(out))
     return out.astype(bool)

@@ -24,6 +24,7 @@ def analyse(case, act, ts, A: int) -> dict:
     tr = traces(case, act, ts)
     cnt = defaultdict(int)
     dsum = defaultdict(int)
+    dmin, dmax = {}, {}
     start = defaultdict(int)
     end = defaultdict(int)
     cases = []
@@ -35,13 +36,16 @@ def analyse(case, act, ts, A: int) -> dict:
         for (t0, _, a0), (t1, _, a1) in zip(evs, evs[1:]):
             cnt[(a0, a1)] += 1
             dsum[(a0, a1)] += t1 - t0
+            dmin[(a0, a1)] = min(dmin.get((a0, a1), t1 - t0), t1 - t0)
+            dmax[(a0, a1)] = max(dmax.get((a0, a1), t1 - t0), t1 - t0)
         start[seq[0]] += 1
         end[seq[-1]] += 1
         cases.append((c, len(evs), evs[-1][0] - evs[0][0]))
         variants[seq] += 1
         rep.setdefault(seq, c)
     mean = {k: dsum[k] / cnt[k] for k in cnt}
-    return {"cnt": dict(cnt), "sum": dict(dsum), "mean": mean, "start": dict(start),
+    return {"cnt": dict(cnt), "sum": dict(dsum), "mean": mean, "min": dmin, "max": dmax,
+            "start": dict(start),
             "end": dict(end), "cases": cases, "variants": dict(variants), "rep": rep,
             "sorted": [(c, t, i, a) for c in sorted(tr) for (t, i, a) in tr[c]]}
 
@@ -71,3 +75,35 @@ def filter_codes(case, col, codes, level, keep=True):
     for c, x in zip(case, m):
         anym[int(c)] |= x
     return [i for i, c in enumerate(case) if anym[int(c)] == keep]
+
+
+def filter_cases(case, act, ts, kind, codes=(), lo=0, hi=0, keep=True):
+    """S:428-435, S:454-471 by enumeration over traces; kept row indices.
+    kind 0 start in codes, 1 end in codes, 2 size in [lo, hi], 3 throughput in
+    [lo, hi], 4 some directly-follows pair in the pairs (codes[0::2], codes[1::2])."""
+    tr = traces(case, act, ts)
+    codes = [int(x) for x in codes]
+    pairs = set(zip(codes[0::2], codes[1::2]))
+    ok = {}
+    for c, evs in tr.items():
+        seq = [a for _, _, a in evs]
+        if kind == 0:
+            m = seq[0] in codes
+        elif kind == 1:
+            m = seq[-1] in codes
+        elif kind == 2:
+            m = lo <= len(seq) <= hi
+        elif kind == 3:
+            m = lo <= evs[-1][0] - evs[0][0] <= hi
+        else:
+            m = any((x, y) in pairs for x, y in zip(seq, seq[1:]))
+        ok[c] = m == keep
+    return [i for i, c in enumerate(case) if ok[int(c)]]
+
+
+def filter_variants(case, act, ts, seqs, keep=True):
+    """S:372-380 by enumeration: cases whose exact sequence is in seqs."""
+    tr = traces(case, act, ts)
+    want = set(tuple(int(x) for x in q) for q in seqs)
+    ok = {c: (tuple(a for _, _, a in evs) in want) == keep for c, evs in tr.items()}
+    return [i for i, c in enumerate(case) if ok[int(c)]]

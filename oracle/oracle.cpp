@@ -25,7 +25,10 @@
 //           sequence ("double aggregation"), keyed here by
 //           the sequence itself in a std::map (no hashing at all).
 // Filters (P:126 timestamp.py, P:128 attributes.py) are plain
-// per-row / per-case predicates evaluated on the definition.
+// per-row / per-case predicates evaluated on the definition; the NEXT rows of
+// SURVEY.md 8(f) add whole-case filters (start / end activity, case size,
+// throughput, paths, variants: P:98-103) and
+// the per-edge min / max pair duration.
 //
 // Readings where the paper is silent are the ones listed in DESIGN.md
 // "Readings" (R1..R19, = SURVEY.md §8(c) table); each is cited at its use.
@@ -64,6 +67,10 @@ struct orc_result {
     std::vector<int64_t> sum;       // modulo 2^64 (R8)
     std::vector<__int128> sum_wide; // shadow, to detect wrap-around
     std::vector<double> mean;
+    // performance DFG min / max of the pair durations (NEXT-2, S:281, S:306,
+    // S:339): over the u64 difference ts_{i+1} - ts_i, which is exact because
+    // 0 <= ts_{i+1} - ts_i < 2^64 after the sort (R20); 0 where cnt == 0
+    std::vector<uint64_t> dmin, dmax;
     // cases dataframe (step 3)
     std::vector<uint64_t> start, end;
     std::vector<uint32_t> case_code, n_events;
@@ -121,6 +128,8 @@ orc_result* orc_run(int64_t n, const uint32_t* case_, const uint32_t* act,
     r->cnt.assign(AA, 0);
     r->sum.assign(AA, 0);
     r->sum_wide.assign(AA, 0);
+    r->dmin.assign(AA, 0);
+    r->dmax.assign(AA, 0);
     r->start.assign(A, 0);
     r->end.assign(A, 0);
 
@@ -156,6 +165,9 @@ orc_result* orc_run(int64_t n, const uint32_t* case_, const uint32_t* act,
             r->cnt[e] += 1;                                              // R5: occurrences
             r->sum[e] = (int64_t)((uint64_t)r->sum[e] + (uint64_t)d);    // R8: mod 2^64
             r->sum_wide[e] += (__int128)d;
+            const uint64_t du = (uint64_t)r->s_ts[k] - (uint64_t)r->s_ts[k - 1];  // R20
+            if (r->cnt[e] == 1 || du < r->dmin[e]) r->dmin[e] = du;
+            if (r->cnt[e] == 1 || du > r->dmax[e]) r->dmax[e] = du;
         }
         seq.push_back(r->s_act[k]);
     }
@@ -207,6 +219,10 @@ void orc_get_dfg(const orc_result* r, uint64_t* cnt, int64_t* sum, double* mean)
     copy_out(r->cnt, cnt);
     copy_out(r->sum, sum);
     copy_out(r->mean, mean);
+}
+void orc_get_dfg_minmax(const orc_result* r, uint64_t* dmin, uint64_t* dmax) {
+    copy_out(r->dmin, dmin);
+    copy_out(r->dmax, dmax);
 }
 void orc_get_start_end(const orc_result* r, uint64_t* start, uint64_t* end) {
     copy_out(r->start, start);
@@ -306,6 +322,85 @@ int orc_filter_attr(int64_t n, const uint32_t* case_, int kind, const void* col,
     }
     for (int64_t i = 0; i < n; ++i)
         keep[i] = (any[case_[i]] == (keep_matching != 0)) ? 1 : 0;
+    return 0;
+}
+
+// ---------------------------------------------------------------- case-level filters (NEXT-1)
+// Whole-case filters on the formatted log (S:372-380,
+// S:428-435).  The case's rows are its rows in (case, ts, ingest)
+// order (step 1); match(case) is:
+//   kind 0 START_IN:   first activity in codes[0..ncodes)
+//   kind 1 END_IN:     last activity in codes
+//   kind 2 SIZE:       lo <= n_events <= hi
+//   kind 3 THROUGHPUT: lo <= last ts - first ts <= hi
+//   kind 4 PATHS:      some consecutive pair (a_k, a_{k+1}) equals one of the
+//                      pairs (codes[2j], codes[2j+1])
+// and every row of the case is kept iff match(case) == keep_matching (keep /
+// remove mode).  Returns 1 (EINVAL) on lo > hi or an odd
+// number of path codes; keep[] is in input order.
+int orc_filter_cases(int64_t n, const uint32_t* case_, const uint32_t* act, const int64_t* ts,
+                     int kind, const uint32_t* codes, int64_t ncodes, int64_t lo, int64_t hi,
+                     int keep_matching, uint8_t* keep) {
+    if (kind < 0 || kind > 4) return 1;
+    if ((kind == 2 || kind == 3) && lo > hi) return 1;
+    if (kind == 4 && (ncodes % 2) != 0) return 1;
+    std::vector<int64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), (int64_t)0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t i, int64_t j) {
+        if (case_[i] != case_[j]) return case_[i] < case_[j];
+        return ts[i] < ts[j];
+    });
+    auto in_codes = [&](uint32_t a) {
+        for (int64_t s = 0; s < ncodes; ++s)
+            if (codes[s] == a) return true;
+        return false;
+    };
+    std::map<uint32_t, bool> case_keep;
+    for (int64_t k = 0; k < n;) {
+        int64_t e = k;
+        while (e + 1 < n && case_[idx[e + 1]] == case_[idx[k]]) ++e;
+        bool m = false;
+        if (kind == 0) m = in_codes(act[idx[k]]);
+        if (kind == 1) m = in_codes(act[idx[e]]);
+        if (kind == 2) m = (e - k + 1) >= lo && (e - k + 1) <= hi;
+        if (kind == 3) m = (ts[idx[e]] - ts[idx[k]]) >= lo && (ts[idx[e]] - ts[idx[k]]) <= hi;
+        if (kind == 4)
+            for (int64_t q = k; q < e && !m; ++q)
+                for (int64_t j = 0; j + 1 < ncodes; j += 2)
+                    if (act[idx[q]] == codes[j] && act[idx[q + 1]] == codes[j + 1]) m = true;
+        case_keep[case_[idx[k]]] = (m == (keep_matching != 0));
+        k = e + 1;
+    }
+    for (int64_t i = 0; i < n; ++i) keep[i] = case_keep[case_[i]] ? 1 : 0;
+    return 0;
+}
+
+// filter_by_variants ("keeps/remove all the cases whose variant fall
+// inside the collection"): match(case) = its exact activity
+// sequence equals one of the given sequences (CSR seq_off[0..nseq], seq_act).
+int orc_filter_variants(int64_t n, const uint32_t* case_, const uint32_t* act, const int64_t* ts,
+                        const uint64_t* seq_off, const uint32_t* seq_act, int64_t nseq,
+                        int keep_matching, uint8_t* keep) {
+    std::map<std::vector<uint32_t>, bool> wanted;
+    for (int64_t s = 0; s < nseq; ++s)
+        wanted[std::vector<uint32_t>(seq_act + seq_off[s], seq_act + seq_off[s + 1])] = true;
+    std::vector<int64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), (int64_t)0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t i, int64_t j) {
+        if (case_[i] != case_[j]) return case_[i] < case_[j];
+        return ts[i] < ts[j];
+    });
+    std::map<uint32_t, bool> case_keep;
+    for (int64_t k = 0; k < n;) {
+        int64_t e = k;
+        std::vector<uint32_t> seq;
+        seq.push_back(act[idx[k]]);
+        while (e + 1 < n && case_[idx[e + 1]] == case_[idx[k]]) seq.push_back(act[idx[++e]]);
+        const bool m = wanted.count(seq) > 0;
+        case_keep[case_[idx[k]]] = (m == (keep_matching != 0));
+        k = e + 1;
+    }
+    for (int64_t i = 0; i < n; ++i) keep[i] = case_keep[case_[i]] ? 1 : 0;
     return 0;
 }
 
