@@ -143,6 +143,15 @@ pm4g_status pm4g_sorted_columns(const pm4g_log* log, uint32_t* case_code, uint32
 pm4g_status pm4g_dfg(const pm4g_log* log, uint64_t* cnt, int64_t* dur_sum, double* mean,
                      pm4g_comm* comm, pm4g_stream_t stream);
 
+/* Performance-DFG extremes: for
+ * every edge, dur_min[k] / dur_max[k] = the smallest / largest pair duration
+ * ts_{i+1} - ts_i over its occurrences, as u64 (exact: 0 <= difference < 2^64
+ * after the sort, R20); 0 where cnt[k] = 0.  With comm: min / max over ranks
+ * (NCCL allreduce with ncclMin / ncclMax).  dur_min, dur_max: device [A*A]
+ * (one may be NULL). */
+pm4g_status pm4g_dfg_minmax(const pm4g_log* log, uint64_t* dur_min, uint64_t* dur_max,
+                            pm4g_comm* comm, pm4g_stream_t stream);
+
 /* Start / end activities: start[a] = number of cases whose
  * first formatted row has activity a; end[a] likewise for the last row.
  * Sum start = sum end = n_cases.  start, end: device [A]. */
@@ -200,6 +209,8 @@ typedef struct pm4g_outputs {
     int64_t* dur;         /* [capacity] device */
     uint64_t capacity;
     pm4g_variant_table** variants; /* host out-pointer */
+    uint64_t* dur_min;    /* [A*A] device, optional (NEXT-2, see pm4g_dfg_minmax) */
+    uint64_t* dur_max;    /* [A*A] device, optional */
 } pm4g_outputs;
 pm4g_status pm4g_analyze(const pm4g_log* log, const pm4g_outputs* out, pm4g_comm* comm,
                          pm4g_stream_t stream);
@@ -218,6 +229,38 @@ enum { PM4G_TIME_EVENTS = 0, PM4G_TIME_CASES_CONTAINED = 1, PM4G_TIME_CASES_INTE
  * row of cases with first ts <= t2 and last ts >= t1.  EINVAL if t1 > t2. */
 pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t mode,
                              pm4g_stream_t stream, pm4g_log** out);
+
+/* Whole-case filters on a FORMATTED log (P:98-103,
+ * P:121-127; reading R21).  A case matches on its
+ * formatted rows:
+ *   START_IN / END_IN: its first / last activity is in codes[0..n_codes)
+ *                      (codes >= A never match);
+ *   SIZE:              lo <= n_events <= hi;
+ *   THROUGHPUT:        lo <= last ts - first ts <= hi;
+ *   PATHS:             some consecutive pair (a_k, a_{k+1}) equals one of the
+ *                      pairs (codes[2j], codes[2j+1]).
+ * Every row of the case is kept iff match == (keep != 0) (keep / remove mode,
+ * S:465).  codes: HOST array.  EINVAL: unsorted input, lo > hi, odd
+ * n_codes for PATHS, bad kind.  Returns a new formatted log. */
+enum { PM4G_CASE_START_IN = 0, PM4G_CASE_END_IN = 1, PM4G_CASE_SIZE = 2, PM4G_CASE_THROUGHPUT = 3,
+       PM4G_CASE_PATHS = 4 };
+typedef struct pm4g_case_pred {
+    int32_t kind;              /* PM4G_CASE_* */
+    const uint32_t* codes;     /* host: activity codes, or flattened (a, b) pairs */
+    int64_t n_codes;
+    int64_t lo, hi;            /* SIZE / THROUGHPUT bounds, inclusive */
+} pm4g_case_pred;
+pm4g_status pm4g_filter_cases(const pm4g_log* in, const pm4g_case_pred* pred, int32_t keep,
+                              pm4g_stream_t stream, pm4g_log** out);
+
+/* filter_by_variants ("keeps/remove all the cases whose variant fall
+ * inside the collection"): a case matches iff its exact activity
+ * sequence equals one of the n_seqs sequences given in HOST CSR form
+ * (seq_off[n_seqs + 1] ascending, seq_act[seq_off[n_seqs]]); unknown or empty
+ * sequences never match.  Rows kept iff match == (keep != 0).  Formatted
+ * input required (EINVAL otherwise).  Returns a new formatted log. */
+pm4g_status pm4g_filter_variants(const pm4g_log* in, const uint64_t* seq_off, const uint32_t* seq_act,
+                                 int64_t n_seqs, int32_t keep, pm4g_stream_t stream, pm4g_log** out);
 
 enum { PM4G_COL_ACTIVITY = -1 };
 enum { PM4G_PRED_IN_SET = 0, PM4G_PRED_RANGE_I64 = 1, PM4G_PRED_RANGE_F64 = 2 };

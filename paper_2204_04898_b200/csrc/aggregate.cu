@@ -42,30 +42,6 @@ constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
-// Variant-key hash (internal, verified): Horner polynomial mod 2^64 over act+1.
-constexpr uint64_t HB1 = 0x00000100000001B3ull;
-constexpr uint64_t HB2 = 0xC2B2AE3D27D4EB4Full;
-
-__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdull;
-    k ^= k >> 33;
-    k *= 0xc4ceb9fe1a85ec53ull;
-    k ^= k >> 33;
-    return k;
-}
-
-__device__ __forceinline__ void finish_key(uint64_t h1, uint64_t h2, uint32_t len, bool weak,
-                                           uint64_t& k1, uint64_t& k2) {
-    if (weak) {  // debug: 4-bit key, forces collisions (exercises the exact fallback)
-        k1 = 1ull | ((fmix64(h1) & 0xFull) << 1);
-        k2 = 0;
-        return;
-    }
-    k1 = fmix64(h1 ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) | 1ull;
-    k2 = fmix64(h2 + (uint64_t)len * 0xff51afd7ed558ccdull);
-}
-
 constexpr uint32_t AGG_STAGE = 4096;   // rows of a case tile staged in smem (+ alignment slack)
 constexpr int AGG_CONSUMERS = 256;     // 8 consumer warps; + 1 producer warp
 constexpr int AGG_BLOCK = AGG_CONSUMERS + 32;
@@ -88,16 +64,32 @@ constexpr int HASH_PROBES = 16;
 constexpr uint32_t HASH_EMPTY = 0xffffffffu;
 
 // shared-memory hash slots: as many as fit next to the two stages
-template <class P>
-__host__ __device__ constexpr uint32_t hash_slots() { return sizeof(P) == 1 ? 8192u : 4096u; }
+template <class P, bool MM>
+__host__ __device__ constexpr uint32_t hash_slots() { return (sizeof(P) == 1 && !MM) ? 8192u : 4096u; }
 
 // start/end counters are privatised when A is small enough
 constexpr uint32_t SE_SMEM_MAX_A = 2048;
 __host__ __device__ constexpr uint32_t se_words(uint32_t A) { return A <= SE_SMEM_MAX_A ? 2 * A : 0u; }
 
-template <class P>
+// table layout (u32 words): FULL [cnt | lo | hi](A^2 each) [start | end](A) [min | max](A^2 each, MM);
+// HASH [cnt | lo | hi | key](HS each) [start | end] [min | max](HS each, MM)
+template <class P, bool MM>
 __host__ __device__ constexpr uint32_t tab_words_for(int mode, uint32_t A) {
-    return mode == TAB_FULL ? ((3 * A * A + 2 * A + 31) & ~31u) : (4 * hash_slots<P>() + se_words(A) + 31) & ~31u;
+    return mode == TAB_FULL ? (((3 + (MM ? 2 : 0)) * A * A + 2 * A + 31) & ~31u)
+                            : ((4 + (MM ? 2 : 0)) * hash_slots<P, MM>() + se_words(A) + 31) & ~31u;
+}
+
+// per-pair min / max of the u64 duration (R20): u32 shared tables for
+// durations below 2^32, the global u64 table otherwise
+__device__ __forceinline__ void smem_minmax(uint32_t* mn, uint32_t* mx, unsigned long long* gmn,
+                                            unsigned long long* gmx, uint64_t d) {
+    if ((d >> 32) == 0) {
+        atomicMin(mn, (uint32_t)d);
+        atomicMax(mx, (uint32_t)d);
+    } else {
+        atomicMin(gmn, (unsigned long long)d);
+        atomicMax(gmx, (unsigned long long)d);
+    }
 }
 
 // per-pair accumulation into a (count, lo, hi) triple in shared memory; the
@@ -111,18 +103,18 @@ __device__ __forceinline__ void smem_acc(uint32_t* cnt, uint32_t* lo, uint32_t* 
     if (h) atomicAdd(hi, h);
 }
 
-template <class P, int MODE>
+template <class P, int MODE, bool MM>
 __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
-    uint64_t* __restrict__ packed, uint32_t* __restrict__ n_events, int64_t* __restrict__ dur,
-    uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
+    uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
+    int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
     const bool tables = packed != nullptr;
     const uint32_t AA = A * A;
-    const uint32_t tab_words = tables ? tab_words_for<P>(MODE, A) : 0;
-    constexpr uint32_t HS = hash_slots<P>();
+    const uint32_t tab_words = tables ? tab_words_for<P, MM>(MODE, A) : 0;
+    constexpr uint32_t HS = hash_slots<P, MM>();
     const uint32_t TW = MODE == TAB_FULL ? AA : HS;         // table entries
     uint32_t* sm = (uint32_t*)agg_sm;
     uint32_t* s_cnt = sm;
@@ -131,14 +123,21 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     uint32_t* s_key = sm + 3 * TW;                          // HASH: edge id or HASH_EMPTY
     uint32_t* s_st = sm + (MODE == TAB_FULL ? 3 * AA : 4 * HS);
     uint32_t* s_en = s_st + A;
+    uint32_t* s_mn = s_st + (MODE == TAB_FULL ? 2 * A : se_words(A));   // MM: [TW]
+    uint32_t* s_mx = s_mn + TW;
+    unsigned long long* g_mn = (unsigned long long*)mm;
+    unsigned long long* g_mx = g_mn + AA;
     AggStage<P>* stage = (AggStage<P>*)(agg_sm + (size_t)tab_words * 4);
     uint64_t* g_cnt = packed;
     uint64_t* g_sum = packed + AA;
     uint64_t* g_st = packed + 2 * (size_t)AA;
     uint64_t* g_en = g_st + A;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (uint32_t i = tid; i < tab_words; i += AGG_BLOCK)
-        sm[i] = (MODE == TAB_HASH && i >= 3 * HS && i < 4 * HS) ? HASH_EMPTY : 0u;
+    for (uint32_t i = tid; i < tab_words; i += AGG_BLOCK) {
+        const bool empty_key = MODE == TAB_HASH && i >= 3 * HS && i < 4 * HS;
+        const bool min_init = MM && sm + i >= s_mn && sm + i < s_mx;
+        sm[i] = (empty_key || min_init) ? 0xffffffffu : 0u;
+    }
     if (tid == 0) {
         for (int s = 0; s < AGG_STAGES; ++s) {
             mbar_init(&s_full[s], 1);
@@ -204,6 +203,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                     const uint64_t d = kn - kk;
                     if (MODE == TAB_FULL) {
                         smem_acc(&s_cnt[e], &s_lo[e], &s_hi[e], d);
+                        if (MM) smem_minmax(&s_mn[e], &s_mx[e], &g_mn[e], &g_mx[e], d);
                         continue;
                     }
                     uint32_t h = (e * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
@@ -213,6 +213,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                         if (k == HASH_EMPTY) k = atomicCAS(&s_key[h], HASH_EMPTY, e);
                         if (k == HASH_EMPTY || k == e) {
                             smem_acc(&s_cnt[h], &s_lo[h], &s_hi[h], d);
+                            if (MM) smem_minmax(&s_mn[h], &s_mx[h], &g_mn[e], &g_mx[e], d);
                             done = true;
                             break;
                         }
@@ -220,6 +221,10 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                     if (!done) {   // no slot near: straight to the global table
                         atomicAdd((unsigned long long*)&g_cnt[e], 1ull);
                         atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)d);
+                        if (MM) {
+                            atomicMin(&g_mn[e], (unsigned long long)d);
+                            atomicMax(&g_mx[e], (unsigned long long)d);
+                        }
                     }
                 }
             }
@@ -267,18 +272,22 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
             atomicAdd((unsigned long long*)&g_cnt[e], (unsigned long long)cn);
             const uint64_t sm64 = ((uint64_t)s_hi[j] << 32) | s_lo[j];
             if (sm64) atomicAdd((unsigned long long*)&g_sum[e], (unsigned long long)sm64);
+            if (MM) {
+                if (s_mn[j] != 0xffffffffu) atomicMin(&g_mn[e], (unsigned long long)s_mn[j]);
+                if (s_mx[j]) atomicMax(&g_mx[e], (unsigned long long)s_mx[j]);
+            }
         }
     }
 }
 
-template <class P, int MODE>
+template <class P, int MODE, bool MM>
 static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
-    const size_t tab = o.tables ? (size_t)tab_words_for<P>(MODE, A) * 4 : 0;
+    const size_t tab = o.tables ? (size_t)tab_words_for<P, MM>(MODE, A) * 4 : 0;
     const size_t smem = tab + AGG_STAGES * sizeof(AggStage<P>);
     static size_t attr = 0;
     if (smem > attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, MODE, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = smem;
     }
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
@@ -294,25 +303,32 @@ static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s
     const double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
                          (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, MODE><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
+                (k_aggregate<P, MODE, MM><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
-                    o.tables ? o.packed : nullptr, o.n_events, o.dur, o.k1, o.k2,
+                    o.tables ? o.packed : nullptr, o.mm, o.n_events, o.dur, o.k1, o.k2,
                     debug_weak_hash() ? 1 : 0)));
     return PM4G_OK;
 }
 
+template <class P>
+static pm4g_status launch_agg_p(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
+    const uint32_t A = L->A;
+    const bool mm = o.tables && o.mm;
+    if (mm) {
+        if ((size_t)tab_words_for<P, true>(TAB_FULL, A) * 4 <= AGG_SMEM_MAX) return launch_agg<P, TAB_FULL, true>(L, o, s);
+        return launch_agg<P, TAB_HASH, true>(L, o, s);
+    }
+    if ((size_t)tab_words_for<P, false>(TAB_FULL, A) * 4 <= AGG_SMEM_MAX) return launch_agg<P, TAB_FULL, false>(L, o, s);
+    return launch_agg<P, TAB_HASH, false>(L, o, s);
+}
+
 pm4g_status aggregate(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     if (L->n == 0) return PM4G_OK;
-    const uint32_t A = L->A;
-    const int mode = (size_t)tab_words_for<uint32_t>(TAB_FULL, A) * 4 <= AGG_SMEM_MAX ? TAB_FULL : TAB_HASH;
-#define PM4G_AGG_MODES(P) \
-    return mode == TAB_FULL ? launch_agg<P, TAB_FULL>(L, o, s) : launch_agg<P, TAB_HASH>(L, o, s)
     switch (L->act_bytes) {
-        case 1: PM4G_AGG_MODES(uint8_t);
-        case 2: PM4G_AGG_MODES(uint16_t);
-        default: PM4G_AGG_MODES(uint32_t);
+        case 1: return launch_agg_p<uint8_t>(L, o, s);
+        case 2: return launch_agg_p<uint16_t>(L, o, s);
+        default: return launch_agg_p<uint32_t>(L, o, s);
     }
-#undef PM4G_AGG_MODES
 }
 
 // ------------------------------------------------------------------ K11 finalise
@@ -343,6 +359,40 @@ pm4g_status finalize_tables(const uint64_t* packed, uint32_t A, uint64_t* cnt, i
     PM4G_LAUNCH("k_finalize", total * 8.0 * 2, s,
                 k_finalize<<<std::max(g, 1), 256, 0, s>>>(packed, A, cnt, sum, mean, st, en));
     return PM4G_OK;
+}
+
+// R20: per-edge min / max of the pair duration, 0 where the edge never occurs
+__global__ void k_finalize_minmax(const uint64_t* __restrict__ packed, const uint64_t* __restrict__ mm,
+                                  uint32_t A, uint64_t* dmin, uint64_t* dmax) {
+    const size_t AA = (size_t)A * A;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < AA; e += (size_t)gridDim.x * blockDim.x) {
+        const bool any = packed[e] != 0;
+        if (dmin) dmin[e] = any ? mm[e] : 0;
+        if (dmax) dmax[e] = any ? mm[AA + e] : 0;
+    }
+}
+
+static pm4g_status finalize_minmax(const uint64_t* packed, const uint64_t* mm, uint32_t A, uint64_t* dmin,
+                                   uint64_t* dmax, cudaStream_t s) {
+    const size_t AA = (size_t)A * A;
+    const int g = (int)std::min<size_t>((AA + 255) / 256, (size_t)num_sms() * 4);
+    PM4G_LAUNCH("k_finalize_minmax", AA * 8.0 * 5, s,
+                k_finalize_minmax<<<std::max(g, 1), 256, 0, s>>>(packed, mm, A, dmin, dmax));
+    return PM4G_OK;
+}
+
+// [min A2 | max A2] initial values: min = ~0, max = 0
+static pm4g_status init_minmax(uint64_t* mm, uint32_t A, cudaStream_t s) {
+    const size_t AA = (size_t)A * A;
+    PM4G_CK(cudaMemsetAsync(mm, 0xff, AA * 8, s));
+    PM4G_CK(cudaMemsetAsync(mm + AA, 0, AA * 8, s));
+    return PM4G_OK;
+}
+
+static pm4g_status reduce_minmax(pm4g_comm* comm, uint64_t* mm, uint32_t A, cudaStream_t s) {
+    const size_t AA = (size_t)A * A;
+    PM4G_TRY(comm_allreduce_u64_op(comm, mm, AA, COMM_MIN, s));
+    return comm_allreduce_u64_op(comm, mm + AA, AA, COMM_MAX, s);
 }
 
 static pm4g_status require_sorted(const pm4g_log* L) {
@@ -399,6 +449,30 @@ pm4g_status pm4g_dfg(const pm4g_log* L, uint64_t* cnt, int64_t* dur_sum, double*
     PM4G_TRY(tables_into(L, pk.as<uint64_t>(), s));
     if (comm) PM4G_TRY(comm_allreduce_u64(comm, pk.as<uint64_t>(), packed_len(L->A), s));
     return finalize_tables(pk.as<uint64_t>(), L->A, cnt, dur_sum, mean, nullptr, nullptr, s);
+}
+
+pm4g_status pm4g_dfg_minmax(const pm4g_log* L, uint64_t* dur_min, uint64_t* dur_max, pm4g_comm* comm,
+                            pm4g_stream_t stream) {
+    PM4G_TRY(require_sorted(L));
+    if (!dur_min && !dur_max) return fail(PM4G_EINVAL, "dur_min or dur_max is required");
+    PM4G_TRY(check_table_size(L));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t AA = (size_t)L->A * L->A;
+    Scratch pk(s), mm(s);
+    PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
+    PM4G_TRY(mm.alloc(2 * AA * 8));
+    PM4G_CK(cudaMemsetAsync(pk.p, 0, packed_len(L->A) * 8, s));
+    PM4G_TRY(init_minmax(mm.as<uint64_t>(), L->A, s));
+    AggOut o;
+    o.packed = pk.as<uint64_t>();
+    o.mm = mm.as<uint64_t>();
+    o.tables = true;
+    PM4G_TRY(aggregate(L, o, s));
+    if (comm) {
+        PM4G_TRY(comm_allreduce_u64(comm, pk.as<uint64_t>(), AA, s));   // counts decide empty edges
+        PM4G_TRY(reduce_minmax(comm, mm.as<uint64_t>(), L->A, s));
+    }
+    return finalize_minmax(pk.as<uint64_t>(), mm.as<uint64_t>(), L->A, dur_min, dur_max, s);
 }
 
 pm4g_status pm4g_start_end(const pm4g_log* L, uint64_t* start, uint64_t* end, pm4g_comm* comm,
@@ -471,14 +545,20 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
         if (out->capacity < (uint64_t)L->n_cases) return fail(PM4G_EINVAL, "capacity < n_cases");
     }
     uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
-    Scratch pk(s), keys(s);
+    Scratch pk(s), keys(s), mm(s);
     AggOut o;
-    if (want_tables) {
+    const bool want_mm = out->dur_min || out->dur_max;
+    if (want_tables || want_mm) {
         PM4G_TRY(check_table_size(L));
         PM4G_TRY(pk.alloc(packed_len(L->A) * 8));
         PM4G_CK(cudaMemsetAsync(pk.p, 0, packed_len(L->A) * 8, s));
         o.packed = pk.as<uint64_t>();
         o.tables = true;
+    }
+    if (want_mm) {
+        PM4G_TRY(mm.alloc(2 * (size_t)L->A * L->A * 8));
+        PM4G_TRY(init_minmax(mm.as<uint64_t>(), L->A, s));
+        o.mm = mm.as<uint64_t>();
     }
     o.n_events = out->n_events;
     o.dur = out->dur;
@@ -490,10 +570,14 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
     PM4G_TRY(aggregate(L, o, s));
     if (out->case_code && L->n_cases > 0)
         PM4G_CK(cudaMemcpyAsync(out->case_code, L->s_case_code, L->n_cases * 4, cudaMemcpyDeviceToDevice, s));
-    if (want_tables) {
+    if (want_tables || want_mm) {
         if (comm) PM4G_TRY(comm_allreduce_u64(comm, o.packed, packed_len(L->A), s));
         PM4G_TRY(finalize_tables(o.packed, L->A, out->cnt, out->dur_sum, out->mean, out->start,
                                  out->end, s));
+    }
+    if (want_mm) {
+        if (comm) PM4G_TRY(reduce_minmax(comm, o.mm, L->A, s));
+        PM4G_TRY(finalize_minmax(o.packed, o.mm, L->A, out->dur_min, out->dur_max, s));
     }
     if (out->variants) {
         *out->variants = nullptr;

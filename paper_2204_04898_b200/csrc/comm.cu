@@ -79,8 +79,12 @@ struct pm4g_comm {
 namespace pm4g {
 
 pm4g_status comm_allreduce_u64(pm4g_comm* c, uint64_t* buf, size_t count, cudaStream_t s) {
+    return comm_allreduce_u64_op(c, buf, count, COMM_SUM, s);
+}
+
+pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int op, cudaStream_t s) {
     if (c->nranks == 1) return PM4G_OK;
-    NcclResult r = g_nccl.allReduce(buf, buf, count, NCCL_UINT64, NCCL_SUM, c->comm, s);
+    NcclResult r = g_nccl.allReduce(buf, buf, count, NCCL_UINT64, op, c->comm, s);
     if (r) return nccl_fail(r, "ncclAllReduce");
     return PM4G_OK;
 }

@@ -564,6 +564,98 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
     return PM4G_OK;
 }
 
+// ------------------------------------------------------------------ whole-case filters (NEXT-1)
+// On a formatted log: one thread per case evaluates the case predicate on its
+// rows [off[c], off[c+1]) and writes the case's keep bytes; compact_log then
+// moves the kept rows and rebuilds the case offsets (R21).
+struct CasePred {
+    int kind;
+    const uint32_t* bitmap;   // START_IN / END_IN: A-bit activity set
+    const uint64_t* pairs;    // PATHS: sorted unique edge ids a * A + b
+    int64_t npairs;
+    int64_t lo, hi;
+    int keep;
+};
+
+__device__ __forceinline__ bool in_sorted(const uint64_t* v, int64_t n, uint64_t x) {
+    int64_t a = 0, b = n;
+    while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if (v[m] < x) a = m + 1; else b = m;
+    }
+    return a < n && v[a] == x;
+}
+
+template <class P>
+__global__ void k_case_filter(const uint64_t* __restrict__ key, const P* __restrict__ act,
+                              const uint32_t* __restrict__ off, const uint64_t* __restrict__ d_n_cases,
+                              uint32_t A, CasePred p, uint8_t* __restrict__ mask) {
+    const uint64_t C = *d_n_cases;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < C; c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = off[c], e = off[c + 1];
+        bool m = false;
+        if (p.kind == PM4G_CASE_START_IN || p.kind == PM4G_CASE_END_IN) {
+            const uint32_t a = (uint32_t)act[p.kind == PM4G_CASE_START_IN ? f : e - 1];
+            m = (p.bitmap[a >> 5] >> (a & 31)) & 1u;
+        } else if (p.kind == PM4G_CASE_SIZE) {
+            const int64_t len = (int64_t)(e - f);
+            m = len >= p.lo && len <= p.hi;
+        } else if (p.kind == PM4G_CASE_THROUGHPUT) {
+            const int64_t d = (int64_t)(key[e - 1] - key[f]);   // last ts - first ts (R9)
+            m = d >= p.lo && d <= p.hi;
+        } else {   // PATHS
+            for (uint32_t r = f; r + 1 < e && !m; ++r)
+                m = in_sorted(p.pairs, p.npairs, (uint64_t)act[r] * A + (uint64_t)act[r + 1]);
+        }
+        const uint8_t k = (m == (p.keep != 0)) ? 1 : 0;
+        for (uint32_t r = f; r < e; ++r) mask[r] = k;
+    }
+}
+
+// filter_by_variants: the case's variant key (same hash as A8) is looked up
+// among the query keys (sorted, host-hashed); every equal key is verified by
+// comparing the sequences exactly.
+struct VarQuery {
+    const uint64_t* k1;       // sorted by (k1, k2)
+    const uint64_t* k2;
+    const uint32_t* qi;       // query sequence of each key
+    int64_t nq;
+    const uint64_t* qoff;     // query CSR
+    const uint32_t* qact;
+    int keep;
+};
+
+template <class P>
+__global__ void k_variant_filter(const P* __restrict__ act, const uint32_t* __restrict__ off,
+                                 const uint64_t* __restrict__ d_n_cases, const uint64_t* __restrict__ ck1,
+                                 const uint64_t* __restrict__ ck2, VarQuery q, uint8_t* __restrict__ mask) {
+    const uint64_t C = *d_n_cases;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < C; c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = off[c], e = off[c + 1];
+        const uint64_t a1 = ck1[c], a2 = ck2[c];
+        int64_t lo = 0, hi = q.nq;   // first key >= (a1, a2)
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (q.k1[mid] < a1 || (q.k1[mid] == a1 && q.k2[mid] < a2)) lo = mid + 1; else hi = mid;
+        }
+        bool m = false;
+        for (int64_t j = lo; j < q.nq && q.k1[j] == a1 && q.k2[j] == a2 && !m; ++j) {
+            const uint32_t s = q.qi[j];
+            const uint64_t s0 = q.qoff[s], s1 = q.qoff[s + 1];
+            if (s1 - s0 != (uint64_t)(e - f)) continue;
+            bool eq = true;
+            for (uint64_t t = 0; t < s1 - s0 && eq; ++t) eq = (uint32_t)act[f + t] == q.qact[s0 + t];
+            m = eq;
+        }
+        const uint8_t k = (m == (q.keep != 0)) ? 1 : 0;
+        for (uint32_t r = f; r < e; ++r) mask[r] = k;
+    }
+}
+
+static int case_grid(uint64_t C) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((C + 255) / 256, (uint64_t)num_sms() * 8));
+}
+
 }  // namespace pm4g
 
 using namespace pm4g;
@@ -596,6 +688,141 @@ pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t
             PM4G_LAUNCH("k_init_span", R * 16.0, s, k_init_span<<<gsz(R), 256, 0, s>>>(lo, hi, R));
             PM4G_LAUNCH("k_case_span", n * 12.0, s, k_case_span<<<gsz(n), 256, 0, s>>>(v, n, lo, hi));
             PM4G_LAUNCH("k_time_cases", n * 13.0, s, k_time_cases<<<gsz(n), 256, 0, s>>>(v, n, lo, hi, t1, t2, mode, mask.as<uint8_t>()));
+        }
+    }
+    return compact_log(in, mask.as<uint8_t>(), s, out);
+}
+
+pm4g_status pm4g_filter_cases(const pm4g_log* in, const pm4g_case_pred* pred, int32_t keep,
+                              pm4g_stream_t stream, pm4g_log** out) {
+    if (!in || !pred || !out) return fail(PM4G_EINVAL, "null argument");
+    *out = nullptr;
+    if (!in->sorted) return fail(PM4G_EINVAL, "case-level filters need a formatted log (call pm4g_sort first)");
+    const int kind = pred->kind;
+    if (kind < PM4G_CASE_START_IN || kind > PM4G_CASE_PATHS) return fail(PM4G_EINVAL, "bad case predicate kind");
+    if ((kind == PM4G_CASE_SIZE || kind == PM4G_CASE_THROUGHPUT) && pred->lo > pred->hi)
+        return fail(PM4G_EINVAL, "lo > hi (S:459)");
+    if (pred->n_codes < 0 || (pred->n_codes > 0 && !pred->codes)) return fail(PM4G_EINVAL, "bad code list");
+    if (kind == PM4G_CASE_PATHS && (pred->n_codes % 2) != 0) return fail(PM4G_EINVAL, "paths need (a, b) pairs");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t A = in->A;
+    CasePred p{};
+    p.kind = kind;
+    p.lo = pred->lo;
+    p.hi = pred->hi;
+    p.keep = keep ? 1 : 0;
+    Scratch aux(s), mask(s);
+    if (kind == PM4G_CASE_START_IN || kind == PM4G_CASE_END_IN) {
+        std::vector<uint32_t> bm((A + 31) / 32, 0u);
+        for (int64_t i = 0; i < pred->n_codes; ++i)
+            if (pred->codes[i] < A) bm[pred->codes[i] >> 5] |= 1u << (pred->codes[i] & 31);
+        PM4G_TRY(aux.alloc(bm.size() * 4));
+        PM4G_CK(cudaMemcpyAsync(aux.p, bm.data(), bm.size() * 4, cudaMemcpyHostToDevice, s));
+        p.bitmap = aux.as<uint32_t>();
+    } else if (kind == PM4G_CASE_PATHS) {
+        std::vector<uint64_t> pr;
+        for (int64_t i = 0; i + 1 < pred->n_codes; i += 2)
+            if (pred->codes[i] < A && pred->codes[i + 1] < A)
+                pr.push_back((uint64_t)pred->codes[i] * A + pred->codes[i + 1]);
+        std::sort(pr.begin(), pr.end());
+        pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+        PM4G_TRY(aux.alloc(std::max<size_t>(pr.size(), 1) * 8));
+        if (!pr.empty()) PM4G_CK(cudaMemcpyAsync(aux.p, pr.data(), pr.size() * 8, cudaMemcpyHostToDevice, s));
+        p.pairs = aux.as<uint64_t>();
+        p.npairs = (int64_t)pr.size();
+    }
+    const int64_t n = in->n;
+    PM4G_TRY(mask.alloc(std::max<int64_t>(n, 1)));
+    if (n > 0) {
+        const uint64_t cap = std::min<uint64_t>((uint64_t)n, (uint64_t)(in->case_max - in->case_min) + 1);
+        const int g = case_grid(cap);
+        switch (in->act_bytes) {
+            case 1: PM4G_LAUNCH("k_case_filter", n * 1.0 + cap * 8.0, s, (k_case_filter<uint8_t><<<g, 256, 0, s>>>(in->key, (const uint8_t*)in->s_act, in->off, in->d_n_cases, A, p, mask.as<uint8_t>()))); break;
+            case 2: PM4G_LAUNCH("k_case_filter", n * 1.0 + cap * 8.0, s, (k_case_filter<uint16_t><<<g, 256, 0, s>>>(in->key, (const uint16_t*)in->s_act, in->off, in->d_n_cases, A, p, mask.as<uint8_t>()))); break;
+            default: PM4G_LAUNCH("k_case_filter", n * 1.0 + cap * 8.0, s, (k_case_filter<uint32_t><<<g, 256, 0, s>>>(in->key, (const uint32_t*)in->s_act, in->off, in->d_n_cases, A, p, mask.as<uint8_t>()))); break;
+        }
+    }
+    return compact_log(in, mask.as<uint8_t>(), s, out);
+}
+
+pm4g_status pm4g_filter_variants(const pm4g_log* in, const uint64_t* seq_off, const uint32_t* seq_act,
+                                 int64_t n_seqs, int32_t keep, pm4g_stream_t stream, pm4g_log** out) {
+    if (!in || !out) return fail(PM4G_EINVAL, "null argument");
+    *out = nullptr;
+    if (!in->sorted) return fail(PM4G_EINVAL, "case-level filters need a formatted log (call pm4g_sort first)");
+    if (n_seqs < 0 || (n_seqs > 0 && (!seq_off || !seq_act))) return fail(PM4G_EINVAL, "bad sequence list");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t A = in->A;
+    // host: hash every query sequence like A8 (sequences with codes >= A cannot match)
+    const bool weak = debug_weak_hash();
+    struct QK {
+        uint64_t k1, k2;
+        uint32_t qi;
+    };
+    std::vector<QK> keys;
+    std::vector<uint64_t> qoff(1, 0);
+    std::vector<uint32_t> qact;
+    for (int64_t i = 0; i < n_seqs; ++i) {
+        const uint64_t b = seq_off[i], e = seq_off[i + 1];
+        if (e < b) return fail(PM4G_EINVAL, "seq_off not ascending");
+        if (e == b) continue;   // the empty sequence is no case's variant
+        bool ok = true;
+        uint64_t h1 = 0, h2 = 0;
+        for (uint64_t t = b; t < e; ++t) {
+            ok = ok && seq_act[t] < A;
+            h1 = h1 * HB1 + ((uint64_t)seq_act[t] + 1);
+            h2 = h2 * HB2 + ((uint64_t)seq_act[t] + 1);
+        }
+        if (!ok || e - b > 0xffffffffull) continue;
+        QK k;
+        finish_key(h1, h2, (uint32_t)(e - b), weak, k.k1, k.k2);
+        k.qi = (uint32_t)(qoff.size() - 1);
+        keys.push_back(k);
+        qact.insert(qact.end(), seq_act + b, seq_act + e);
+        qoff.push_back(qact.size());
+    }
+    std::sort(keys.begin(), keys.end(), [](const QK& x, const QK& y) {
+        return x.k1 != y.k1 ? x.k1 < y.k1 : (x.k2 != y.k2 ? x.k2 < y.k2 : x.qi < y.qi);
+    });
+    const size_t nq = keys.size();
+    std::vector<uint64_t> hk1(nq), hk2(nq);
+    std::vector<uint32_t> hqi(nq);
+    for (size_t i = 0; i < nq; ++i) {
+        hk1[i] = keys[i].k1;
+        hk2[i] = keys[i].k2;
+        hqi[i] = keys[i].qi;
+    }
+    Scratch qb(s), ck(s), mask(s);
+    const size_t n1 = std::max<size_t>(nq, 1), no = qoff.size(), na = std::max<size_t>(qact.size(), 1);
+    PM4G_TRY(qb.alloc(n1 * 20 + no * 8 + na * 4 + 64));
+    uint64_t* d_k1 = qb.as<uint64_t>();
+    uint64_t* d_k2 = d_k1 + n1;
+    uint64_t* d_off = d_k2 + n1;
+    uint32_t* d_qi = (uint32_t*)(d_off + no);
+    uint32_t* d_act = d_qi + n1;
+    if (nq) {
+        PM4G_CK(cudaMemcpyAsync(d_k1, hk1.data(), nq * 8, cudaMemcpyHostToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(d_k2, hk2.data(), nq * 8, cudaMemcpyHostToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(d_qi, hqi.data(), nq * 4, cudaMemcpyHostToDevice, s));
+        PM4G_CK(cudaMemcpyAsync(d_act, qact.data(), qact.size() * 4, cudaMemcpyHostToDevice, s));
+    }
+    PM4G_CK(cudaMemcpyAsync(d_off, qoff.data(), no * 8, cudaMemcpyHostToDevice, s));
+    // per-case keys: the same A8 pass the variant pipeline uses
+    const int64_t n = in->n;
+    const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)n, (uint64_t)(in->case_max - in->case_min) + 1));
+    PM4G_TRY(ck.alloc(cap * 16));
+    PM4G_TRY(mask.alloc(std::max<int64_t>(n, 1)));
+    if (n > 0) {
+        AggOut o;
+        o.k1 = ck.as<uint64_t>();
+        o.k2 = o.k1 + cap;
+        PM4G_TRY(aggregate(in, o, s));
+        VarQuery q{d_k1, d_k2, d_qi, (int64_t)nq, d_off, d_act, keep ? 1 : 0};
+        const int g = case_grid(cap);
+        switch (in->act_bytes) {
+            case 1: PM4G_LAUNCH("k_variant_filter", n * 2.0 + cap * 24.0, s, (k_variant_filter<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)in->s_act, in->off, in->d_n_cases, o.k1, o.k2, q, mask.as<uint8_t>()))); break;
+            case 2: PM4G_LAUNCH("k_variant_filter", n * 3.0 + cap * 24.0, s, (k_variant_filter<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)in->s_act, in->off, in->d_n_cases, o.k1, o.k2, q, mask.as<uint8_t>()))); break;
+            default: PM4G_LAUNCH("k_variant_filter", n * 5.0 + cap * 24.0, s, (k_variant_filter<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)in->s_act, in->off, in->d_n_cases, o.k1, o.k2, q, mask.as<uint8_t>()))); break;
         }
     }
     return compact_log(in, mask.as<uint8_t>(), s, out);

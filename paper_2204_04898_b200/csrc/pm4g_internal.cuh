@@ -292,8 +292,35 @@ pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits,
                            cudaStream_t s);  // generic: (key, u32 payload), in place
 pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s);
 
+// Variant-key hash (internal, verified): Horner polynomial mod 2^64 over
+// act + 1, two bases, finished with the length.  Host and device: the variant
+// filter hashes its query sequences on the host the same way.
+constexpr uint64_t HB1 = 0x00000100000001B3ull;
+constexpr uint64_t HB2 = 0xC2B2AE3D27D4EB4Full;
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__host__ __device__ __forceinline__ void finish_key(uint64_t h1, uint64_t h2, uint32_t len, bool weak,
+                                                    uint64_t& k1, uint64_t& k2) {
+    if (weak) {  // debug: 4-bit key, forces collisions (exercises the exact fallback)
+        k1 = 1ull | ((fmix64(h1) & 0xFull) << 1);
+        k2 = 0;
+        return;
+    }
+    k1 = fmix64(h1 ^ ((uint64_t)len * 0x9E3779B97F4A7C15ull)) | 1ull;
+    k2 = fmix64(h2 + (uint64_t)len * 0xff51afd7ed558ccdull);
+}
+
 struct AggOut {
     uint64_t* packed = nullptr;   // [cnt A2 | sum A2 | start A | end A] (zeroed by caller)
+    uint64_t* mm = nullptr;       // [min A2 | max A2] (caller sets min = ~0, max = 0); with packed only
     uint32_t* n_events = nullptr; // [n_cases]
     int64_t* dur = nullptr;       // [n_cases]
     uint64_t* k1 = nullptr;       // [n_cases] variant keys
@@ -306,6 +333,8 @@ pm4g_status finalize_tables(const uint64_t* packed, uint32_t A, uint64_t* cnt, i
 pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint64_t* k2,
                                cudaStream_t s, pm4g_variant_table** out);
 pm4g_status comm_allreduce_u64(pm4g_comm* c, uint64_t* buf, size_t count, cudaStream_t s);
+enum { COMM_SUM = 0, COMM_MAX = 2, COMM_MIN = 3 };   // ncclRedOp_t values
+pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int op, cudaStream_t s);
 pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
                                           pm4g_variant_table** out);
 pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,

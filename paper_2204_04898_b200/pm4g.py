@@ -26,6 +26,7 @@ PM4G_TIME_EVENTS, PM4G_TIME_CASES_CONTAINED, PM4G_TIME_CASES_INTERSECTING = 0, 1
 PM4G_COL_ACTIVITY = -1
 PM4G_PRED_IN_SET, PM4G_PRED_RANGE_I64, PM4G_PRED_RANGE_F64 = 0, 1, 2
 PM4G_LEVEL_EVENTS, PM4G_LEVEL_CASES = 0, 1
+PM4G_CASE_START_IN, PM4G_CASE_END_IN, PM4G_CASE_SIZE, PM4G_CASE_THROUGHPUT, PM4G_CASE_PATHS = range(5)
 
 _STATUS = {1: "EINVAL", 2: "EDATA", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "EKEYWIDTH", 7: "ECOLLISION"}
 
@@ -62,10 +63,14 @@ class pm4g_pred(ctypes.Structure):
                 ("lo_f", ctypes.c_double), ("hi_f", ctypes.c_double)]
 
 
+class pm4g_case_pred(ctypes.Structure):
+    _fields_ = [("kind", I32), ("codes", P), ("n_codes", I64), ("lo", I64), ("hi", I64)]
+
+
 class pm4g_outputs(ctypes.Structure):
     _fields_ = [("cnt", P), ("dur_sum", P), ("mean", P), ("start", P), ("end", P),
                 ("case_code", P), ("n_events", P), ("dur", P), ("capacity", U64),
-                ("variants", ctypes.POINTER(P))]
+                ("variants", ctypes.POINTER(P)), ("dur_min", P), ("dur_max", P)]
 
 
 _SIGS = {
@@ -76,6 +81,7 @@ _SIGS = {
     "pm4g_sorted_columns": ([P, P, P, P, P], I32),
     "pm4g_dfg": ([P, P, P, P, P, P], I32),
     "pm4g_start_end": ([P, P, P, P, P], I32),
+    "pm4g_dfg_minmax": ([P, P, P, P, P], I32),
     "pm4g_case_durations": ([P, P, P, P, U64, ctypes.POINTER(U64), P], I32),
     "pm4g_variants": ([P, P, P, ctypes.POINTER(P)], I32),
     "pm4g_variants_size": ([P, ctypes.POINTER(U64), ctypes.POINTER(U64)], I32),
@@ -85,6 +91,8 @@ _SIGS = {
     "pm4g_analyze": ([P, ctypes.POINTER(pm4g_outputs), P, P], I32),
     "pm4g_filter_time": ([P, I64, I64, I32, P, ctypes.POINTER(P)], I32),
     "pm4g_filter_attr": ([P, I32, ctypes.POINTER(pm4g_pred), I32, I32, P, ctypes.POINTER(P)], I32),
+    "pm4g_filter_cases": ([P, ctypes.POINTER(pm4g_case_pred), I32, P, ctypes.POINTER(P)], I32),
+    "pm4g_filter_variants": ([P, P, P, I64, I32, P, ctypes.POINTER(P)], I32),
     "pm4g_comm_unique_id": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
     "pm4g_comm_create": ([P, I32, I32, ctypes.POINTER(P)], I32),
     "pm4g_comm_destroy": ([P], I32),
@@ -231,6 +239,14 @@ class Log:
         _check(lib().pm4g_dfg(self.h, _ptr(cnt), _ptr(sm), _ptr(mean), _comm(comm), _stream(stream)))
         return cnt.view(A, A), sm.view(A, A), (mean.view(A, A) if with_mean else None)
 
+    def dfg_minmax(self, comm=None, stream=None):
+        """NEXT-2: per-edge (min, max) pair duration, u64 as int64 tensors [A, A]."""
+        A, dev = self.A, _dev()
+        mn = torch.empty(A * A, dtype=torch.int64, device=dev)
+        mx = torch.empty(A * A, dtype=torch.int64, device=dev)
+        _check(lib().pm4g_dfg_minmax(self.h, _ptr(mn), _ptr(mx), _comm(comm), _stream(stream)))
+        return mn.view(A, A), mx.view(A, A)
+
     def start_end(self, comm=None, stream=None):
         A, dev = self.A, _dev()
         st = torch.empty(A, dtype=torch.int64, device=dev)
@@ -254,8 +270,10 @@ class Log:
         _check(lib().pm4g_variants(self.h, _comm(comm), _stream(stream), ctypes.byref(out)))
         return VariantTable(out)
 
-    def analyze(self, comm=None, stream=None, tables=True, cases=True, variants=True, out=None):
-        """Fused pass.  ``out``: optional dict of preallocated tensors (reused across calls)."""
+    def analyze(self, comm=None, stream=None, tables=True, cases=True, variants=True, out=None,
+                minmax=False):
+        """Fused pass.  ``out``: optional dict of preallocated tensors (reused across calls).
+        ``minmax``: also the per-edge min / max durations ("dur_min", "dur_max")."""
         A, dev = self.A, _dev()
         C = self.info().n_cases if cases else 0
         o = dict(out or {})
@@ -265,6 +283,9 @@ class Log:
             o.setdefault("mean", torch.empty(A * A, dtype=torch.float64, device=dev))
             o.setdefault("start", torch.empty(A, dtype=torch.int64, device=dev))
             o.setdefault("end", torch.empty(A, dtype=torch.int64, device=dev))
+        if minmax:
+            o.setdefault("dur_min", torch.empty(A * A, dtype=torch.int64, device=dev))
+            o.setdefault("dur_max", torch.empty(A * A, dtype=torch.int64, device=dev))
         if cases:
             for k, dt in (("case_code", torch.uint32), ("n_events", torch.uint32), ("dur", torch.int64)):
                 if k not in o or o[k].numel() < C:
@@ -274,7 +295,7 @@ class Log:
         outs = pm4g_outputs(g("cnt"), g("dur_sum"), g("mean"), g("start"), g("end"),
                             g("case_code"), g("n_events"), g("dur"),
                             min((o[k].numel() for k in ("case_code", "n_events", "dur") if k in o), default=0),
-                            ctypes.pointer(vh) if variants else None)
+                            ctypes.pointer(vh) if variants else None, g("dur_min"), g("dur_max"))
         _check(lib().pm4g_analyze(self.h, ctypes.byref(outs), _comm(comm), _stream(stream)))
         res = dict(o)
         if variants:
@@ -300,6 +321,33 @@ class Log:
         out = ctypes.c_void_p()
         _check(lib().pm4g_filter_attr(self.h, int(column), ctypes.byref(pred), int(level),
                                       1 if keep else 0, _stream(stream), ctypes.byref(out)))
+        return Log(out, self.A, self.act_bytes)
+
+    def filter_cases(self, kind: int, codes=None, lo: int = 0, hi: int = 0, keep: bool = True,
+                     stream=None) -> "Log":
+        """NEXT-1 whole-case filter (formatted log): PM4G_CASE_START_IN / END_IN (codes),
+        SIZE / THROUGHPUT (lo, hi inclusive), PATHS (codes = flattened (a, b) pairs)."""
+        vals = [int(c) for c in (codes or [])]
+        arr = (U32 * max(1, len(vals)))(*vals)
+        pred = pm4g_case_pred(int(kind), ctypes.cast(arr, P) if vals else None, len(vals), int(lo), int(hi))
+        out = ctypes.c_void_p()
+        _check(lib().pm4g_filter_cases(self.h, ctypes.byref(pred), 1 if keep else 0, _stream(stream),
+                                       ctypes.byref(out)))
+        return Log(out, self.A, self.act_bytes)
+
+    def filter_variants(self, seqs, keep: bool = True, stream=None) -> "Log":
+        """filter_by_variants: keep / remove the cases whose exact activity
+        sequence is one of ``seqs`` (iterable of code sequences)."""
+        seqs = [[int(x) for x in q] for q in seqs]
+        off = [0]
+        for q in seqs:
+            off.append(off[-1] + len(q))
+        flat = [x for q in seqs for x in q]
+        off_arr = (U64 * len(off))(*off)
+        act_arr = (U32 * max(1, len(flat)))(*flat)
+        out = ctypes.c_void_p()
+        _check(lib().pm4g_filter_variants(self.h, ctypes.cast(off_arr, P), ctypes.cast(act_arr, P),
+                                          len(seqs), 1 if keep else 0, _stream(stream), ctypes.byref(out)))
         return Log(out, self.A, self.act_bytes)
 
 
