@@ -67,6 +67,7 @@ def _load():
         L.orc_filter_cases.restype = I32
         L.orc_filter_variants.argtypes = [I64, P, P, P, P, P, I64, I32, P]
         L.orc_filter_variants.restype = I32
+        L.orc_efg.argtypes = [I64, P, P, P, ctypes.c_uint32, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -244,3 +245,19 @@ def filter_variants(case, act, ts, seqs, keep: bool = True) -> np.ndarray:
     L.orc_filter_variants(c.size, _ptr(c), _ptr(a), _ptr(t), _ptr(off), _ptr(flat), len(seqs),
                           1 if keep else 0, _ptr(out))
     return out.astype(bool)
+
+
+def efg(case, act, ts, n_activities: int) -> dict:
+    """NEXT-3: eventually-follows graph over all
+    in-case ordered pairs i < j and the temporal profile (reading R22).
+    Returns {"cnt", "sum" (u64), "sumsq" (Python int matrix as lo / hi u64),
+    "sq_lo", "sq_hi", "mean", "stdev"}, each [A, A]."""
+    L = _load()
+    c, a, t = _u32(case), _u32(act), _i64(ts)
+    A = int(n_activities)
+    out = {k: np.zeros(A * A, np.uint64) for k in ("cnt", "sum", "sq_lo", "sq_hi")}
+    out["mean"] = np.zeros(A * A, np.float64)
+    out["stdev"] = np.zeros(A * A, np.float64)
+    L.orc_efg(c.size, _ptr(c), _ptr(a), _ptr(t), A, _ptr(out["cnt"]), _ptr(out["sum"]),
+              _ptr(out["sq_lo"]), _ptr(out["sq_hi"]), _ptr(out["mean"]), _ptr(out["stdev"]))
+    return {k: v.reshape(A, A) for k, v in out.items()}

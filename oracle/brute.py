@@ -107,3 +107,13 @@ def filter_variants(case, act, ts, seqs, keep=True):
     want = set(tuple(int(x) for x in q) for q in seqs)
     ok = {c: (tuple(a for _, _, a in evs) in want) == keep for c, evs in tr.items()}
     return [i for i, c in enumerate(case) if ok[int(c)]]
+
+
+def efg(case, act, ts):
+    """S:318-329 by enumeration: {(a, b): [durations of every in-case pair i < j]}."""
+    out = defaultdict(list)
+    for c, evs in traces(case, act, ts).items():
+        for x in range(len(evs)):
+            for y in range(x + 1, len(evs)):
+                out[(evs[x][2], evs[y][2])].append(evs[y][0] - evs[x][0])
+    return dict(out)

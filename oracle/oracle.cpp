@@ -36,6 +36,7 @@
 // __int128 shadow records whether any sum wrapped.
 // ============================================================================
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -402,6 +403,60 @@ int orc_filter_variants(int64_t n, const uint32_t* case_, const uint32_t* act, c
     }
     for (int64_t i = 0; i < n; ++i) keep[i] = case_keep[case_[i]] ? 1 : 0;
     return 0;
+}
+
+// ---------------------------------------------------------------- EFG + temporal profile (NEXT-3)
+// P:122 "EFG retrieval / Temporal Profile (efg.py): discovers the
+// eventually-follows graphs or the temporal profile".
+// For every case of the formatted log (step 1) and every ordered index pair
+// i < j inside it: edge (act_i, act_j) gets count += 1, sum += d and
+// sumsq += d^2 with d = ts_j - ts_i >= 0 taken as u64 (R20); sum modulo 2^64
+// (R8), sumsq as an exact unsigned 128-bit value ("unsigned 128-bit"),
+// returned as lo / hi u64 words.  Temporal profile (reading R22): with
+// m = (double)count, mean = (double)sum / m; s2 = (double)sumsq_hi * 2^64 +
+// (double)sumsq_lo; V = (s2 - (double)sum * mean) / m; stdev = V > 0 ?
+// sqrt(V) : 0 -- IEEE fp64 round-to-nearest, no contraction (ISO C++ mode);
+// mean = stdev = 0 where count = 0.
+void orc_efg(int64_t n, const uint32_t* case_, const uint32_t* act, const int64_t* ts, uint32_t A,
+             uint64_t* cnt, uint64_t* sum, uint64_t* sq_lo, uint64_t* sq_hi, double* mean, double* stdev) {
+    const size_t AA = (size_t)A * A;
+    std::vector<uint64_t> c(AA, 0), sm(AA, 0);
+    std::vector<unsigned __int128> q(AA, 0);
+    std::vector<int64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), (int64_t)0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t i, int64_t j) {
+        if (case_[i] != case_[j]) return case_[i] < case_[j];
+        return ts[i] < ts[j];
+    });
+    for (int64_t k = 0; k < n;) {
+        int64_t e = k;
+        while (e + 1 < n && case_[idx[e + 1]] == case_[idx[k]]) ++e;
+        for (int64_t x = k; x <= e; ++x)
+            for (int64_t y = x + 1; y <= e; ++y) {
+                const size_t ed = (size_t)act[idx[x]] * A + act[idx[y]];
+                const uint64_t d = (uint64_t)ts[idx[y]] - (uint64_t)ts[idx[x]];
+                c[ed] += 1;
+                sm[ed] += d;
+                q[ed] += (unsigned __int128)d * d;
+            }
+        k = e + 1;
+    }
+    for (size_t ed = 0; ed < AA; ++ed) {
+        if (cnt) cnt[ed] = c[ed];
+        if (sum) sum[ed] = sm[ed];
+        if (sq_lo) sq_lo[ed] = (uint64_t)q[ed];
+        if (sq_hi) sq_hi[ed] = (uint64_t)(q[ed] >> 64);
+        double mu = 0.0, sd = 0.0;
+        if (c[ed] > 0) {
+            const double m = (double)c[ed];
+            mu = (double)sm[ed] / m;
+            const double s2 = (double)(uint64_t)(q[ed] >> 64) * 18446744073709551616.0 + (double)(uint64_t)q[ed];
+            const double V = (s2 - (double)sm[ed] * mu) / m;
+            sd = V > 0.0 ? std::sqrt(V) : 0.0;
+        }
+        if (mean) mean[ed] = mu;
+        if (stdev) stdev[ed] = sd;
+    }
 }
 
 }  // extern "C"

@@ -103,3 +103,56 @@ def test_case_filter_partition_and_variant_subset():
         a = oracle.filter_cases(case, act, ts, kind, keep=True, **kw)
         b = oracle.filter_cases(case, act, ts, kind, keep=False, **kw)
         assert (a ^ b).all()
+
+
+# ------------------------------------------------------------------ NEXT-3: EFG + temporal profile
+def test_l1_efg(l1):
+    case, act, ts, A = _l1(l1)
+    ex = l1["expected"]
+    e = oracle.efg(case, act, ts, A)
+    want = np.zeros((A, A), np.uint64)
+    for a, b, k in ex["efg_count"]["value"]:
+        want[a, b] = k
+    assert (e["cnt"] == want).all()
+    assert int(e["sum"][0, 2]) == ex["efg_sum_AC"]["value"]
+    mu, sd = ex["temporal_profile_AC"]["value"]
+    assert round(float(e["mean"][0, 2]), 2) == mu and round(float(e["stdev"][0, 2]), 2) == sd
+    assert int(e["sq_lo"][0, 2]) == 20**2 + 10**2 + 100**2 and int(e["sq_hi"][0, 2]) == 0
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_efg_o1_equals_o2_random(seed):
+    """Exact count / sum / sumsq against per-trace enumeration; the R22 stdev
+    against statistics.pstdev of the enumerated durations; S:328 invariant."""
+    import statistics
+    case, act, ts, A, _ = random_log(2000 + seed)
+    e = oracle.efg(case, act, ts, A)
+    b = brute.efg(case, act, ts)
+    for (x, y), ds in b.items():
+        assert int(e["cnt"][x, y]) == len(ds)
+        assert int(e["sum"][x, y]) == sum(ds) % (1 << 64)
+        assert int(e["sq_lo"][x, y]) + (int(e["sq_hi"][x, y]) << 64) == sum(d * d for d in ds) % (1 << 128)
+        sd = statistics.pstdev(ds)
+        mu = statistics.fmean(ds)
+        assert e["mean"][x, y] == pytest.approx(mu, rel=1e-12)
+        if sd > 1e-6 * max(mu, 1.0):            # well-conditioned: the formula is accurate
+            assert e["stdev"][x, y] == pytest.approx(sd, rel=1e-6)
+    assert int(e["cnt"].sum()) == sum(len(ds) for ds in b.values())
+    per = {}
+    for c in case:
+        per[c] = per.get(c, 0) + 1
+    assert int(e["cnt"].sum()) == sum(m * (m - 1) // 2 for m in per.values())    # S:328
+
+
+def test_efg_huge_durations_exact_128():
+    """d up to ~2^62: d^2 needs the high word; sums wrap modulo 2^64 (R8)."""
+    case = [0, 0, 0, 1, 1]
+    act = [0, 1, 1, 0, 1]
+    ts = [-(2**61), 0, 2**61, 5, 7]
+    e = oracle.efg(case, act, ts, 2)
+    ds = [2**61, 2**62, 2**61, 2]                    # (0,1) pairs: 0->1 (x2 in case 0) and case 1
+    q = sum(d * d for d in ds[:2] + [2])
+    assert int(e["cnt"][0, 1]) == 3
+    assert int(e["sq_lo"][0, 1]) + (int(e["sq_hi"][0, 1]) << 64) == q
+    assert int(e["sum"][0, 1]) == (2**61 + 2**62 + 2) % (1 << 64)
+    assert int(e["cnt"][1, 1]) == 1 and int(e["sq_hi"][1, 1]) == (2**61) ** 2 >> 64
