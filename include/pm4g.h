@@ -152,6 +152,19 @@ pm4g_status pm4g_dfg(const pm4g_log* log, uint64_t* cnt, int64_t* dur_sum, doubl
 pm4g_status pm4g_dfg_minmax(const pm4g_log* log, uint64_t* dur_min, uint64_t* dur_max,
                             pm4g_comm* comm, pm4g_stream_t stream);
 
+/* Eventually-follows graph + temporal profile (P:122
+ * "discovers the eventually-follows graphs or the temporal profile";
+ * S:284-291; reading R22).  For every case and every ordered row
+ * pair i < j inside it (O(sum m^2) pairs): cnt[a_i * A + a_j] += 1,
+ * dur_sum[..] += d (u64, modulo 2^64), dur_sumsq += d^2 as an exact unsigned
+ * 128-bit value, d = ts_j - ts_i >= 0.  dur_sumsq is [2*A*A]: low words at
+ * [0, A*A), high words at [A*A, 2*A*A).  mean = dur_sum / cnt and the
+ * population stdev per R22 (fp64, identical formula to the oracle's); 0 where
+ * cnt = 0.  Any output may be NULL (at least one required).  With comm: summed
+ * over ranks (the 128-bit words as four 32-bit limbs, exact). */
+pm4g_status pm4g_efg(const pm4g_log* log, uint64_t* cnt, uint64_t* dur_sum, uint64_t* dur_sumsq,
+                     double* mean, double* stdev, pm4g_comm* comm, pm4g_stream_t stream);
+
 /* Start / end activities: start[a] = number of cases whose
  * first formatted row has activity a; end[a] likewise for the last row.
  * Sum start = sum end = n_cases.  start, end: device [A]. */

@@ -82,6 +82,7 @@ _SIGS = {
     "pm4g_dfg": ([P, P, P, P, P, P], I32),
     "pm4g_start_end": ([P, P, P, P, P], I32),
     "pm4g_dfg_minmax": ([P, P, P, P, P], I32),
+    "pm4g_efg": ([P, P, P, P, P, P, P, P], I32),
     "pm4g_case_durations": ([P, P, P, P, U64, ctypes.POINTER(U64), P], I32),
     "pm4g_variants": ([P, P, P, ctypes.POINTER(P)], I32),
     "pm4g_variants_size": ([P, ctypes.POINTER(U64), ctypes.POINTER(U64)], I32),
@@ -246,6 +247,21 @@ class Log:
         mx = torch.empty(A * A, dtype=torch.int64, device=dev)
         _check(lib().pm4g_dfg_minmax(self.h, _ptr(mn), _ptr(mx), _comm(comm), _stream(stream)))
         return mn.view(A, A), mx.view(A, A)
+
+    def efg(self, comm=None, stream=None):
+        """NEXT-3: eventually-follows graph + temporal profile.  Returns a dict of
+        [A, A] tensors: cnt, sum (u64 as int64), sumsq_lo / sumsq_hi (the u128
+        sum of squared durations), mean, stdev."""
+        A, dev = self.A, _dev()
+        cnt = torch.empty(A * A, dtype=torch.int64, device=dev)
+        sm = torch.empty(A * A, dtype=torch.int64, device=dev)
+        sq = torch.empty(2 * A * A, dtype=torch.int64, device=dev)
+        mean = torch.empty(A * A, dtype=torch.float64, device=dev)
+        sd = torch.empty(A * A, dtype=torch.float64, device=dev)
+        _check(lib().pm4g_efg(self.h, _ptr(cnt), _ptr(sm), _ptr(sq), _ptr(mean), _ptr(sd), _comm(comm),
+                              _stream(stream)))
+        return {"cnt": cnt.view(A, A), "sum": sm.view(A, A), "sumsq_lo": sq[:A * A].view(A, A),
+                "sumsq_hi": sq[A * A:].view(A, A), "mean": mean.view(A, A), "stdev": sd.view(A, A)}
 
     def start_end(self, comm=None, stream=None):
         A, dev = self.A, _dev()

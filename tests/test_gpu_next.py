@@ -202,3 +202,52 @@ def test_variant_filter_random(seed):
     seqs = list(r.variants())[::2]
     _variant_check(case, act, ts, A, seqs, True, ncodes)
     _variant_check(case, act, ts, A, seqs, False, ncodes)
+
+
+# ------------------------------------------------------------------ NEXT-3: EFG + temporal profile
+def _check_efg(case, act, ts, A, ncodes=None):
+    log = _sorted_log(case, act, ts, A, ncodes)
+    g = log.efg()
+    r = oracle.efg(case, act, ts, A)
+    for k_gpu, k_ref in (("cnt", "cnt"), ("sum", "sum"), ("sumsq_lo", "sq_lo"), ("sumsq_hi", "sq_hi")):
+        assert np.array_equal(_u64(g[k_gpu]), r[k_ref].reshape(-1)), k_gpu
+    # R22: same IEEE operations on both sides -> identical doubles
+    assert np.array_equal(g["mean"].cpu().numpy().reshape(-1), r["mean"].reshape(-1))
+    assert np.array_equal(g["stdev"].cpu().numpy().reshape(-1), r["stdev"].reshape(-1))
+    log.close()
+
+
+def test_efg_l1(l1):
+    rows = l1["rows_ingest_order"]
+    _check_efg(rows["case"], rows["act"], rows["ts"], 3, 3)
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 2))
+def test_efg_random(seed):
+    case, act, ts, A, ncodes = random_log(seed)
+    _check_efg(case, act, ts, A, ncodes)
+
+
+@pytest.mark.parametrize("name", ["tiny", "roadtraffic", "bpic2019"])
+def test_efg_configs(name):
+    L = generate(CONFIGS[name])
+    _check_efg(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities, L.n_case_codes)
+
+
+@pytest.mark.parametrize("A", [72, 256, 300])
+def test_efg_hash_mode_long_cases_wide_gaps(A):
+    """A > 71: hash tables; gaps >= 2^32: the global 128-bit path; a 3000-event
+    case makes an unstaged tile walked case by case from global memory."""
+    rng = np.random.default_rng(A + 1)
+    lens = rng.integers(1, 20, 1500)
+    case = np.repeat(np.arange(1500, dtype=np.int64), lens)
+    act = rng.integers(0, A, case.size)
+    gaps = np.where(rng.random(case.size) < 0.05, rng.integers(2**32, 2**34, case.size),
+                    rng.integers(0, 10**6, case.size))
+    ts = np.cumsum(gaps).astype(np.int64)
+    big = 3000
+    case = np.concatenate([case, np.full(big, 1500)])
+    act = np.concatenate([act, rng.integers(0, 4, big)])
+    ts = np.concatenate([ts, rng.integers(0, 2**40, big)])
+    p = rng.permutation(case.size)
+    _check_efg(case[p], act[p], ts[p], A, 1501)

@@ -9,7 +9,8 @@ Times, with CUDA events on the launching stream after warm-up:
   * pm4g_dfg_minmax alone;
   * every NEXT-1 whole-case filter (START_IN, END_IN, SIZE, THROUGHPUT, PATHS)
     and filter_variants (top-10 variants), output log included;
-  * for reference, the A10 case-level time filter on the same formatted log.
+  * for reference, the A10 case-level time filter on the same formatted log;
+  * NEXT-3 efg (eventually-follows graph + temporal profile) with its pair count.
 Prints one JSON object per line: {"op", "ms", "events", "G_events_per_s", ...}.
 """
 from __future__ import annotations
@@ -67,6 +68,14 @@ def main():
     emit("analyze", timed(lambda: analyze(False), args.reps))
     emit("analyze+minmax", timed(lambda: analyze(True), args.reps))
     emit("dfg_minmax", timed(lambda: log.dfg_minmax(), args.reps))
+
+    # EFG: pairs = sum over cases of m (m - 1) / 2
+    C = log.info().n_cases
+    cc, ne, du = log.case_durations()
+    m = ne[:C].to(torch.int64)
+    pairs = int((m * (m - 1) // 2).sum())
+    ms = timed(lambda: log.efg(), max(3, args.reps // 2), warm=2)
+    emit("efg + temporal profile", ms, pairs=pairs, G_pairs_per_s=round(pairs / (ms / 1e3) / 1e9, 3))
 
     vt = log.variants()
     d = vt.as_dict()
