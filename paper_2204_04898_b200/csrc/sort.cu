@@ -110,8 +110,10 @@ struct PassArgs {
 
 // Shared-memory layout of one tile (all offsets multiples of 16):
 //   u_case[T] u_ts[T] (FROM_COLS) | u_key[T];  u_idx[T];  u_act[T]  -- as loaded
-//   s_src[T]                      -- slot (in the loaded tile) of the i-th key in digit order
-// (FROM_COLS keeps the built keys in u_key over the consumed u_ts.)
+//   v_act[T], v_idx[T] (WITH_IDX)  -- payloads in digit order
+// After ranking every key is in registers, so the keys are permuted IN PLACE
+// (u_key holds them in digit order for the write-out); payloads are copied to
+// v_*.  (FROM_COLS builds the keys over the consumed u_ts.)
 template <class P, bool FROM_COLS, bool WITH_IDX>
 struct OsLayout {
     static constexpr size_t T = SORT_TILE;
@@ -119,8 +121,9 @@ struct OsLayout {
     static constexpr size_t o_case = o_in + T * 8;                      // FROM_COLS only
     static constexpr size_t o_idx = o_case + (FROM_COLS ? T * 4 : 0);
     static constexpr size_t o_act = o_idx + (WITH_IDX ? T * 4 : 0);
-    static constexpr size_t o_src = (o_act + T * sizeof(P) + 15) / 16 * 16;
-    static constexpr size_t bytes = o_src + T * 2;
+    static constexpr size_t o_vidx = (o_act + T * sizeof(P) + 15) / 16 * 16;
+    static constexpr size_t o_vact = o_vidx + (WITH_IDX ? T * 4 : 0);
+    static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
 };
 
 template <class P, bool FROM_COLS, bool WITH_IDX>
@@ -132,9 +135,9 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
     uint32_t* u_idx = (uint32_t*)(smem + Lay::o_idx);
     P* u_act = (P*)(smem + Lay::o_act);
-    uint16_t* s_src = (uint16_t*)(smem + Lay::o_src);
+    uint32_t* v_idx = (uint32_t*)(smem + Lay::o_vidx);
+    P* v_act = (P*)(smem + Lay::o_vact);
     __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
-    __shared__ uint32_t s_start[RADIX];
     __shared__ long long s_gbase[RADIX];
     __shared__ uint32_t s_scan[SORT_WARPS + 1];
     __shared__ uint32_t s_tile;
@@ -153,6 +156,10 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
     const uint32_t dmask = (1u << a.bits) - 1;
     const bool gen_idx = WITH_IDX && a.in_idx == nullptr;
+    // digit of a key: shift < 64 except for a single-case log (no case bits)
+    const int sh = a.shift;
+    const bool sh_ok = sh < 64;
+    auto digit = [&](uint64_t k) -> uint32_t { return sh_ok ? (uint32_t)(k >> sh) & dmask : 0u; };
 
     // ---- tile load: TMA bulk copies for full aligned tiles, plain loads otherwise
     if (nvalid == SORT_TILE && a.aligned) {
@@ -186,8 +193,9 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
 
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
     // Peers (lanes holding the same digit) from one ballot per digit bit.
+    // dp[j] = digit << 16 | rank of the key among its warp's keys of that digit.
     uint64_t k[SORT_IPT];
-    uint32_t pos[SORT_IPT];
+    uint32_t dp[SORT_IPT];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
@@ -197,7 +205,7 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
                              : u_key[li];
         else
             k[j] = ~0ull;
-        const uint32_t d = li < nvalid ? (uint32_t)shr64(k[j], a.shift) & dmask : dmask;
+        const uint32_t d = li < nvalid ? digit(k[j]) : dmask;
         uint32_t peers = 0xffffffffu;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {   // bits above a.bits are 0 in every lane: no-ops
@@ -212,18 +220,12 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
             s_whist[warp][d] = bse + __popc(peers);
         }
         bse = __shfl_sync(0xffffffffu, bse, leader);
-        pos[j] = bse + __popc(peers & lt);
+        dp[j] = (d << 16) | (bse + __popc(peers & lt));
         __syncwarp();
     }
-    // FROM_COLS: the built keys replace the consumed timestamps in smem
-    if (FROM_COLS) {
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < SORT_IPT; ++j) u_key[warp * (32 * SORT_IPT) + j * 32 + lane] = k[j];
-    }
-    __syncthreads();
+    __syncthreads();   // every key is in registers: u_key may be overwritten
 
-    // ---- per-digit totals and warp-exclusive prefixes (thread == digit, tid < 256)
+    // ---- per-digit totals; warp bases = tile-exclusive start + warp-exclusive prefix
     const int d = tid;
     const bool dig = tid < RADIX && d <= (int)dmask;
     uint32_t tot = 0;
@@ -246,16 +248,20 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
         }
     }
     const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, nullptr);
-    if (tid < RADIX) s_start[d] = start;
+    if (tid < RADIX) {
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; ++w) s_whist[w][d] += start;
+    }
     __syncthreads();
 
-    // ---- keys (and their source slot) into smem in digit order
+    // ---- keys in place, payloads to v_*, all in digit order
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
-        const uint32_t dd = li < nvalid ? (uint32_t)shr64(k[j], a.shift) & dmask : dmask;
-        const uint32_t p = pos[j] + s_start[dd] + s_whist[warp][dd];
-        s_src[p] = (uint16_t)li;
+        const uint32_t p = (dp[j] & 0xffffu) + s_whist[warp][dp[j] >> 16];
+        u_key[p] = k[j];
+        v_act[p] = u_act[li];
+        if (WITH_IDX) v_idx[p] = gen_idx ? (uint32_t)(base + li) : u_idx[li];
     }
 
     // ---- decoupled look-back for this digit, 4 predecessors per round trip
@@ -284,18 +290,16 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     }
     __syncthreads();
 
-    // ---- coalesced write-out: consecutive threads, consecutive positions;
-    // payloads are gathered from the loaded tile through s_src
+    // ---- coalesced write-out: consecutive threads, consecutive positions
 #pragma unroll 4
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t sidx = j * SORT_THREADS + tid;
         if (sidx < nvalid) {
-            const uint32_t src = s_src[sidx];
-            const uint64_t kk = u_key[src];
-            const long long g = s_gbase[(uint32_t)shr64(kk, a.shift) & dmask] + sidx;
+            const uint64_t kk = u_key[sidx];
+            const long long g = s_gbase[digit(kk)] + sidx;
             a.out_key[g] = kk;
-            a.out_act[g] = u_act[src];
-            if (WITH_IDX) a.out_idx[g] = gen_idx ? (uint32_t)(base + src) : u_idx[src];
+            a.out_act[g] = v_act[sidx];
+            if (WITH_IDX) a.out_idx[g] = v_idx[sidx];
         }
     }
 }
