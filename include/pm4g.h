@@ -208,9 +208,15 @@ pm4g_status pm4g_variants_case_index(const pm4g_variant_table* v, uint32_t* case
                                      pm4g_stream_t stream);
 pm4g_status pm4g_variants_destroy(pm4g_variant_table* v);
 
+/* Upper bound on n_cases known on the host without waiting for the device:
+ * min(n_events, case_max - case_min + 1) (0 for an empty log).  Any state. */
+pm4g_status pm4g_case_capacity(const pm4g_log* log, uint64_t* capacity);
+
 /* Fused pass: one read of the formatted log produces every requested output
  * (each pointer may be NULL to skip it; variants == NULL skips variants).
- * Same semantics as the separate calls above. */
+ * Same semantics as the separate calls above.  With capacity >=
+ * pm4g_case_capacity the call does not wait for the case count (entries past
+ * n_cases are left untouched); otherwise it synchronises to check it. */
 typedef struct pm4g_outputs {
     uint64_t* cnt;        /* [A*A] device */
     int64_t* dur_sum;     /* [A*A] device */

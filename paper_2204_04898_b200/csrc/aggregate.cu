@@ -108,7 +108,8 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
     uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
-    int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak) {
+    int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak,
+    uint32_t* __restrict__ cco, uint32_t case_min) {
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
     const bool tables = packed != nullptr;
@@ -198,7 +199,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                 // directly-follows pairs (r, r+1) of one case
                 for (uint32_t r = e0 + ct; r + 1 < e1; r += AGG_CONSUMERS) {
                     const uint64_t kk = K_at(r), kn = K_at(r + 1);
-                    if (shr64(kk, ts_bits) != shr64(kn, ts_bits)) continue;
+                    if (!same_case(kk, kn, ts_bits)) continue;
                     const uint32_t e = A_at(r) * A + A_at(r + 1);
                     const uint64_t d = kn - kk;
                     if (MODE == TAB_FULL) {
@@ -242,6 +243,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                     }
                 }
                 if (n_events) n_events[c] = l - f + 1;
+                if (cco) cco[c] = case_min + case32(K_at(f), ts_bits);
                 if (dur) dur[c] = (int64_t)(K_at(l) - K_at(f));
                 if (k1o) {
                     uint64_t h1 = 0, h2 = 0;
@@ -301,12 +303,12 @@ static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
     const double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
-                         (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0);
+                         (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0) + (o.case_code ? cap * 4.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
                 (k_aggregate<P, MODE, MM><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
                     o.tables ? o.packed : nullptr, o.mm, o.n_events, o.dur, o.k1, o.k2,
-                    debug_weak_hash() ? 1 : 0)));
+                    debug_weak_hash() ? 1 : 0, o.case_code, L->case_min)));
     return PM4G_OK;
 }
 
@@ -451,6 +453,12 @@ pm4g_status pm4g_dfg(const pm4g_log* L, uint64_t* cnt, int64_t* dur_sum, double*
     return finalize_tables(pk.as<uint64_t>(), L->A, cnt, dur_sum, mean, nullptr, nullptr, s);
 }
 
+pm4g_status pm4g_case_capacity(const pm4g_log* L, uint64_t* capacity) {
+    if (!L || !capacity) return fail(PM4G_EINVAL, "null argument");
+    *capacity = L->n > 0 ? std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1) : 0;
+    return PM4G_OK;
+}
+
 pm4g_status pm4g_dfg_minmax(const pm4g_log* L, uint64_t* dur_min, uint64_t* dur_max, pm4g_comm* comm,
                             pm4g_stream_t stream) {
     PM4G_TRY(require_sorted(L));
@@ -540,11 +548,12 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
     cudaStream_t s = (cudaStream_t)stream;
     const bool want_tables = out->cnt || out->dur_sum || out->mean || out->start || out->end;
     const bool want_cases = out->case_code || out->n_events || out->dur;
-    if (want_cases) {
+    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    // capacity >= the host-known bound on n_cases: no need to wait for the count
+    if (want_cases && out->capacity < cap) {
         PM4G_TRY(fetch_n_cases(L, s));
         if (out->capacity < (uint64_t)L->n_cases) return fail(PM4G_EINVAL, "capacity < n_cases");
     }
-    uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     Scratch pk(s), keys(s), mm(s);
     AggOut o;
     const bool want_mm = out->dur_min || out->dur_max;
@@ -562,14 +571,13 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
     }
     o.n_events = out->n_events;
     o.dur = out->dur;
+    o.case_code = out->case_code;
     if (out->variants) {
         PM4G_TRY(keys.alloc(std::max<uint64_t>(cap, 1) * 16));
         o.k1 = keys.as<uint64_t>();
         o.k2 = o.k1 + std::max<uint64_t>(cap, 1);
     }
     PM4G_TRY(aggregate(L, o, s));
-    if (out->case_code && L->n_cases > 0)
-        PM4G_CK(cudaMemcpyAsync(out->case_code, L->s_case_code, L->n_cases * 4, cudaMemcpyDeviceToDevice, s));
     if (want_tables || want_mm) {
         if (comm) PM4G_TRY(comm_allreduce_u64(comm, o.packed, packed_len(L->A), s));
         PM4G_TRY(finalize_tables(o.packed, L->A, out->cnt, out->dur_sum, out->mean, out->start,

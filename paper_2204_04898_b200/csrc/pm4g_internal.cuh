@@ -144,6 +144,14 @@ __host__ __device__ inline int bit_width_u64(uint64_t x) {
 #endif
 }
 __host__ __device__ inline uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0 : (x >> s); }
+// the case part of a composite key (case - case_min < 2^32) as one 32-bit word
+__host__ __device__ __forceinline__ uint32_t case32(uint64_t key, int ts_bits) {
+    return ts_bits >= 64 ? 0u : (uint32_t)(key >> ts_bits);
+}
+// two composite keys of the same case
+__host__ __device__ __forceinline__ bool same_case(uint64_t a, uint64_t b, int ts_bits) {
+    return ts_bits >= 64 || ((a ^ b) >> ts_bits) == 0;
+}
 __host__ __device__ inline uint64_t low_mask(int bits) {
     return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
 }
@@ -322,6 +330,7 @@ struct AggOut {
     uint64_t* packed = nullptr;   // [cnt A2 | sum A2 | start A | end A] (zeroed by caller)
     uint64_t* mm = nullptr;       // [min A2 | max A2] (caller sets min = ~0, max = 0); with packed only
     uint32_t* n_events = nullptr; // [n_cases]
+    uint32_t* case_code = nullptr; // [n_cases] (case_min + case part of the first key)
     int64_t* dur = nullptr;       // [n_cases]
     uint64_t* k1 = nullptr;       // [n_cases] variant keys
     uint64_t* k2 = nullptr;

@@ -461,23 +461,23 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             if (WI) s_idx[p] = a.gidx[base + p];
         }
     }
-    uint64_t prev_case = 0;
+    uint32_t prev_case = 0;
     {
         const int64_t pi = base + warp * (32 * FMT_IPT) - 1;
-        if (pi >= 0 && pi < a.n) prev_case = shr64(a.gkey[pi], tb);
+        if (pi >= 0 && pi < a.n) prev_case = case32(a.gkey[pi], tb);
     }
     __syncthreads();
     if (bulk) mbar_wait(&s_bar, 0);
     uint32_t ball[FMT_IPT], wc = 0;
     {
-        uint64_t prev = prev_case;
+        uint32_t prev = prev_case;
 #pragma unroll
         for (int j = 0; j < FMT_IPT; ++j) {
             const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
             const int64_t i = base + li;
             const bool ok = li < tn;
-            const uint64_t c = ok ? shr64(s_key[li], tb) : 0ull;
-            uint64_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+            const uint32_t c = ok ? case32(s_key[li], tb) : 0u;
+            uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
             if (lane == 0) pc = prev;
             prev = __shfl_sync(0xffffffffu, c, 31);
             ball[j] = __ballot_sync(0xffffffffu, ok && (i == 0 || c != pc));
@@ -535,11 +535,11 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         if (warp == 1) {   // how far the last case runs past the tile end
             int ext = 0;
             if (base + tn < a.n) {
-                const uint64_t last = shr64(s_key[lastp], tb);
+                const uint64_t last = s_key[lastp];
                 ext = -1;
                 for (int o = 0; o <= FMT_EXT; o += 32) {
                     const int64_t i = base + tn + o + lane;
-                    const bool stop = i >= a.n || shr64(a.gkey[i], tb) != last;
+                    const bool stop = i >= a.n || !same_case(a.gkey[i], last, tb);
                     const uint32_t bb = __ballot_sync(0xffffffffu, stop);
                     if (bb) {
                         const int e = o + __ffs(bb) - 1;
@@ -611,7 +611,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     for (uint32_t h = tid; h < H; h += FMT_THREADS) {
         const int hp = s_head[h];
         a.off[R0 + h] = (uint32_t)(base + hp);
-        a.case_code[R0 + h] = a.case_min + (uint32_t)shr64(s_key[hp], tb);
+        a.case_code[R0 + h] = a.case_min + case32(s_key[hp], tb);
     }
     if (tid < min(s_nbig, 16u)) a.big[atomicAdd(a.big_count, 1u)] = R0 + s_bigh[tid];
     if (tid == 0 && base + tn >= a.n) {
@@ -750,19 +750,19 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
     const int64_t wbase = (int64_t)tile * SEG_TILE + warp * (32 * SEG_IPT);
     const uint32_t lt = lanemask_lt();
     uint32_t ballots[SEG_IPT];
-    uint64_t cs[SEG_IPT];
-    uint64_t prev_last = 0;
+    uint32_t cs[SEG_IPT];
+    uint32_t prev_last = 0;
     {
         int64_t pi = wbase - 1;
-        if (pi >= 0 && pi < n) prev_last = shr64(key[pi], ts_bits);
+        if (pi >= 0 && pi < n) prev_last = case32(key[pi], ts_bits);
     }
     uint32_t wcount = 0;
 #pragma unroll
     for (int j = 0; j < SEG_IPT; ++j) {
         int64_t i = wbase + j * 32 + lane;
         bool ok = i < n;
-        uint64_t c = ok ? shr64(key[i], ts_bits) : 0;
-        uint64_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+        uint32_t c = ok ? case32(key[i], ts_bits) : 0u;
+        uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
         if (lane == 0) pc = prev_last;
         prev_last = __shfl_sync(0xffffffffu, c, 31);
         bool head = ok && (i == 0 || c != pc);
@@ -790,7 +790,7 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
         if (b & (1u << lane)) {
             uint32_t rk = r + __popc(b & lt);
             off[rk] = (uint32_t)i;
-            case_code[rk] = case_min + (uint32_t)cs[j];
+            case_code[rk] = case_min + cs[j];
         }
         r += __popc(b);
     }

@@ -83,6 +83,7 @@ _SIGS = {
     "pm4g_start_end": ([P, P, P, P, P], I32),
     "pm4g_dfg_minmax": ([P, P, P, P, P], I32),
     "pm4g_efg": ([P, P, P, P, P, P, P, P], I32),
+    "pm4g_case_capacity": ([P, ctypes.POINTER(U64)], I32),
     "pm4g_case_durations": ([P, P, P, P, U64, ctypes.POINTER(U64), P], I32),
     "pm4g_variants": ([P, P, P, ctypes.POINTER(P)], I32),
     "pm4g_variants_size": ([P, ctypes.POINTER(U64), ctypes.POINTER(U64)], I32),
@@ -286,34 +287,45 @@ class Log:
         _check(lib().pm4g_variants(self.h, _comm(comm), _stream(stream), ctypes.byref(out)))
         return VariantTable(out)
 
+    def case_capacity(self) -> int:
+        """Host-known upper bound on n_cases (no device synchronisation)."""
+        c = U64(0)
+        _check(lib().pm4g_case_capacity(self.h, ctypes.byref(c)))
+        return c.value
+
     def analyze(self, comm=None, stream=None, tables=True, cases=True, variants=True, out=None,
                 minmax=False):
-        """Fused pass.  ``out``: optional dict of preallocated tensors (reused across calls).
-        ``minmax``: also the per-edge min / max durations ("dur_min", "dur_max")."""
+        """Fused pass.  ``out``: optional dict of tensors, filled on first use and reused
+        by later calls (per-case arrays are sized by case_capacity(), valid up to
+        info().n_cases).  ``minmax``: also the per-edge min / max durations."""
         A, dev = self.A, _dev()
-        C = self.info().n_cases if cases else 0
-        o = dict(out or {})
+        C = self.case_capacity() if cases else 0
+        o = out if out is not None else {}
+        def need(k, size, dt):
+            if k not in o or o[k].numel() < size:
+                o[k] = torch.empty(size, dtype=dt, device=dev)
+        want = set()
         if tables:
-            o.setdefault("cnt", torch.empty(A * A, dtype=torch.int64, device=dev))
-            o.setdefault("dur_sum", torch.empty(A * A, dtype=torch.int64, device=dev))
-            o.setdefault("mean", torch.empty(A * A, dtype=torch.float64, device=dev))
-            o.setdefault("start", torch.empty(A, dtype=torch.int64, device=dev))
-            o.setdefault("end", torch.empty(A, dtype=torch.int64, device=dev))
+            for k, sz, dt in (("cnt", A * A, torch.int64), ("dur_sum", A * A, torch.int64),
+                              ("mean", A * A, torch.float64), ("start", A, torch.int64), ("end", A, torch.int64)):
+                need(k, sz, dt)
+                want.add(k)
         if minmax:
-            o.setdefault("dur_min", torch.empty(A * A, dtype=torch.int64, device=dev))
-            o.setdefault("dur_max", torch.empty(A * A, dtype=torch.int64, device=dev))
+            for k in ("dur_min", "dur_max"):
+                need(k, A * A, torch.int64)
+                want.add(k)
         if cases:
             for k, dt in (("case_code", torch.uint32), ("n_events", torch.uint32), ("dur", torch.int64)):
-                if k not in o or o[k].numel() < C:
-                    o[k] = torch.empty(C, dtype=dt, device=dev)
+                need(k, C, dt)
+                want.add(k)
         vh = ctypes.c_void_p()
-        g = lambda k: _ptr(o[k]) if k in o else None  # noqa: E731
+        g = lambda k: _ptr(o[k]) if k in want else None  # noqa: E731
         outs = pm4g_outputs(g("cnt"), g("dur_sum"), g("mean"), g("start"), g("end"),
                             g("case_code"), g("n_events"), g("dur"),
-                            min((o[k].numel() for k in ("case_code", "n_events", "dur") if k in o), default=0),
+                            min((o[k].numel() for k in ("case_code", "n_events", "dur") if k in want), default=0),
                             ctypes.pointer(vh) if variants else None, g("dur_min"), g("dur_max"))
         _check(lib().pm4g_analyze(self.h, ctypes.byref(outs), _comm(comm), _stream(stream)))
-        res = dict(o)
+        res = {k: o[k] for k in want}
         if variants:
             res["variants"] = VariantTable(vh)
         return res
