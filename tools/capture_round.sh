@@ -1,0 +1,12 @@
+set -x
+python -m paper_2204_04898_b200.build >/dev/null
+mkdir -p gpurun_out/prof
+export PYTHONPATH=.
+(nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,memory.total --format=csv,noheader; nproc; lscpu | grep -E "Model name|^CPU\(s\)") > gpurun_out/prof/host.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/prof/launch_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_" -c 40 -o gpurun_out/prof/full python tools/prof_step.py 100M 1 > gpurun_out/prof/full.log 2>&1
+timeout 600 python bench.py > gpurun_out/prof/bench.json 2> gpurun_out/prof/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/prof/bench_reference.json 2> gpurun_out/prof/bench_reference.err
+timeout 900 python bench.py --config 1B --filter --steps 5 --warmup 3 --cpu-cases 2000000 > gpurun_out/prof/bench_1B.json 2> gpurun_out/prof/bench_1B.err
+for c in tiny roadtraffic bpic2019; do timeout 300 python bench.py --config $c --steps 100 --warmup 10 --cpu-cases 300000 >> gpurun_out/prof/bench_small.jsonl 2>> gpurun_out/prof/bench_small.err; done
+ls -la gpurun_out/prof

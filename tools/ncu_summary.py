@@ -79,6 +79,8 @@ def launches_md(path):
         unit = d["Metric Unit"]
         ms = v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1e-6)
         k = base_name(d["Kernel Name"])
+        if not k.startswith("k_"):   # the workload generator's torch kernels are not part of the step
+            continue
         agg[k][0] += 1
         agg[k][1] += ms
     tot = sum(v[1] for v in agg.values())
@@ -110,7 +112,9 @@ def main():
         open(a.out + "_kernels.md", "w").write("\n".join(md) + "\n")
     if a.launches:
         md = [f"# Launch list (ncu gpu__time_duration.sum, --clock-control none): {a.config}", "",
-              "Cold-cache and serialised per launch: compare shares, not absolutes.", "", a.note, "",
+              "Cold-cache and serialised per launch: compare shares, not absolutes.  libpm4g kernels",
+              "only (k_*); the synthetic generator's torch kernels in the same process are excluded.", "",
+              a.note, "",
               launches_md(a.launches)]
         open(a.out + "_launches.md", "w").write("\n".join(md) + "\n")
     if traffic:
