@@ -167,11 +167,13 @@ def check_invariants(pm4g, case, act, ts, meta, comm, out, filt, dist, dev, keep
     return {"all": all(ok.values()), **ok}
 
 
-def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt: bool) -> dict:
+def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt: bool,
+                    n_total: int | None = None) -> dict:
     """The `config` object of the JSON line (shared by both arms)."""
     return {"workload": f"synthetic-{cfg}: {n_local:,} events / {cases:,} cases / {A} activities per GPU, "
                         f"fully shuffled rows (full radix sort)" + (", events-mode time filter" if filt else ""),
-            "events_per_gpu": n_local, "global_events": n_local * world, "parallelism": f"case-sharded x{world}",
+            "events_per_gpu": n_local, "global_events": n_total if n_total is not None else n_local * world,
+            "parallelism": f"case-sharded x{world}",
             "l2": "inputs (13 B/event) larger than L2; no flush needed",
             "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")}
 
@@ -313,7 +315,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    n_total = n_local * world
+    n_total = n_local
+    if dist:   # shards hold about, not exactly, the same number of events
+        t = torch.tensor([n_local], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        n_total = int(t.item())
     value = n_total * args.steps / (ms / 1e3)
 
     # ---------------- end to end through the C-ABI with host buffers
@@ -417,7 +423,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": workload_config(args.config, n_local, meta["case_hi"] - meta["case_lo"], meta["A"], world,
-                                      filt is not None),
+                                      filt is not None, n_total),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "verified": verified,
             "cpu_baseline": cpu,
             "hbm_pipeline": {"algorithmic_GB_per_step": step_bytes / args.steps / 1e9,

@@ -315,8 +315,11 @@ pm4g_status pm4g_comm_destroy(pm4g_comm* comm);
 /* Loopback merge for R shards held by ONE process on one device (the
  * fake-collective used to test the merge logic without NCCL): combines the
  * per-shard variant tables exactly as the NCCL path does after its allgather.
- * parts: host array of R variant tables computed on disjoint case ranges. */
-pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts,
+ * parts: host array of R variant tables computed on disjoint case ranges.
+ * local_part in [0, R): the merged table also carries the case -> variant
+ * index (pm4g_variants_case_index) of that part's cases, in the merged order --
+ * what every rank gets for its own cases from the NCCL path; -1: none. */
+pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts, int32_t local_part,
                                 pm4g_stream_t stream, pm4g_variant_table** out);
 /* Loopback sum of R packed integer tables (device [R][len] u64 -> [len]):
  * the reduction C1 performs over NVLink, for fake-collective tests. */

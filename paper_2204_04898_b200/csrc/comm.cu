@@ -120,7 +120,7 @@ pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* loca
     const int R = c->nranks;
     if (R == 1) {
         const pm4g_variant_table* parts[1] = {local};
-        return merge_variant_tables(parts, 1, s, out);
+        return merge_variant_tables(parts, 1, s, out, 0);
     }
     // sizes
     Scratch sz(s);
@@ -154,10 +154,12 @@ pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* loca
     if (r) return nccl_fail(r, "ncclAllGather(entries)");
     r = g_nccl.allGather(sa, ra, Tmax * 4, NCCL_UINT8, c->comm, s);
     if (r) return nccl_fail(r, "ncclAllGather(sequences)");
-    // unpack into R temporary tables and merge
+    // unpack into R temporary tables (this rank's own table is used as is, so
+    // its per-case index survives) and merge
     std::vector<pm4g_variant_table*> parts(R, nullptr);
     pm4g_status st = PM4G_OK;
     for (int i = 0; i < R && st == PM4G_OK; ++i) {
+        if (i == c->rank) continue;
         pm4g_variant_table* v = new pm4g_variant_table();
         v->stream = s;
         v->V = sizes[2 * i];
@@ -180,8 +182,13 @@ pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* loca
             if (e != cudaSuccess) st = cuda_fail(e, "k_unpack_entries");
         }
     }
-    if (st == PM4G_OK) st = merge_variant_tables(parts.data(), R, s, out);
-    for (auto* v : parts) free_variants(v);
+    if (st == PM4G_OK) {
+        std::vector<const pm4g_variant_table*> cparts(parts.begin(), parts.end());
+        cparts[c->rank] = local;
+        st = merge_variant_tables(cparts.data(), R, s, out, c->rank);
+    }
+    for (int i = 0; i < R; ++i)
+        if (i != c->rank) free_variants(parts[i]);
     return st;
 }
 

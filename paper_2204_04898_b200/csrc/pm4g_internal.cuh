@@ -347,7 +347,7 @@ pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int
 pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
                                           pm4g_variant_table** out);
 pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
-                                 pm4g_variant_table** out);
+                                 pm4g_variant_table** out, int local_part);
 void free_variants(pm4g_variant_table* v);
 
 }  // namespace pm4g

@@ -684,9 +684,20 @@ pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint
     }
 }
 
-// Merge R per-shard tables (disjoint case ranges): items = entries.
+// Merge R per-shard tables (disjoint case ranges): items = entries.  With
+// local_part >= 0, the merged table also carries the case -> variant index of
+// that part's cases: its local index composed with the merged position of the
+// part's entries (the merge groups entries, so entry i of part r lands at
+// item_out[offset_r + i]).
+__global__ void k_compose_case_variant(const uint32_t* __restrict__ local_cv, uint64_t C,
+                                       const uint32_t* __restrict__ item_out, uint64_t offset,
+                                       uint32_t* __restrict__ out) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < C; c += (uint64_t)gridDim.x * blockDim.x)
+        out[c] = item_out[offset + local_cv[c]];
+}
+
 pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
-                                 pm4g_variant_table** out) {
+                                 pm4g_variant_table** out, int local_part) {
     uint64_t V = 0, T = 0;
     for (int r = 0; r < n_parts; ++r) {
         V += parts[r]->V;
@@ -716,7 +727,28 @@ pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_p
         to += p->total_len;
     }
     PM4G_TRY(excl_scan_u32_to_u64(ln, so, (int64_t)V, s));
-    return build_variants<uint64_t, uint32_t>(V, k1, k2, so, sa, w, ord, 32, ord, false, s, out);
+    const pm4g_variant_table* lp = local_part >= 0 ? parts[local_part] : nullptr;
+    const bool compose = lp && lp->case_variant && lp->n_cases;
+    pm4g_variant_table* v = nullptr;
+    PM4G_TRY((build_variants<uint64_t, uint32_t>(V, k1, k2, so, sa, w, ord, 32, ord, compose, s, &v)));
+    if (compose) {   // v->case_variant holds item -> output for the V merged entries
+        uint64_t offset = 0;
+        for (int r = 0; r < local_part; ++r) offset += parts[r]->V;
+        uint32_t* cv = nullptr;
+        pm4g_status st = dalloc_t(&cv, std::max<uint64_t>(lp->n_cases, 1), s);
+        if (st) {
+            free_variants(v);
+            return st;
+        }
+        PM4G_LAUNCH("k_compose_case_variant", lp->n_cases * 12.0, s,
+                    (k_compose_case_variant<<<gsz(lp->n_cases), 256, 0, s>>>(lp->case_variant, lp->n_cases,
+                                                                             v->case_variant, offset, cv)));
+        dfree(v->case_variant, s);
+        v->case_variant = cv;
+        v->n_cases = lp->n_cases;
+    }
+    *out = v;
+    return PM4G_OK;
 }
 
 }  // namespace pm4g
@@ -765,13 +797,13 @@ pm4g_status pm4g_variants_destroy(pm4g_variant_table* v) {
     return PM4G_OK;
 }
 
-pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts,
+pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts, int32_t local_part,
                                 pm4g_stream_t stream, pm4g_variant_table** out) {
-    if (!parts || n_parts <= 0 || !out) return fail(PM4G_EINVAL, "bad arguments");
+    if (!parts || n_parts <= 0 || !out || local_part >= n_parts) return fail(PM4G_EINVAL, "bad arguments");
     for (int i = 0; i < n_parts; ++i)
         if (!parts[i]) return fail(PM4G_EINVAL, "null part");
     *out = nullptr;
-    return merge_variant_tables(parts, n_parts, (cudaStream_t)stream, out);
+    return merge_variant_tables(parts, n_parts, (cudaStream_t)stream, out, local_part < 0 ? -1 : local_part);
 }
 
 }  // extern "C"

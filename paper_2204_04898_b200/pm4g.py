@@ -98,7 +98,7 @@ _SIGS = {
     "pm4g_comm_unique_id": ([P, ctypes.POINTER(ctypes.c_size_t)], I32),
     "pm4g_comm_create": ([P, I32, I32, ctypes.POINTER(P)], I32),
     "pm4g_comm_destroy": ([P], I32),
-    "pm4g_variants_merge": ([ctypes.POINTER(P), I32, P, ctypes.POINTER(P)], I32),
+    "pm4g_variants_merge": ([ctypes.POINTER(P), I32, I32, P, ctypes.POINTER(P)], I32),
     "pm4g_sum_u64": ([P, I32, U64, P, P], I32),
     "pm4g_tables_partial": ([P, P, P], I32),
     "pm4g_tables_finalize": ([P, U32, P, P, P, P, P, P], I32),
@@ -425,10 +425,10 @@ class VariantTable:
         return {tuple(acts[off[i]:off[i + 1]]): cnt[i] for i in range(len(cnt))}
 
 
-def pm4g_variants_merge(parts: list, stream=None) -> VariantTable:
+def pm4g_variants_merge(parts: list, local_part: int = -1, stream=None) -> VariantTable:
     arr = (P * len(parts))(*[p.h for p in parts])
     out = ctypes.c_void_p()
-    _check(lib().pm4g_variants_merge(arr, len(parts), _stream(stream), ctypes.byref(out)))
+    _check(lib().pm4g_variants_merge(arr, len(parts), int(local_part), _stream(stream), ctypes.byref(out)))
     return VariantTable(out)
 
 

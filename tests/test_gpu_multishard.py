@@ -56,6 +56,14 @@ def test_sharded_merge_equals_whole(name, R):
     cc = np.concatenate([lg.case_durations()[0].cpu().numpy() for lg in logs])
     du = np.concatenate([lg.case_durations()[2].cpu().numpy() for lg in logs])
     assert np.array_equal(cc, full.case_code) and np.array_equal(du, full.dur)
+    # what each rank gets for its own cases from the NCCL path: the global variant
+    # index of every local case (merge with local_part = rank)
+    cv = []
+    for r, lg in enumerate(logs):
+        mr = pm4g.pm4g_variants_merge(parts, local_part=r)
+        cv.append(mr.case_index(lg.info().n_cases).cpu().numpy())
+        mr.close()
+    assert np.array_equal(np.concatenate(cv), full.case_variant)
 
 
 def test_weak_hash_cross_shard_merge(monkeypatch):
@@ -80,5 +88,7 @@ def test_world_one_communicator_path():
     v = o["variants"].as_dict()
     full = oracle.run(L.case.numpy(), L.act.numpy(), L.ts.numpy(), spec.n_activities)
     assert v == full.variants()
+    ci = o["variants"].case_index(log.info().n_cases).cpu().numpy()
+    assert np.array_equal(ci, full.case_variant)
     assert np.array_equal(o["cnt"].cpu().numpy().view(np.uint64).reshape(full.cnt.shape), full.cnt)
     comm.close()
