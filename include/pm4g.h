@@ -312,6 +312,32 @@ pm4g_status pm4g_comm_unique_id(void* id_out, size_t* id_bytes); /* id_out: host
 pm4g_status pm4g_comm_create(const void* id, int32_t nranks, int32_t rank, pm4g_comm** out);
 pm4g_status pm4g_comm_destroy(pm4g_comm* comm);
 
+/* ---------------------------------------------------------------- global repartition (NEXT-4)
+ * a single unsorted global table, ingested in arbitrary
+ * row slices on the ranks (the log as a columnar table), is moved so
+ * that rank r holds exactly the rows with bounds[r] <= case < bounds[r + 1]
+ * (contiguous case ranges, R19).  Rows arrive in (source rank, row)
+ * order, so the destination's ingest order is the global table's order
+ * restricted to its cases (the stable tie-break of R2 is preserved).
+ * bounds: HOST u32[nranks + 1], ascending, covering every case code of the
+ * input (EINVAL otherwise), bounds[nranks] <= n_case_codes.  `in` must be
+ * ingested (not sorted).  Every column (activity, timestamp, extra columns) is
+ * exchanged with grouped ncclSend / ncclRecv; the result is a new ingested
+ * log with case range [bounds[rank], bounds[rank + 1]), validated. */
+pm4g_status pm4g_repartition(const pm4g_log* in, const uint32_t* bounds, pm4g_comm* comm,
+                             pm4g_stream_t stream, pm4g_log** out);
+/* The same data movement on one device: parts[r] (r < n_parts) receives the
+ * rows of `in` with bounds[r] <= case < bounds[r + 1], in their original order
+ * (a stable split), as a new ingested log with case range [bounds[r],
+ * bounds[r + 1]).  parts: host array of n_parts out-pointers. */
+pm4g_status pm4g_partition_by_case(const pm4g_log* in, const uint32_t* bounds, int32_t n_parts,
+                                   pm4g_stream_t stream, pm4g_log** parts);
+/* Concatenation of ingested logs (same activity dictionary and columns) in the
+ * given order -- what a rank holds after the exchange -- as a new ingested log
+ * with case range [case_lo, case_hi), validated. */
+pm4g_status pm4g_log_concat(const pm4g_log* const* logs, int32_t n_logs, uint32_t case_lo, uint32_t case_hi,
+                            pm4g_stream_t stream, pm4g_log** out);
+
 /* Loopback merge for R shards held by ONE process on one device (the
  * fake-collective used to test the merge logic without NCCL): combines the
  * per-shard variant tables exactly as the NCCL path does after its allgather.

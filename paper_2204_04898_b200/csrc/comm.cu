@@ -36,6 +36,10 @@ struct NcclApi {
     NcclResult (*commDestroy)(NcclComm) = nullptr;
     NcclResult (*allReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
     NcclResult (*allGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t) = nullptr;
+    NcclResult (*send)(const void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    NcclResult (*recv)(void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    NcclResult (*groupStart)() = nullptr;
+    NcclResult (*groupEnd)() = nullptr;
     const char* (*getErrorString)(NcclResult) = nullptr;
 };
 
@@ -55,8 +59,12 @@ static pm4g_status load_nccl() {
     g_nccl.allReduce = (NcclResult(*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllReduce");
     g_nccl.allGather = (NcclResult(*)(const void*, void*, size_t, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllGather");
     g_nccl.getErrorString = (const char* (*)(NcclResult))dlsym(h, "ncclGetErrorString");
+    g_nccl.send = (NcclResult(*)(const void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclSend");
+    g_nccl.recv = (NcclResult(*)(void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclRecv");
+    g_nccl.groupStart = (NcclResult(*)())dlsym(h, "ncclGroupStart");
+    g_nccl.groupEnd = (NcclResult(*)())dlsym(h, "ncclGroupEnd");
     if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.allReduce ||
-        !g_nccl.allGather) {
+        !g_nccl.allGather || !g_nccl.send || !g_nccl.recv || !g_nccl.groupStart || !g_nccl.groupEnd) {
         g_nccl = NcclApi();
         return fail(PM4G_ENCCL, "NCCL symbols missing");
     }
@@ -247,6 +255,61 @@ pm4g_status pm4g_comm_destroy(pm4g_comm* c) {
     if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
     delete c;
     return PM4G_OK;
+}
+
+pm4g_status pm4g_repartition(const pm4g_log* in, const uint32_t* bounds, pm4g_comm* c, pm4g_stream_t stream,
+                             pm4g_log** out) {
+    if (!in || !bounds || !c || !out) return fail(PM4G_EINVAL, "bad arguments");
+    *out = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int R = c->nranks, me = c->rank;
+    PartitionedRows pr(s);
+    PM4G_TRY(partition_rows(in, bounds, R, s, &pr));
+    // counts matrix M[src][dst] through one allgather
+    std::vector<uint64_t> M((size_t)R * R, 0);
+    if (R == 1) {
+        M[0] = pr.counts[0];
+    } else {
+        Scratch cb(s);
+        PM4G_TRY(cb.alloc((size_t)R * (R + 1) * 8));
+        uint64_t* d_all = cb.as<uint64_t>();
+        uint64_t* d_mine = d_all + (size_t)R * R;
+        PM4G_CK(cudaMemcpyAsync(d_mine, pr.counts.data(), R * 8, cudaMemcpyHostToDevice, s));
+        NcclResult r = g_nccl.allGather(d_mine, d_all, R, NCCL_UINT64, c->comm, s);
+        if (r) return nccl_fail(r, "ncclAllGather(counts)");
+        PM4G_CK(cudaMemcpyAsync(M.data(), d_all, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaStreamSynchronize(s));
+    }
+    std::vector<uint64_t> soff(R, 0), roff(R, 0);
+    uint64_t n_recv = 0;
+    for (int p = 0; p < R; ++p) {
+        soff[p] = p ? soff[p - 1] + M[(size_t)me * R + p - 1] : 0;
+        roff[p] = n_recv;
+        n_recv += M[(size_t)p * R + me];
+    }
+    if (n_recv > (uint64_t)ST_VAL) return fail(PM4G_EINVAL, "a destination shard exceeds 2^30-1 events");
+    auto fill = [&](const std::vector<void*>& dst) -> pm4g_status {
+        if (R == 1) {
+            for (size_t k = 0; k < dst.size(); ++k)
+                if (n_recv) PM4G_CK(cudaMemcpyAsync(dst[k], pr.cols[k], n_recv * pr.elems[k], cudaMemcpyDeviceToDevice, s));
+            return PM4G_OK;
+        }
+        // one NCCL group: every column to / from every peer (self included)
+        NcclResult r = g_nccl.groupStart();
+        for (size_t k = 0; k < dst.size() && !r; ++k) {
+            const int e = pr.elems[k];
+            for (int p = 0; p < R && !r; ++p) {
+                const uint64_t ns = M[(size_t)me * R + p], nr = M[(size_t)p * R + me];
+                if (ns) r = g_nccl.send((char*)pr.cols[k] + soff[p] * e, ns * e, NCCL_UINT8, p, c->comm, s);
+                if (!r && nr) r = g_nccl.recv((char*)dst[k] + roff[p] * e, nr * e, NCCL_UINT8, p, c->comm, s);
+            }
+        }
+        NcclResult r2 = g_nccl.groupEnd();
+        if (r) return nccl_fail(r, "ncclSend/ncclRecv");
+        if (r2) return nccl_fail(r2, "ncclGroupEnd");
+        return PM4G_OK;
+    };
+    return make_ingested_log(in, (int64_t)n_recv, bounds[me], bounds[me + 1], fill, s, out);
 }
 
 pm4g_status pm4g_sum_u64(const uint64_t* parts, int32_t n_parts, uint64_t len, uint64_t* out,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -346,6 +347,21 @@ enum { COMM_SUM = 0, COMM_MAX = 2, COMM_MIN = 3 };   // ncclRedOp_t values
 pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int op, cudaStream_t s);
 pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
                                           pm4g_variant_table** out);
+// NEXT-4 repartition (repartition.cu): rows of an ingested log grouped by
+// destination rank, every column gathered into one buffer (dest-major)
+struct PartitionedRows {
+    Scratch buf;
+    std::vector<void*> cols;          // per column: [n] rows, destination-major
+    std::vector<int> elems;           // bytes per element
+    std::vector<uint64_t> counts;     // rows per destination
+    explicit PartitionedRows(cudaStream_t s) : buf(s) {}
+};
+void log_columns(const pm4g_log* L, std::vector<const void*>* cols, std::vector<int>* elems);
+pm4g_status partition_rows(const pm4g_log* in, const uint32_t* bounds, int R, cudaStream_t s, PartitionedRows* out);
+pm4g_status make_ingested_log(const pm4g_log* like, int64_t n, uint32_t case_lo, uint32_t case_hi,
+                              const std::function<pm4g_status(const std::vector<void*>&)>& fill, cudaStream_t s,
+                              pm4g_log** out);
+
 pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
                                  pm4g_variant_table** out, int local_part);
 void free_variants(pm4g_variant_table* v);

@@ -84,6 +84,9 @@ _SIGS = {
     "pm4g_dfg_minmax": ([P, P, P, P, P], I32),
     "pm4g_efg": ([P, P, P, P, P, P, P, P], I32),
     "pm4g_case_capacity": ([P, ctypes.POINTER(U64)], I32),
+    "pm4g_repartition": ([P, P, P, P, ctypes.POINTER(P)], I32),
+    "pm4g_partition_by_case": ([P, P, I32, P, ctypes.POINTER(P)], I32),
+    "pm4g_log_concat": ([ctypes.POINTER(P), I32, U32, U32, P, ctypes.POINTER(P)], I32),
     "pm4g_case_durations": ([P, P, P, P, U64, ctypes.POINTER(U64), P], I32),
     "pm4g_variants": ([P, P, P, ctypes.POINTER(P)], I32),
     "pm4g_variants_size": ([P, ctypes.POINTER(U64), ctypes.POINTER(U64)], I32),
@@ -351,6 +354,23 @@ class Log:
                                       1 if keep else 0, _stream(stream), ctypes.byref(out)))
         return Log(out, self.A, self.act_bytes)
 
+    def repartition(self, bounds, comm, stream=None) -> "Log":
+        """NEXT-4: all-to-all by case range over NCCL; this rank receives the rows with
+        bounds[rank] <= case < bounds[rank + 1] of every rank's (ingested) log."""
+        arr = (U32 * len(bounds))(*[int(b) for b in bounds])
+        out = ctypes.c_void_p()
+        _check(lib().pm4g_repartition(self.h, ctypes.cast(arr, P), _comm(comm), _stream(stream), ctypes.byref(out)))
+        return Log(out, self.A, self.act_bytes)
+
+    def partition_by_case(self, bounds, stream=None) -> list:
+        """The same split on one device: one new ingested log per case range."""
+        R = len(bounds) - 1
+        arr = (U32 * len(bounds))(*[int(b) for b in bounds])
+        outs = (P * R)()
+        _check(lib().pm4g_partition_by_case(self.h, ctypes.cast(arr, P), R, _stream(stream),
+                                            ctypes.cast(outs, ctypes.POINTER(P))))
+        return [Log(ctypes.c_void_p(outs[i]), self.A, self.act_bytes) for i in range(R)]
+
     def filter_cases(self, kind: int, codes=None, lo: int = 0, hi: int = 0, keep: bool = True,
                      stream=None) -> "Log":
         """NEXT-1 whole-case filter (formatted log): PM4G_CASE_START_IN / END_IN (codes),
@@ -430,6 +450,14 @@ def pm4g_variants_merge(parts: list, local_part: int = -1, stream=None) -> Varia
     out = ctypes.c_void_p()
     _check(lib().pm4g_variants_merge(arr, len(parts), int(local_part), _stream(stream), ctypes.byref(out)))
     return VariantTable(out)
+
+
+def pm4g_log_concat(logs: list, case_lo: int, case_hi: int, stream=None) -> Log:
+    """Concatenate ingested logs (in order) into one log with case range [case_lo, case_hi)."""
+    arr = (P * len(logs))(*[lg.h for lg in logs])
+    out = ctypes.c_void_p()
+    _check(lib().pm4g_log_concat(arr, len(logs), int(case_lo), int(case_hi), _stream(stream), ctypes.byref(out)))
+    return Log(out, logs[0].A, logs[0].act_bytes)
 
 
 def pm4g_sum_u64(parts: torch.Tensor, stream=None) -> torch.Tensor:
@@ -533,3 +561,10 @@ pm4g_variants = Log.variants
 pm4g_analyze = Log.analyze
 pm4g_filter_time = Log.filter_time
 pm4g_filter_attr = Log.filter_attr
+pm4g_filter_cases = Log.filter_cases
+pm4g_filter_variants = Log.filter_variants
+pm4g_dfg_minmax = Log.dfg_minmax
+pm4g_efg = Log.efg
+pm4g_repartition = Log.repartition
+pm4g_partition_by_case = Log.partition_by_case
+pm4g_case_capacity = Log.case_capacity

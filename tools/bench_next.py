@@ -51,15 +51,59 @@ def main():
     spec = CONFIGS[args.config]
     L = generate(spec, device="cuda")
     act = L.act.to(torch.uint8 if spec.n_activities <= 256 else torch.int16)
-    log = pm4g.pm4g_log_create(L.case.to(torch.uint32), act, L.ts, spec.n_activities,
+    case32 = L.case.to(torch.uint32)
+    log = pm4g.pm4g_log_create(case32, act, L.ts, spec.n_activities,
                                n_case_codes=spec.n_cases, borrow=True)
-    log.sort()
     n = log.n
-    torch.cuda.synchronize()
 
     def emit(op, ms, **kw):
         print(json.dumps({"op": op, "config": args.config, "ms": round(ms, 4), "events": n,
                           "G_events_per_s": round(n / (ms / 1e3) / 1e9, 3), **kw}), flush=True)
+
+    # NEXT-4 on the ingested log: the 8-way case-range split (an all-to-all's send
+    # side) and the concatenation a destination performs; and Parquet ingest
+    R = 8
+    bounds = [spec.n_cases * r // R for r in range(R + 1)]
+
+    def split():
+        for p in log.partition_by_case(bounds):
+            p.close()
+    emit("partition_by_case 8 ranges (NEXT-4)", timed(split, max(3, args.reps // 2), warm=1))
+    parts = log.partition_by_case(bounds)
+
+    def concat():
+        pm4g.pm4g_log_concat(parts, 0, spec.n_cases).close()
+    emit("log_concat 8 parts (NEXT-4)", timed(concat, max(3, args.reps // 2), warm=1))
+    for p in parts:
+        p.close()
+    try:
+        import tempfile
+        import time as _t
+        import pyarrow as pa
+        import pyarrow.parquet as pq
+        from paper_2204_04898_b200.io import read_parquet
+        m = min(n, 10_000_000)
+        tbl = pa.table({"case:concept:name": pa.array(L.case[:m].cpu().numpy()),
+                        "concept:name": pa.array(L.act[:m].cpu().numpy()),
+                        "time:timestamp": pa.array(L.ts[:m].cpu().numpy(), pa.timestamp("ms"))})
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "log.parquet")
+            pq.write_table(tbl, path)
+            read_parquet(path)[0].close()
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
+            lg = read_parquet(path)[0]
+            torch.cuda.synchronize()
+            dt = _t.perf_counter() - t0
+            lg.close()
+        print(json.dumps({"op": "read_parquet -> log (NEXT-4, host wall clock incl. parse + H2D + validate)",
+                          "config": args.config, "ms": round(dt * 1e3, 2), "events": m,
+                          "M_events_per_s": round(m / dt / 1e6, 1)}), flush=True)
+    except ImportError:
+        pass
+
+    log.sort()
+    torch.cuda.synchronize()
 
     def analyze(minmax):
         o = log.analyze(minmax=minmax)
