@@ -206,12 +206,18 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
         else
             k[j] = ~0ull;
         const uint32_t d = li < nvalid ? digit(k[j]) : dmask;
+        // peers = AND over digit bits of (ballot of lanes with the bit == my bit):
+        // the bit tested against a constant mask is the ballot predicate, and
+        // its sign-extended copy (0 or ~0) folds the choice into one 3-input op
         uint32_t peers = 0xffffffffu;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {   // bits above a.bits are 0 in every lane: no-ops
-            const bool bit = (d >> b) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
+            uint32_t bal, m;   // ballot of the bit, and the bit as 0 / ~0, from one predicate
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, -1, 0, p;\n}"
+                : "=r"(bal), "=r"(m)
+                : "r"(d), "r"(1u << b));
+            peers &= ~(bal ^ m);
         }
         const int leader = __ffs(peers) - 1;
         uint32_t bse = 0;
