@@ -126,7 +126,9 @@ struct OsLayout {
     static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
 };
 
-template <class P, bool FROM_COLS, bool WITH_IDX>
+// HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
+// the digits sit above ts_bits >= 32), extracted with one 32-bit shift
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI>
 __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
     using Lay = OsLayout<P, FROM_COLS, WITH_IDX>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -159,7 +161,11 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     // digit of a key: shift < 64 except for a single-case log (no case bits)
     const int sh = a.shift;
     const bool sh_ok = sh < 64;
-    auto digit = [&](uint64_t k) -> uint32_t { return sh_ok ? (uint32_t)(k >> sh) & dmask : 0u; };
+    const uint32_t shh = (uint32_t)(sh - 32);
+    auto digit = [&](uint64_t k) -> uint32_t {
+        if (HI) return ((uint32_t)(k >> 32) >> shh) & dmask;
+        return sh_ok ? (uint32_t)(k >> sh) & dmask : 0u;
+    };
 
     // ---- tile load: TMA bulk copies for full aligned tiles, plain loads otherwise
     if (nvalid == SORT_TILE && a.aligned) {
@@ -310,18 +316,25 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     }
 }
 
-template <class P, bool FC, bool WI>
-static pm4g_status launch_pass(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
-                               const char* name, double bytes) {
+template <class P, bool FC, bool WI, bool HI>
+static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
+                                 const char* name, double bytes) {
     const size_t smem = OsLayout<P, FC, WI>::bytes;
     static bool attr = false;
     if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_onesweep<P, FC, WI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PM4G_CK(cudaFuncSetAttribute(k_onesweep<P, FC, WI, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         attr = true;
     }
-    PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
+    PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI, HI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
     return PM4G_OK;
+}
+
+template <class P, bool FC, bool WI>
+static pm4g_status launch_pass(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
+                               const char* name, double bytes) {
+    if (args.shift >= 32 && args.shift < 64) return launch_pass_t<P, FC, WI, true>(args, tiles, s, name, bytes);
+    return launch_pass_t<P, FC, WI, false>(args, tiles, s, name, bytes);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
