@@ -206,12 +206,18 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
-        if (li < nvalid)
-            k[j] = FROM_COLS ? make_key(u_case[li] - a.kp.case_min, u_ts[li], a.kp.ts_min, a.kp.ts_bits)
-                             : u_key[li];
-        else
-            k[j] = ~0ull;
-        const uint32_t d = li < nvalid ? digit(k[j]) : dmask;
+        uint32_t d = dmask;
+        k[j] = ~0ull;
+        if (li < nvalid) {
+            if (FROM_COLS) {   // pass 0: its digit is the low bits of case - case_min (shift == ts_bits)
+                const uint32_t crel = u_case[li] - a.kp.case_min;
+                k[j] = make_key(crel, u_ts[li], a.kp.ts_min, a.kp.ts_bits);
+                d = crel & dmask;
+            } else {
+                k[j] = u_key[li];
+                d = digit(k[j]);
+            }
+        }
         // peers = AND over digit bits of (ballot of lanes with the bit == my bit):
         // the bit tested against a constant mask is the ballot predicate, and
         // its sign-extended copy (0 or ~0) folds the choice into one 3-input op
