@@ -98,18 +98,25 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload
-def make_shard(cfg: str, rank: int, world: int, device):
+def make_shard(cfg: str, rank: int, world: int, device, strong: bool = False):
+    """weak: each rank holds a full config-sized shard of a world x larger log;
+    strong: the config's log is split across the world by case range (R19)."""
     from gen.synth import CONFIGS
     from gen.synth import generate
+    from paper_2204_04898_b200.dist import shard_ranges
     base = CONFIGS[cfg]
-    spec = base.with_(n_cases=base.n_cases * world,
-                      n_events=None if base.n_events is None else base.n_events * world)
-    lo = rank * base.n_cases
-    L = generate(spec, lo, lo + base.n_cases, device=device)
+    if strong:
+        spec = base
+        lo, hi = shard_ranges(base.n_cases, world)[rank]
+    else:
+        spec = base.with_(n_cases=base.n_cases * world,
+                          n_events=None if base.n_events is None else base.n_events * world)
+        lo, hi = rank * base.n_cases, (rank + 1) * base.n_cases
+    L = generate(spec, lo, hi, device=device)
     case = L.case.to(torch.uint32)
     act = L.act.to(L.act_dtype()) if L.act_dtype() != torch.uint8 else L.act.to(torch.uint8)
     ts = L.ts.contiguous()
-    meta = dict(n_case_codes=L.n_case_codes, case_lo=lo, case_hi=lo + base.n_cases, A=L.n_activities)
+    meta = dict(n_case_codes=L.n_case_codes, case_lo=lo, case_hi=hi, A=L.n_activities)
     del L
     return case.contiguous(), act.contiguous(), ts, meta, spec
 
@@ -250,6 +257,12 @@ def main():
     ap.add_argument("--ref-cases", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stages", action="store_true", help="print the per-kernel table to stderr")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: a config-sized shard per GPU (default); strong: the config's log split across "
+                         "the GPUs (default for the 1B config, the north-star layout)")
+    ap.add_argument("--emulate", default=None, metavar="R/N",
+                    help="one GPU runs rank R's shard of an N-way split (per-GPU time of an N-GPU run, "
+                         "without the NCCL merge)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -271,7 +284,13 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = pm4g.pm4g_comm_create(uid[0], world, rank)
 
-    case, act, ts, meta, spec = make_shard(args.config, rank, world, dev)
+    scaling = args.scaling or ("strong" if args.config == "1B" else "weak")
+    shard_rank, shard_world = rank, world
+    if args.emulate:
+        if world != 1:
+            raise SystemExit("--emulate runs on one process")
+        shard_rank, shard_world = (int(x) for x in args.emulate.split("/"))
+    case, act, ts, meta, spec = make_shard(args.config, shard_rank, shard_world, dev, strong=scaling == "strong")
     n_local = int(case.numel())
     filt = None
     if args.filter:
@@ -412,7 +431,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         gpu_cases = None
-        if filt is None:
+        if filt is None and meta["case_lo"] == 0:   # the oracle sample is cases [0, k) of the config
             k = min(args.cpu_cases, meta["case_hi"] - meta["case_lo"])
             gpu_cases = (kept["n_events"][:k].cpu().numpy(), kept["dur"][:k].cpu().numpy())
         cpu = cpu_baseline(args.config, args.cpu_cases, dev, gpu_cases)
@@ -421,7 +440,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": workload_config(args.config, n_local, meta["case_hi"] - meta["case_lo"], meta["A"], world,
                                       filt is not None, n_total),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "verified": verified,
@@ -431,6 +450,11 @@ def main():
                              "frac_of_peak": step_bytes / (ms / 1e3) / 1e9 / peak},
             "stages": stages,
         }
+        line["config"]["scaling_layout"] = (f"{scaling}: " + ("the config's log split across the GPUs by case range"
+                                                       if scaling == "strong" else "one config-sized shard per GPU"))
+        if args.emulate:
+            line["config"]["emulated_shard"] = (f"rank {shard_rank} of {shard_world} on one GPU "
+                                                "(per-GPU step of that run, without the NCCL merge)")
         print(json.dumps(line))
     if comm is not None:
         comm.close()
