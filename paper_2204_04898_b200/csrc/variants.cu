@@ -352,13 +352,17 @@ __global__ void k_item_group(const uint32_t* __restrict__ list, uint64_t n_items
     }
 }
 
+// sort key of a group: (Wmax - weight) above the order key, Wmax = 2^wbits - 1
+// (wbits = bit width of the item count when weights are 1, else 32 with
+// clipping), so one LSD sort orders by weight desc, then order asc
 __global__ void k_sort_keys(const uint64_t* __restrict__ g_weight, const uint32_t* __restrict__ g_order,
-                            uint64_t G, uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                            uint64_t G, int wbits, int order_bits, uint64_t* __restrict__ key,
+                            uint32_t* __restrict__ val) {
+    const uint64_t wmax = (1ull << wbits) - 1;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G;
          g += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t w = g_weight[g];
-        uint32_t wc = w > 0xffffffffull ? 0xffffffffu : (uint32_t)w;
-        key[g] = ((uint64_t)(0xffffffffu - wc) << 32) | g_order[g];
+        const uint64_t w = min(g_weight[g], wmax);
+        key[g] = ((wmax - w) << order_bits) | g_order[g];
         val[g] = (uint32_t)g;
     }
 }
@@ -502,13 +506,15 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
     }
     g.G = G;
     // sort groups: count desc, order asc
+    const int wbits = weight ? 32 : std::max(1, bit_width_u64(n_items));
     Scratch sk(s);
     if ((st = sk.alloc(G * 8 + 16))) return bail(st);
     if ((st = dalloc_t(&g.sorted, std::max<uint64_t>(G, 1), s))) return bail(st);
     if ((st = dalloc_t(&g.inv, std::max<uint64_t>(G, 1), s))) return bail(st);
     PM4G_LAUNCH("k_variant_sortkeys", G * 16.0, s,
-                (k_sort_keys<<<gsz(G), 256, 0, s>>>(g.weight, g.order, G, sk.as<uint64_t>(), g.sorted)));
-    PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, 32 + order_bits, s));
+                (k_sort_keys<<<gsz(G), 256, 0, s>>>(g.weight, g.order, G, wbits, order_bits, sk.as<uint64_t>(),
+                                                     g.sorted)));
+    PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, wbits + order_bits, s));
     PM4G_LAUNCH("k_variant_inv", G * 8.0, s, (k_inv<<<gsz(G), 256, 0, s>>>(g.sorted, G, g.inv)));
     *out = g;
     return PM4G_OK;
