@@ -425,10 +425,8 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
     L->case_lo = in->case_lo;
     L->case_hi = in->case_hi;
     L->stream = s;
-    auto bail = [&](pm4g_status st) {
-        pm4g_log_destroy(L);
-        return st;
-    };
+    LogGuard guard(L);
+    auto bail = [&](pm4g_status st) { return st; };   // the guard destroys L
     pm4g_status st;
     if ((st = dalloc((void**)&L->d_n_cases, 8, s))) return bail(st);
     const int64_t N = std::max<int64_t>(n, 1);
@@ -560,7 +558,7 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
     } else {
         apply_meta(L, fm.ts_min, fm.ts_max, fm.case_min, fm.case_max, hpasses, hbits);
     }
-    *out = L;
+    *out = guard.release();
     return PM4G_OK;
 }
 

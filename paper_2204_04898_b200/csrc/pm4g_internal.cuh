@@ -347,6 +347,23 @@ enum { COMM_SUM = 0, COMM_MAX = 2, COMM_MIN = 3 };   // ncclRedOp_t values
 pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int op, cudaStream_t s);
 pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
                                           pm4g_variant_table** out);
+// Owns a log under construction: destroyed on every early return (the
+// PM4G_CK / PM4G_TRY / PM4G_LAUNCH macros return directly), released on success.
+struct LogGuard {
+    pm4g_log* L;
+    explicit LogGuard(pm4g_log* l) : L(l) {}
+    LogGuard(const LogGuard&) = delete;
+    LogGuard& operator=(const LogGuard&) = delete;
+    ~LogGuard() {
+        if (L) pm4g_log_destroy(L);
+    }
+    pm4g_log* release() {
+        pm4g_log* t = L;
+        L = nullptr;
+        return t;
+    }
+};
+
 // NEXT-4 repartition (repartition.cu): rows of an ingested log grouped by
 // destination rank, every column gathered into one buffer (dest-major)
 struct PartitionedRows {

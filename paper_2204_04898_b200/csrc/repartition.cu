@@ -93,8 +93,6 @@ pm4g_status partition_rows(const pm4g_log* in, const uint32_t* bounds, int R, cu
     log_columns(in, &cols, &elems);
     out->elems = elems;
     out->counts.assign(R, 0);
-    size_t row_bytes = 0;
-    for (int e : elems) row_bytes += e;
     // [bounds R+1 u32] [counts R u64] | keys u64[n] | perm u32[n] | columns (16-byte aligned each)
     Scratch meta(s), kv(s);
     PM4G_TRY(meta.alloc((R + 1) * 4 + 16 + R * 8));
@@ -146,10 +144,8 @@ pm4g_status make_ingested_log(const pm4g_log* like, int64_t n, uint32_t case_lo,
     L->case_hi = case_hi;
     L->stream = s;
     L->owns_cols = true;
-    auto bail = [&](pm4g_status st) {
-        pm4g_log_destroy(L);
-        return st;
-    };
+    LogGuard guard(L);
+    auto bail = [&](pm4g_status st) { return st; };   // the guard destroys L
     pm4g_status st;
     const int64_t N = std::max<int64_t>(n, 1);
     if ((st = dalloc((void**)&L->case_, N * 4, s))) return bail(st);
@@ -170,7 +166,7 @@ pm4g_status make_ingested_log(const pm4g_log* like, int64_t n, uint32_t case_lo,
     if ((st = fill(dst))) return bail(st);
     if ((st = dalloc((void**)&L->d_n_cases, 8, s))) return bail(st);
     if ((st = validate_and_meta(L, s))) return bail(st);
-    *out = L;
+    *out = guard.release();
     return PM4G_OK;
 }
 
