@@ -219,3 +219,32 @@ def test_cnt16_table_flush_exact(A):
     ts = np.concatenate([ts, t_big, t_alt])
     p = rng.permutation(case.size)
     check_log(case[p], act[p], ts[p], A, n_case_codes=6002)
+
+
+@pytest.mark.parametrize("ts_bits,case_bits", [(0, 12), (1, 20), (24, 8), (31, 9), (32, 10), (33, 18),
+                                               (40, 24), (56, 8), (62, 2), (63, 1), (64, 0), (20, 32)])
+def test_digit_shift_boundaries(ts_bits, case_bits):
+    """Onesweep digits sit at shift = ts_bits + 8p: the 64-bit path (shift < 32),
+    the high-word path (32 <= shift < 64) and the single-case guard (shift 64);
+    pass 0 takes its digit from the case column.  Spans are chosen so the
+    composite key has exactly ts_bits + case_bits bits."""
+    rng = np.random.default_rng(ts_bits * 100 + case_bits)
+    n = 6000
+    ncases = 1 << case_bits if case_bits < 32 else 2**32 - 1
+    case = rng.integers(0, min(ncases, 3000), n).astype(np.int64)
+    if case_bits == 32:
+        case[:2] = [0, 2**32 - 2]            # the full 32-bit case range
+    elif case_bits > 0:
+        case[:2] = [0, ncases - 1]
+    base = -(2**63) if ts_bits == 64 else -(2**(max(ts_bits, 1) - 1))
+    span = (2**64 - 1) if ts_bits == 64 else ((1 << ts_bits) - 1 if ts_bits else 0)
+    ts = (base + rng.integers(0, span + 1 if span < 2**63 else 2**63, n, dtype=np.int64)
+          if span else np.full(n, 7, np.int64))
+    if span:
+        ts[2], ts[3] = base, base + span if span < 2**63 else 2**63 - 1
+        if ts_bits == 64:
+            ts[3] = 2**63 - 1
+    act = rng.integers(0, 5, n)
+    if case_bits + ts_bits > 64:
+        pytest.skip("key wider than 64 bits")
+    check_log(case.tolist(), act.tolist(), ts.tolist(), 5, n_case_codes=int(case.max()) + 1)
