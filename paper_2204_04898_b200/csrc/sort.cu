@@ -446,6 +446,9 @@ struct FmtArgs {
     bool aligned;              // gkey / gact / gidx 16-byte aligned (TMA bulk path)
 };
 
+// the TMA targets (s_key at 0, s_act, s_idx) must stay 16-byte aligned
+static_assert(((FMT_BUF * 8 + FMT_BUF * 2 * 2 + (FMT_TILE + 8) * 2 + (FMT_TILE + 16)) % 16) == 0, "s_act alignment");
+
 template <class P, bool WI>
 __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     extern __shared__ __align__(16) unsigned char fsm[];
@@ -453,7 +456,8 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     uint16_t* s_dst = (uint16_t*)(s_key + FMT_BUF);                // [FMT_BUF]
     uint16_t* s_ci = s_dst + FMT_BUF;                              // [FMT_BUF] case of each row
     uint16_t* s_head = s_ci + FMT_BUF;                             // [FMT_TILE + 8]
-    P* s_act = (P*)(s_head + FMT_TILE + 8);                        // [FMT_BUF]
+    uint8_t* s_wide = (uint8_t*)(s_head + FMT_TILE + 8);           // [FMT_TILE + 16] case needs 64-bit ranks
+    P* s_act = (P*)(s_wide + FMT_TILE + 16);                       // [FMT_BUF] (16-byte aligned: TMA target)
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
     __shared__ uint32_t s_prefix, s_nbig, s_bigh[16];
@@ -546,6 +550,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     }
     if (tid < 16) s_bigh[tid] = 0;
     if (tid == 0) s_nbig = 0;
+    for (uint32_t h = tid; h < H; h += FMT_THREADS) s_wide[h] = 0;
     __syncthreads();
 
     // ---- 3. warp 0 resolves the case ranks (decoupled look-back) while warps
@@ -594,6 +599,16 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         }
         wsync();
 
+        // ---- 4a. narrow cases: every key within +-2^30 of the case's first key,
+        // so any two keys of the case differ by < 2^31 and a comparison is the
+        // sign of their 32-bit low-word difference (exact, modular)
+        for (int p = h0 + wt; p < oend; p += NW) {
+            const uint32_t h = s_ci[p];
+            const int64_t d = (int64_t)(s_key[p] - s_key[s_head[h]]);
+            if (d < -(1ll << 30) || d >= (1ll << 30)) s_wide[h] = 1;
+        }
+        wsync();
+
         // ---- 4. rank each row inside its case: #(key_j < key_p) + #(j < p with key_j == key_p).
         // Event-parallel with one uniform loop per case (a warp mostly reads one
         // case -> broadcast smem reads, equal trip counts).
@@ -610,7 +625,11 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             // has no successor and takes the two-compare form
             int r = 0;
             const uint64_t ki = s_key[p], ki1 = ki + 1;
-            if (ki1 != 0) {
+            if (!s_wide[h]) {   // 32-bit: r += sign(lo_j - lo_T), T = ki + [j < p]
+                const uint32_t* lo = (const uint32_t*)s_key;   // low word of key j at lo[2 j]
+                const uint32_t ti = (uint32_t)ki, ti1 = ti + 1u;
+                for (int j = s0; j < e0; ++j) r += (int)((lo[2 * j] - (j < p ? ti1 : ti)) >> 31);
+            } else if (ki1 != 0) {
                 for (int j = s0; j < e0; ++j) r += s_key[j] < (j < p ? ki1 : ki);
             } else {
                 for (int j = s0; j < e0; ++j) r += (s_key[j] < ki) | ((s_key[j] == ki) & (j < p));
@@ -679,7 +698,7 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
     fa.big = fa.status + tiles;
     const bool wi = fa.perm_out != nullptr;
     fa.aligned = aligned16(fa.gkey) && aligned16(fa.gact) && (!wi || aligned16(fa.gidx));
-    const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + 16;
+    const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + (FMT_TILE + 16) + 16;
     const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0);
     static bool attr = false;
     if (!attr) {
