@@ -367,6 +367,30 @@ __global__ void k_sort_keys(const uint64_t* __restrict__ g_weight, const uint32_
     }
 }
 
+// Small group counts: every key's output position = #(keys smaller) + #(equal
+// keys at lower index), all pairs compared (keys staged through shared memory
+// in chunks) -- one launch instead of ~6 latency-bound radix passes.
+constexpr uint64_t RANK_SORT_MAX = 4096;
+__global__ __launch_bounds__(256) void k_rank_sort(const uint64_t* __restrict__ key, uint32_t n,
+                                                   uint32_t* __restrict__ sorted) {
+    __shared__ uint64_t s_k[2048];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t ki = i < n ? key[i] : 0;
+    uint32_t r = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 2048) {
+        const uint32_t cn = min(2048u, n - c0);
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < cn; t += blockDim.x) s_k[t] = key[c0 + t];
+        __syncthreads();
+        if (i < n)
+            for (uint32_t t = 0; t < cn; ++t) {
+                const uint64_t kj = s_k[t];
+                r += (kj < ki) | ((kj == ki) & (c0 + t < i));
+            }
+    }
+    if (i < n) sorted[r] = i;
+}
+
 struct Groups {
     uint64_t G = 0;
     uint64_t* weight = nullptr;     // [G]
@@ -514,7 +538,14 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
     PM4G_LAUNCH("k_variant_sortkeys", G * 16.0, s,
                 (k_sort_keys<<<gsz(G), 256, 0, s>>>(g.weight, g.order, G, wbits, order_bits, sk.as<uint64_t>(),
                                                      g.sorted)));
-    PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, wbits + order_bits, s));
+    if (G <= RANK_SORT_MAX) {
+        if (G)
+            PM4G_LAUNCH("k_rank_sort", G * 8.0 + G * 4.0, s,
+                        (k_rank_sort<<<(unsigned)((G + 255) / 256), 256, 0, s>>>(sk.as<uint64_t>(), (uint32_t)G,
+                                                                               g.sorted)));
+    } else {
+        PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, wbits + order_bits, s));
+    }
     PM4G_LAUNCH("k_variant_inv", G * 8.0, s, (k_inv<<<gsz(G), 256, 0, s>>>(g.sorted, G, g.inv)));
     *out = g;
     return PM4G_OK;
