@@ -322,22 +322,35 @@ __global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
 
 // occupied slots with weight > 0 -> groups (append order is irrelevant: the
 // final sort is a total order)
-__global__ void k_compact(const Slot* __restrict__ table, uint64_t cap,
-                          const uint32_t* __restrict__ item_of_rep_slot, uint32_t* __restrict__ slot_group,
-                          uint64_t* __restrict__ g_weight, uint32_t* __restrict__ g_rep_item,
-                          uint32_t* __restrict__ g_order, uint32_t* __restrict__ n_groups,
-                          const uint32_t* __restrict__ overflow) {
+// also sums the new groups' sequence lengths (one atomic per block) so the
+// host learns the total variant length with the round's counters
+template <class OFF>
+__global__ __launch_bounds__(256) void k_compact(const Slot* __restrict__ table, uint64_t cap,
+                                                 const uint32_t* __restrict__ item_of_rep_slot,
+                                                 uint32_t* __restrict__ slot_group, uint64_t* __restrict__ g_weight,
+                                                 uint32_t* __restrict__ g_rep_item, uint32_t* __restrict__ g_order,
+                                                 uint32_t* __restrict__ n_groups, const uint32_t* __restrict__ overflow,
+                                                 const OFF* __restrict__ off, unsigned long long* total_len) {
+    __shared__ unsigned long long s_tot;
     if (*overflow) return;
+    if (threadIdx.x == 0) s_tot = 0;
+    __syncthreads();
+    unsigned long long tl = 0;
     for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < cap;
          sl += (uint64_t)gridDim.x * blockDim.x) {
         const Slot& s = table[sl];
         if ((s.k1 | s.k2) == 0 || s.weight == 0) continue;
         uint32_t g = atomicAdd(n_groups, 1u);
+        const uint32_t rep_item = item_of_rep_slot ? item_of_rep_slot[sl] : s.rep;
         g_weight[g] = s.weight;
-        g_rep_item[g] = item_of_rep_slot ? item_of_rep_slot[sl] : s.rep;
+        g_rep_item[g] = rep_item;
         g_order[g] = s.rep;
         slot_group[sl] = g;
+        tl += (unsigned long long)(off[rep_item + 1] - off[rep_item]);
     }
+    if (tl) atomicAdd(&s_tot, tl);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_tot) atomicAdd(total_len, s_tot);
 }
 
 __global__ void k_item_group(const uint32_t* __restrict__ list, uint64_t n_items,
@@ -393,6 +406,7 @@ __global__ __launch_bounds__(256) void k_rank_sort(const uint64_t* __restrict__ 
 
 struct Groups {
     uint64_t G = 0;
+    uint64_t total_len = 0;         // sum of the groups' sequence lengths
     uint64_t* weight = nullptr;     // [G]
     uint32_t* rep_item = nullptr;   // [G]
     uint32_t* order = nullptr;      // [G] (rep's order key)
@@ -456,7 +470,9 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
     uint32_t* list_b = list_a + N;
     // [0] next_count, [1] overflow, [2] claimed slots, [3] n_groups
     uint32_t* counters = list_b + N;
+    unsigned long long* d_total = (unsigned long long*)(((uintptr_t)(counters + 4) + 7) & ~(uintptr_t)7);
     PM4G_CK(cudaMemsetAsync(counters, 0, 16, s));
+    PM4G_CK(cudaMemsetAsync(d_total, 0, 8, s));
 
     const uint32_t* list = nullptr;   // round 0: all items
     uint64_t n_active = n_items;
@@ -506,15 +522,17 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                                                                ior, table, item_slot,
                                                                pending, next_list, counters, counters + 1)));
             PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
-                        (k_compact<<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
-                                                            g.weight, g.rep_item, g.order,
-                                                            counters + 3, counters + 1)));
+                        (k_compact<OFF><<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
+                                                                 g.weight, g.rep_item, g.order,
+                                                                 counters + 3, counters + 1, off, d_total)));
             PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
                         (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
                                                          g.item_group, counters + 1)));
             // one host round trip per round: next_count, overflow, claims, n_groups
             uint32_t h[4] = {0, 0, 0, 0};
+            unsigned long long htot = 0;
             PM4G_CK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, s));
+            PM4G_CK(cudaMemcpyAsync(&htot, d_total, 8, cudaMemcpyDeviceToHost, s));
             PM4G_CK(cudaStreamSynchronize(s));
             if (h[1]) {  // load limit hit: verify/compact/item_group skipped on the device; regrow
                 if (cap >= full || attempt > 16) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
@@ -522,6 +540,7 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                 continue;
             }
             G = h[3];
+            g.total_len = htot;
             n_active = h[0];
             list = next_list;
             if (round > 64 * 1024) return bail(fail(PM4G_ECUDA, "variant grouping did not converge"));
@@ -686,10 +705,7 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
                                                           v->rep_case, v->k1, v->k2)));
     }
     if ((st = excl_scan_u32_to_u64(v->len, v->seq_off, (int64_t)g.G, s))) return bail(st);
-    uint64_t total = 0;
-    if (cudaMemcpyAsync(&total, v->seq_off + g.G, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return bail(cuda_fail(cudaGetLastError(), "variant total length"));
+    const uint64_t total = g.total_len;   // summed by k_compact, read with the round counters
     v->total_len = total;
     if ((st = dalloc_t(&v->seq_act, std::max<uint64_t>(total, 1), s))) return bail(st);
     if (g.G) {
