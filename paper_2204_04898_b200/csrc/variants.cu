@@ -121,7 +121,8 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     const uint32_t* __restrict__ list, uint64_t n_items, const uint64_t* __restrict__ k1,
     const uint64_t* __restrict__ k2, const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
     const uint32_t* __restrict__ order, Slot* table, uint64_t mask, uint32_t limit, uint64_t salt,
-    uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* ctl) {
+    uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* ctl,
+    const uint64_t* __restrict__ d_n) {
     extern __shared__ __align__(16) unsigned char ins_sm[];
     unsigned long long* s_k1 = (unsigned long long*)ins_sm;
     unsigned long long* s_k2 = s_k1 + INS_SLOTS;
@@ -132,6 +133,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     __shared__ uint32_t s_scan[INS_THREADS / 32 + 1];
     __shared__ uint32_t s_stop;
     (void)off;
+    if (d_n) n_items = min(n_items, *d_n);   // round 0 sized by an upper bound: the device count rules
     for (uint64_t chunk = blockIdx.x; chunk * INS_CHUNK < n_items; chunk += gridDim.x) {
         if (threadIdx.x == 0) s_stop = *(volatile uint32_t*)ctl;   // table abandoned: stop early
         for (int i = threadIdx.x; i < INS_SLOTS; i += INS_THREADS) {
@@ -284,8 +286,9 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
                          const uint32_t* __restrict__ item_of_rep_slot, Slot* table,
                          const uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending,
                          uint32_t* __restrict__ next_list, uint32_t* __restrict__ next_count,
-                         const uint32_t* __restrict__ overflow) {
+                         const uint32_t* __restrict__ overflow, const uint64_t* __restrict__ d_n) {
     if (*overflow) return;   // this attempt's table is abandoned (item_slot incomplete)
+    if (d_n) n_items = min(n_items, *d_n);
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -310,8 +313,9 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
 __global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
                            const uint32_t* __restrict__ order, const Slot* __restrict__ table,
                            const uint32_t* __restrict__ item_slot, uint32_t* __restrict__ item_of_rep_slot,
-                           const uint32_t* __restrict__ overflow) {
+                           const uint32_t* __restrict__ overflow, const uint64_t* __restrict__ d_n) {
     if (*overflow) return;
+    if (d_n) n_items = min(n_items, *d_n);
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -356,8 +360,9 @@ __global__ __launch_bounds__(256) void k_compact(const Slot* __restrict__ table,
 __global__ void k_item_group(const uint32_t* __restrict__ list, uint64_t n_items,
                              const uint32_t* __restrict__ item_slot, const uint8_t* __restrict__ pending,
                              const uint32_t* __restrict__ slot_group, uint32_t* __restrict__ item_group,
-                             const uint32_t* __restrict__ overflow) {
+                             const uint32_t* __restrict__ overflow, const uint64_t* __restrict__ d_n) {
     if (*overflow) return;
+    if (d_n) n_items = min(n_items, *d_n);
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t it = list ? list[t] : (uint32_t)t;
@@ -442,9 +447,14 @@ static uint64_t pow2_at_least(uint64_t x) {
 // Group n_items items by exact sequence.  order: unique u32 per item (nullptr
 // = item index).  order_bits: bits needed by the order key (for the sort).
 template <class OFF, class ACT>
+// d_n (optional): the device item count when n_items is only an upper bound
+// (round 0 clamps to it; the true count comes back with round 0's counters in
+// *n_true), which spares a host round trip before the grouping starts.
 static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint64_t* k2,
                                const OFF* off, const ACT* acts, const uint64_t* weight,
-                               const uint32_t* order, int order_bits, cudaStream_t s, Groups* out) {
+                               const uint32_t* order, int order_bits, cudaStream_t s, Groups* out,
+                               const uint64_t* d_n = nullptr, uint64_t* n_true = nullptr) {
+    if (n_true) *n_true = n_items;
     Groups g;
     auto bail = [&](pm4g_status st) {
         g.free(s);
@@ -510,30 +520,37 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                 PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
                             (k_insert<OFF><<<gi, INS_THREADS, INS_SMEM, s>>>(
                                 list, n_active, k1, k2, off, weight, order, table, cap - 1, limit, salt,
-                                item_slot, pending, counters + 1)));
+                                item_slot, pending, counters + 1, list ? nullptr : d_n)));
             }
             uint32_t* ior = order ? item_of_rep_slot : nullptr;   // identity order: rep item = slot.rep
             if (order)
                 PM4G_LAUNCH("k_variant_rep", n_active * 8.0, s,
                             (k_rep_item<<<gs, 256, 0, s>>>(list, n_active, order, table, item_slot, item_of_rep_slot,
-                                                            counters + 1)));
+                                                            counters + 1, list ? nullptr : d_n)));
             PM4G_LAUNCH("k_variant_verify", n_active * 16.0, s,
                         (k_verify<OFF, ACT><<<gs, 256, 0, s>>>(list, n_active, off, acts, weight, order,
                                                                ior, table, item_slot,
-                                                               pending, next_list, counters, counters + 1)));
+                                                               pending, next_list, counters, counters + 1,
+                                                               list ? nullptr : d_n)));
             PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
                         (k_compact<OFF><<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
                                                                  g.weight, g.rep_item, g.order,
                                                                  counters + 3, counters + 1, off, d_total)));
             PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
                         (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
-                                                         g.item_group, counters + 1)));
+                                                         g.item_group, counters + 1, list ? nullptr : d_n)));
             // one host round trip per round: next_count, overflow, claims, n_groups
             uint32_t h[4] = {0, 0, 0, 0};
             unsigned long long htot = 0;
+            uint64_t hn = n_items;
             PM4G_CK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, s));
             PM4G_CK(cudaMemcpyAsync(&htot, d_total, 8, cudaMemcpyDeviceToHost, s));
+            if (d_n && !list) PM4G_CK(cudaMemcpyAsync(&hn, d_n, 8, cudaMemcpyDeviceToHost, s));
             PM4G_CK(cudaStreamSynchronize(s));
+            if (d_n && !list) {
+                n_items = std::min(n_items, hn);
+                if (n_true) *n_true = n_items;
+            }
             if (h[1]) {  // load limit hit: verify/compact/item_group skipped on the device; regrow
                 if (cap >= full || attempt > 16) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
                 cap = std::min<uint64_t>(full, cap * 4);
@@ -679,9 +696,13 @@ template <class OFF, class ACT>
 static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const uint64_t* k2,
                                   const OFF* off, const ACT* acts, const uint64_t* weight,
                                   const uint32_t* order, int order_bits, const uint32_t* rep_code,
-                                  bool with_case_variant, cudaStream_t s, pm4g_variant_table** out) {
+                                  bool with_case_variant, cudaStream_t s, pm4g_variant_table** out,
+                                  const uint64_t* d_n = nullptr, uint64_t* n_true = nullptr) {
     Groups g;
-    PM4G_TRY((group_items<OFF, ACT>(n_items, k1, k2, off, acts, weight, order, order_bits, s, &g)));
+    uint64_t nt = n_items;
+    PM4G_TRY((group_items<OFF, ACT>(n_items, k1, k2, off, acts, weight, order, order_bits, s, &g, d_n, &nt)));
+    n_items = nt;
+    if (n_true) *n_true = nt;
     pm4g_variant_table* v = new pm4g_variant_table();
     v->stream = s;
     v->V = g.G;
@@ -727,14 +748,22 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
 
 pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint64_t* k2,
                                cudaStream_t s, pm4g_variant_table** out) {
-    PM4G_TRY(fetch_n_cases(L, s));
-    const uint64_t C = (uint64_t)L->n_cases;
+    // without a known case count, start from the host bound (the aggregate
+    // filled the keys of the true cases); round 0 reads the count itself
+    const bool known = L->n_cases >= 0;
+    const uint64_t C = known ? (uint64_t)L->n_cases
+                             : std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
+    const uint64_t* dn = known ? nullptr : L->d_n_cases;
     int order_bits = bit_width_u64(C);
+    uint64_t nt = C;
+    pm4g_status st;
     switch (L->act_bytes) {
-        case 1: return build_variants<uint32_t, uint8_t>(C, k1, k2, L->off, (const uint8_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
-        case 2: return build_variants<uint32_t, uint16_t>(C, k1, k2, L->off, (const uint16_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
-        default: return build_variants<uint32_t, uint32_t>(C, k1, k2, L->off, (const uint32_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out);
+        case 1: st = build_variants<uint32_t, uint8_t>(C, k1, k2, L->off, (const uint8_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out, dn, &nt); break;
+        case 2: st = build_variants<uint32_t, uint16_t>(C, k1, k2, L->off, (const uint16_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out, dn, &nt); break;
+        default: st = build_variants<uint32_t, uint32_t>(C, k1, k2, L->off, (const uint32_t*)L->s_act, nullptr, nullptr, order_bits, L->s_case_code, true, s, out, dn, &nt); break;
     }
+    if (st == PM4G_OK && !known) const_cast<pm4g_log*>(L)->n_cases = (int64_t)nt;
+    return st;
 }
 
 // Merge R per-shard tables (disjoint case ranges): items = entries.  With
