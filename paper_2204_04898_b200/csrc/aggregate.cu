@@ -287,11 +287,7 @@ static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s
     const uint32_t A = L->A;
     const size_t tab = o.tables ? (size_t)tab_words_for<P, MM>(MODE, A) * 4 : 0;
     const size_t smem = tab + AGG_STAGES * sizeof(AggStage<P>);
-    static size_t attr = 0;
-    if (smem > attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_aggregate<P, MODE, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-    }
+    PM4G_MAX_SMEM(k_aggregate<P, MODE, MM>);
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     // cases per tile: a tile's rows should fit one stage (mean length from the
     // case-code range, exact when codes are dense; a rare oversized tile is

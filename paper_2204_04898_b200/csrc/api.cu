@@ -97,6 +97,25 @@ int num_sms() {
     return sms;
 }
 
+int max_smem_optin() {
+    static const int v = [] {
+        int dev = 0, m = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&m, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || m <= 0)
+            m = 227 * 1024;
+        return m;
+    }();
+    return v;
+}
+
+cudaError_t set_max_dynamic_smem(const void* func) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, func);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem_optin() - (int)fa.sharedSizeBytes);
+}
+
 bool debug_weak_hash() {
     const char* e = getenv("PM4G_DEBUG_WEAK_HASH");
     return e && e[0] == '1';

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,10 +48,17 @@ static NcclApi g_nccl;
 
 static pm4g_status load_nccl() {
     if (g_nccl.h) return PM4G_OK;
+    // PM4G_NCCL_LIB: an explicit library path (tests load a loopback NCCL that
+    // runs several ranks as threads of one process on one device)
+    const char* forced = getenv("PM4G_NCCL_LIB");
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     void* h = nullptr;
-    for (const char* nm : names)
-        if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (forced && *forced) {
+        h = dlopen(forced, RTLD_NOW | RTLD_LOCAL);
+    } else {
+        for (const char* nm : names)
+            if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    }
     if (!h) return fail(PM4G_ENCCL, std::string("cannot load NCCL: ") + dlerror());
     g_nccl.h = h;
     g_nccl.getUniqueId = (NcclResult(*)(NcclUid*))dlsym(h, "ncclGetUniqueId");

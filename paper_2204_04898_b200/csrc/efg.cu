@@ -217,11 +217,7 @@ static pm4g_status launch_efg(const pm4g_log* L, const EfgTab& g, cudaStream_t s
     const uint32_t TW = MODE == EFG_FULL ? A * A : EFG_HS;
     const size_t tab = (((size_t)(MODE == EFG_FULL ? 5 : 6) * TW * 4) + 15) & ~(size_t)15;
     const size_t smem = tab + (size_t)EFG_STAGE * (8 + 2 + sizeof(P)) + (EFG_MAX_CPT + 2) * 4 + 16;
-    static size_t attr = 0;
-    if (smem > attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_efg<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-    }
+    PM4G_MAX_SMEM(k_efg<P, MODE>);
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     const double mean_len = (double)L->n / (double)std::max<uint64_t>(cap, 1);
     const uint32_t cpt = (uint32_t)std::max(16.0, std::min((double)EFG_MAX_CPT, 0.7 * EFG_STAGE / std::max(mean_len, 1.0)));

@@ -504,12 +504,8 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
 #define PM4G_FILTER_COLS(P)                                                                                     \
     {                                                                                                           \
         const size_t smem = FS_STAGES * sizeof(FsStage<P>);                                                     \
-        static bool attr = false;                                                                               \
-        if (!attr) {                                                                                            \
-            PM4G_CK(cudaFuncSetAttribute(k_filter_cols<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-            PM4G_CK(cudaFuncSetAttribute(k_filter_cols<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-            attr = true;                                                                                        \
-        }                                                                                                       \
+        PM4G_MAX_SMEM(k_filter_cols<P, true>);                                                                  \
+        PM4G_MAX_SMEM(k_filter_cols<P, false>);                                                                 \
         const int per_sm = std::max(1, std::min(3, (int)((220 * 1024) / (smem + 6 * 1024))));                  \
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * per_sm)); \
         if (tp)                                                                                                 \

@@ -24,6 +24,17 @@ pm4g_status cuda_fail(cudaError_t e, const char* what);
         if (_e != cudaSuccess) return ::pm4g::cuda_fail(_e, #call); \
     } while (0)
 
+// Opt a kernel into the device's full dynamic shared memory once (thread-safe
+// static initialisation; occupancy still follows each launch's actual size).
+// The cap is the device's opt-in limit minus the kernel's static shared memory.
+int max_smem_optin();
+cudaError_t set_max_dynamic_smem(const void* func);
+#define PM4G_MAX_SMEM(...)                                                                          \
+    do {                                                                                            \
+        static const cudaError_t _se = ::pm4g::set_max_dynamic_smem((const void*)(__VA_ARGS__));    \
+        if (_se != cudaSuccess) return ::pm4g::cuda_fail(_se, "cudaFuncSetAttribute");              \
+    } while (0)
+
 #define PM4G_TRY(call)                          \
     do {                                        \
         pm4g_status _s = (call);                \

@@ -326,12 +326,7 @@ template <class P, bool FC, bool WI, bool HI>
 static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                  const char* name, double bytes) {
     const size_t smem = OsLayout<P, FC, WI>::bytes;
-    static bool attr = false;
-    if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_onesweep<P, FC, WI, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr = true;
-    }
+    PM4G_MAX_SMEM(k_onesweep<P, FC, WI, HI>);
     PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI, HI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
     return PM4G_OK;
 }
@@ -700,13 +695,8 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
     fa.aligned = aligned16(fa.gkey) && aligned16(fa.gact) && (!wi || aligned16(fa.gidx));
     const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + (FMT_TILE + 16) + 16;
     const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0);
-    static bool attr = false;
-    if (!attr) {
-        PM4G_CK(cudaFuncSetAttribute(k_format<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_base));
-        PM4G_CK(cudaFuncSetAttribute(k_format<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(smem_base + (size_t)FMT_BUF * 4)));
-        attr = true;
-    }
+    PM4G_MAX_SMEM(k_format<P, false>);
+    PM4G_MAX_SMEM(k_format<P, true>);
     const double bytes = (double)n * (2.0 * (8 + sizeof(P) + (wi ? 4 : 0)));
     if (wi)
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));

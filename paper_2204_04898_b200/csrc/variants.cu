@@ -509,12 +509,7 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
             uint32_t* next_list = (list == list_a) ? list_b : list_a;
             const int gs = gsz(n_active);
             {
-                static bool attr = false;
-                if (!attr) {
-                    PM4G_CK(cudaFuncSetAttribute(k_insert<OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)INS_SMEM));
-                    attr = true;
-                }
+                PM4G_MAX_SMEM(k_insert<OFF>);
                 uint64_t chunks = (n_active + INS_CHUNK - 1) / INS_CHUNK;
                 int gi = (int)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (uint64_t)num_sms() * 3));
                 PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
