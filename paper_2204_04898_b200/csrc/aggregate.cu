@@ -42,28 +42,34 @@ constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
-constexpr uint32_t AGG_STAGE = 4096;   // rows of a case tile staged in smem (+ alignment slack)
 constexpr int AGG_CONSUMERS = 256;     // 8 consumer warps; + 1 producer warp
 constexpr int AGG_BLOCK = AGG_CONSUMERS + 32;
-constexpr int AGG_STAGES = 2;
+
+enum { TAB_FULL = 1, TAB_HASH = 2 };
+
+// Stage geometry per table mode (measured): the dense table leaves room for a
+// second CTA per SM with 3 stages of 2048 rows (0.68 -> 0.53 ms at 100M); the
+// hash table keeps one CTA per SM and prefers 2 stages of 4096 rows.
+template <int MODE>
+struct AggGeom {
+    static constexpr uint32_t ROWS = MODE == TAB_FULL ? 2048 : 4096;   // rows of a staged case tile
+    static constexpr int STAGES = MODE == TAB_FULL ? 3 : 2;
+};
 
 // One pipeline stage: the tile's case offsets and its rows (keys, activities).
-template <class P>
+template <class P, uint32_t ROWS>
 struct alignas(128) AggStage {
     uint32_t off[AGG_CASES + 4];
-    uint64_t key[AGG_STAGE + 16];
-    P act[AGG_STAGE + 32];
+    uint64_t key[ROWS + 16];
+    P act[ROWS + 32];
     uint32_t nc, ka, aa, staged;
     uint64_t c0;
 };
 
-
-enum { TAB_FULL = 1, TAB_HASH = 2 };
-
 constexpr int HASH_PROBES = 16;
 constexpr uint32_t HASH_EMPTY = 0xffffffffu;
 
-// shared-memory hash slots: as many as fit next to the two stages
+// shared-memory hash slots: as many as fit next to the two 4096-row stages
 template <class P, bool MM>
 __host__ __device__ constexpr uint32_t hash_slots() { return (sizeof(P) == 1 && !MM) ? 8192u : 4096u; }
 
@@ -110,6 +116,9 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
     int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak,
     uint32_t* __restrict__ cco, uint32_t case_min) {
+    constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
+    constexpr int AGG_STAGES = AggGeom<MODE>::STAGES;
+    using Stage = AggStage<P, AGG_STAGE>;
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
     const bool tables = packed != nullptr;
@@ -128,7 +137,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     uint32_t* s_mx = s_mn + TW;
     unsigned long long* g_mn = (unsigned long long*)mm;
     unsigned long long* g_mx = g_mn + AA;
-    AggStage<P>* stage = (AggStage<P>*)(agg_sm + (size_t)tab_words * 4);
+    Stage* stage = (Stage*)(agg_sm + (size_t)tab_words * 4);
     uint64_t* g_cnt = packed;
     uint64_t* g_sum = packed + AA;
     uint64_t* g_st = packed + 2 * (size_t)AA;
@@ -155,7 +164,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
         for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
             const int s = i % AGG_STAGES;
             if (i >= AGG_STAGES) mbar_wait(&s_empty[s], ((i / AGG_STAGES) - 1) & 1);
-            AggStage<P>& st = stage[s];
+            Stage& st = stage[s];
             const uint64_t c0 = t * cpt;
             const uint32_t nc = (uint32_t)min((uint64_t)cpt, C - c0);
             for (uint32_t j = lane; j <= nc; j += 32) st.off[j] = off[c0 + j];
@@ -188,7 +197,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
         for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
             const int s = i % AGG_STAGES;
             mbar_wait(&s_full[s], (i / AGG_STAGES) & 1);
-            const AggStage<P>& st = stage[s];
+            const Stage& st = stage[s];
             const uint32_t nc = st.nc, ka = st.ka, aa = st.aa;
             const bool staged = st.staged != 0;
             const uint64_t c0 = st.c0;
@@ -286,7 +295,8 @@ template <class P, int MODE, bool MM>
 static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
     const size_t tab = o.tables ? (size_t)tab_words_for<P, MM>(MODE, A) * 4 : 0;
-    const size_t smem = tab + AGG_STAGES * sizeof(AggStage<P>);
+    constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
+    const size_t smem = tab + AggGeom<MODE>::STAGES * sizeof(AggStage<P, AGG_STAGE>);
     PM4G_MAX_SMEM(k_aggregate<P, MODE, MM>);
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     // cases per tile: a tile's rows should fit one stage (mean length from the
