@@ -27,7 +27,7 @@
 namespace pm4g {
 
 constexpr int EFG_THREADS = 512;
-constexpr int EFG_STAGE = 4096;          // rows of a staged tile
+constexpr int EFG_STAGE = 2048;          // rows of a staged tile (2048: the dense table + stage fit 2 CTAs per SM)
 constexpr int EFG_MAX_CPT = 1024;        // cases per tile
 constexpr uint32_t EFG_HS = 4096;        // hash slots
 constexpr int EFG_PROBES = 16;
