@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "pm4g_internal.cuh"
@@ -126,36 +127,17 @@ struct OsLayout {
     static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
 };
 
-// HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
-// the digits sit above ts_bits >= 32), extracted with one 32-bit shift
+// One tile's stable rank / publish / permute / look-back / write-out.  The
+// tile's rows are in u_key (FROM_COLS: u_case, u_ts) and u_act; s_whist must
+// be zero on entry.
 template <class P, bool FROM_COLS, bool WITH_IDX, bool HI>
-__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
-    using Lay = OsLayout<P, FROM_COLS, WITH_IDX>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* u_key = (uint64_t*)(smem + Lay::o_in);
-    int64_t* u_ts = (int64_t*)(smem + Lay::o_in);
-    uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
-    uint32_t* u_idx = (uint32_t*)(smem + Lay::o_idx);
-    P* u_act = (P*)(smem + Lay::o_act);
-    uint32_t* v_idx = (uint32_t*)(smem + Lay::o_vidx);
-    P* v_act = (P*)(smem + Lay::o_vact);
-    __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
-    __shared__ long long s_gbase[RADIX];
-    __shared__ uint32_t s_scan[SORT_WARPS + 1];
-    __shared__ uint32_t s_tile;
-    __shared__ __align__(8) uint64_t s_bar;
-
+__device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& a, const uint32_t tile,
+                                        const uint32_t nvalid, uint64_t* u_key, const int64_t* u_ts,
+                                        const uint32_t* u_case, const uint32_t* u_idx, const P* u_act,
+                                        uint32_t* v_idx, P* v_act, uint32_t (*s_whist)[RADIX],
+                                        long long* s_gbase, uint32_t* s_scan) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_tile = atomicAdd(a.tile_counter, 1u);
-        mbar_init(&s_bar, 1);
-    }
-    for (int i = tid; i < SORT_WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
     const int64_t base = (int64_t)tile * SORT_TILE;
-    const int64_t nv64 = a.n - base;
-    const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
     const uint32_t dmask = (1u << a.bits) - 1;
     const bool gen_idx = WITH_IDX && a.in_idx == nullptr;
     // digit of a key: shift < 64 except for a single-case log (no case bits)
@@ -166,36 +148,6 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
         if (HI) return ((uint32_t)(k >> 32) >> shh) & dmask;
         return sh_ok ? (uint32_t)(k >> sh) & dmask : 0u;
     };
-
-    // ---- tile load: TMA bulk copies for full aligned tiles, plain loads otherwise
-    if (nvalid == SORT_TILE && a.aligned) {
-        if (tid == 0) {
-            const uint32_t bytes = SORT_TILE * (uint32_t)(8 + sizeof(P) + (FROM_COLS ? 4 : 0) +
-                                                          ((WITH_IDX && !gen_idx) ? 4 : 0));
-            mbar_expect_tx(&s_bar, bytes);
-            if (FROM_COLS) {
-                tma_load_1d(u_ts, a.in_ts + base, SORT_TILE * 8, &s_bar);
-                tma_load_1d(u_case, a.in_case + base, SORT_TILE * 4, &s_bar);
-            } else {
-                tma_load_1d(u_key, a.in_key + base, SORT_TILE * 8, &s_bar);
-            }
-            if (WITH_IDX && !gen_idx) tma_load_1d(u_idx, a.in_idx + base, SORT_TILE * 4, &s_bar);
-            tma_load_1d(u_act, a.in_act + base, SORT_TILE * sizeof(P), &s_bar);
-        }
-        mbar_wait(&s_bar, 0);
-    } else {
-        for (uint32_t i = tid; i < nvalid; i += SORT_THREADS) {
-            if (FROM_COLS) {
-                u_ts[i] = a.in_ts[base + i];
-                u_case[i] = a.in_case[base + i];
-            } else {
-                u_key[i] = a.in_key[base + i];
-            }
-            if (WITH_IDX && !gen_idx) u_idx[i] = a.in_idx[base + i];
-            u_act[i] = a.in_act[base + i];
-        }
-        __syncthreads();
-    }
 
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
     // Peers (lanes holding the same digit) from one ballot per digit bit.
@@ -322,9 +274,170 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
     }
 }
 
+// HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
+// the digits sit above ts_bits >= 32), extracted with one 32-bit shift
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI>
+__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
+    using Lay = OsLayout<P, FROM_COLS, WITH_IDX>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* u_key = (uint64_t*)(smem + Lay::o_in);
+    int64_t* u_ts = (int64_t*)(smem + Lay::o_in);
+    uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
+    uint32_t* u_idx = (uint32_t*)(smem + Lay::o_idx);
+    P* u_act = (P*)(smem + Lay::o_act);
+    uint32_t* v_idx = (uint32_t*)(smem + Lay::o_vidx);
+    P* v_act = (P*)(smem + Lay::o_vact);
+    __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
+    __shared__ long long s_gbase[RADIX];
+    __shared__ uint32_t s_scan[SORT_WARPS + 1];
+    __shared__ uint32_t s_tile;
+    __shared__ __align__(8) uint64_t s_bar;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_tile = atomicAdd(a.tile_counter, 1u);
+        mbar_init(&s_bar, 1);
+    }
+    for (int i = tid; i < SORT_WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * SORT_TILE;
+    const int64_t nv64 = a.n - base;
+    const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
+    const bool gen_idx = WITH_IDX && a.in_idx == nullptr;
+
+    // ---- tile load: TMA bulk copies for full aligned tiles, plain loads otherwise
+    if (nvalid == SORT_TILE && a.aligned) {
+        if (tid == 0) {
+            const uint32_t bytes = SORT_TILE * (uint32_t)(8 + sizeof(P) + (FROM_COLS ? 4 : 0) +
+                                                          ((WITH_IDX && !gen_idx) ? 4 : 0));
+            mbar_expect_tx(&s_bar, bytes);
+            if (FROM_COLS) {
+                tma_load_1d(u_ts, a.in_ts + base, SORT_TILE * 8, &s_bar);
+                tma_load_1d(u_case, a.in_case + base, SORT_TILE * 4, &s_bar);
+            } else {
+                tma_load_1d(u_key, a.in_key + base, SORT_TILE * 8, &s_bar);
+            }
+            if (WITH_IDX && !gen_idx) tma_load_1d(u_idx, a.in_idx + base, SORT_TILE * 4, &s_bar);
+            tma_load_1d(u_act, a.in_act + base, SORT_TILE * sizeof(P), &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
+    } else {
+        for (uint32_t i = tid; i < nvalid; i += SORT_THREADS) {
+            if (FROM_COLS) {
+                u_ts[i] = a.in_ts[base + i];
+                u_case[i] = a.in_case[base + i];
+            } else {
+                u_key[i] = a.in_key[base + i];
+            }
+            if (WITH_IDX && !gen_idx) u_idx[i] = a.in_idx[base + i];
+            u_act[i] = a.in_act[base + i];
+        }
+        __syncthreads();
+    }
+
+    os_tile<P, FROM_COLS, WITH_IDX, HI>(a, tile, nvalid, u_key, u_ts, u_case, u_idx, u_act, v_idx, v_act,
+                                        s_whist, s_gbase, s_scan);
+}
+
+// Persistent form of a key pass (keys + a u8/u16 activity, no ingest row):
+// each CTA claims tiles in order and prefetches its NEXT tile with TMA into
+// the second of two smem buffers while it ranks and writes out the current
+// one, so the load latency (13% of the stall samples of the one-tile-per-CTA
+// kernel, ncu source view) hides behind the previous tile's work.  Look-back
+// safety: a CTA holds at most two claimed tiles and finishes the older first,
+// so the oldest unfinished tile is always being processed.
+template <class P>
+struct OsPfLayout {
+    static constexpr size_t T = SORT_TILE;
+    static constexpr size_t o_act = T * 8;
+    static constexpr size_t buf = (T * 8 + T * sizeof(P) + 15) / 16 * 16;
+    static constexpr size_t o_vact = 2 * buf;
+    static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
+};
+
+template <class P, bool HI>
+__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf(PassArgs<P, false, false> a, uint32_t n_tiles) {
+    using Lay = OsPfLayout<P>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    P* v_act = (P*)(smem + Lay::o_vact);
+    __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
+    __shared__ long long s_gbase[RADIX];
+    __shared__ uint32_t s_scan[SORT_WARPS + 1];
+    __shared__ uint32_t s_tile[2];
+    __shared__ __align__(8) uint64_t s_bar[2];
+
+    const int tid = threadIdx.x;
+    // full tiles of 16-byte aligned inputs come by TMA; the ragged last tile by plain loads
+    auto bulk = [&](uint32_t t) { return a.aligned && (int64_t)(t + 1) * SORT_TILE <= a.n; };
+    auto issue = [&](uint32_t t, int b) {   // thread 0
+        if (t < n_tiles && bulk(t)) {
+            unsigned char* buf = smem + b * Lay::buf;
+            mbar_expect_tx(&s_bar[b], SORT_TILE * (uint32_t)(8 + sizeof(P)));
+            tma_load_1d(buf, a.in_key + (int64_t)t * SORT_TILE, SORT_TILE * 8, &s_bar[b]);
+            tma_load_1d(buf + Lay::o_act, a.in_act + (int64_t)t * SORT_TILE, SORT_TILE * sizeof(P), &s_bar[b]);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        const uint32_t t = atomicAdd(a.tile_counter, 1u);
+        s_tile[0] = t;
+        issue(t, 0);
+    }
+    uint32_t ph = 0;   // mbarrier parity of each buffer (bit b)
+    for (int b = 0;; b ^= 1) {
+        for (int i = tid; i < SORT_WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
+        // the other buffer was written through the generic proxy (in-place
+        // permutation) by the previous tile: order that before the TMA refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        const uint32_t tile = s_tile[b];
+        if (tile >= n_tiles) break;
+        if (tid == 0) {
+            const uint32_t t = atomicAdd(a.tile_counter, 1u);
+            s_tile[b ^ 1] = t;   // read after the next iteration's barrier
+            issue(t, b ^ 1);
+        }
+        uint64_t* u_key = (uint64_t*)(smem + b * Lay::buf);
+        P* u_act = (P*)(smem + b * Lay::buf + Lay::o_act);
+        const int64_t base = (int64_t)tile * SORT_TILE;
+        const int64_t nv64 = a.n - base;
+        const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
+        if (bulk(tile)) {
+            mbar_wait(&s_bar[b], (ph >> b) & 1u);
+            ph ^= 1u << b;
+        } else {
+            for (uint32_t i = tid; i < nvalid; i += SORT_THREADS) {
+                u_key[i] = a.in_key[base + i];
+                u_act[i] = a.in_act[base + i];
+            }
+            __syncthreads();
+        }
+        os_tile<P, false, false, HI>(a, tile, nvalid, u_key, nullptr, nullptr, nullptr, u_act, nullptr, v_act,
+                                     s_whist, s_gbase, s_scan);
+    }
+}
+
 template <class P, bool FC, bool WI, bool HI>
 static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                  const char* name, double bytes) {
+    if constexpr (!FC && !WI && sizeof(P) <= 2) {   // persistent, prefetching form (2 CTAs per SM)
+        if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF")) {
+            const size_t smem = OsPfLayout<P>::bytes;
+            PM4G_MAX_SMEM(k_onesweep_pf<P, HI>);
+            static int per_sm = -1;
+            if (per_sm < 0)
+                PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pf<P, HI>,
+                                                                      SORT_THREADS, smem));
+            if (per_sm >= 2) {
+                const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)per_sm * num_sms());
+                PM4G_LAUNCH(name, bytes, s,
+                            (k_onesweep_pf<P, HI><<<grid, SORT_THREADS, smem, s>>>(args, (uint32_t)tiles)));
+                return PM4G_OK;
+            }
+        }
+    }
     const size_t smem = OsLayout<P, FC, WI>::bytes;
     PM4G_MAX_SMEM(k_onesweep<P, FC, WI, HI>);
     PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI, HI><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
