@@ -248,3 +248,23 @@ def test_digit_shift_boundaries(ts_bits, case_bits):
     if case_bits + ts_bits > 64:
         pytest.skip("key wider than 64 bits")
     check_log(case.tolist(), act.tolist(), ts.tolist(), 5, n_case_codes=int(case.max()) + 1)
+
+
+@pytest.mark.parametrize("act_bits", [8, 16])
+def test_persistent_prefetch_key_passes(monkeypatch, act_bits):
+    """Key passes above 2 x SMs tiles run the persistent, prefetching onesweep
+    (k_onesweep_pf: next tile TMA-loaded into a second buffer); below, or with
+    PM4G_NO_OS_PF, the one-tile-per-CTA kernel.  Both must equal the oracle on a
+    log with 3 case digits (2 key passes), several tiles per CTA and a ragged
+    last tile."""
+    rng = np.random.default_rng(act_bits)
+    n = 1_500_007                       # 367 tiles of 4096 + a ragged tail
+    ncases = 300_000                    # 19 case bits -> pass 0 + 2 key passes
+    case = rng.integers(0, ncases, n)
+    A = 200 if act_bits == 8 else 700   # u8 / u16 activities
+    act = rng.integers(0, A, n)
+    ts = rng.integers(0, 10**9, n)
+    r = oracle.run(case, act, ts, A)
+    assert_parity(gpu_run(case, act, ts, A, n_case_codes=ncases), r)
+    monkeypatch.setenv("PM4G_NO_OS_PF", "1")
+    assert_parity(gpu_run(case, act, ts, A, n_case_codes=ncases), r)

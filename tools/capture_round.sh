@@ -10,3 +10,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/p
 timeout 900 python bench.py --config 1B --filter --steps 5 --warmup 3 --cpu-cases 2000000 > gpurun_out/prof/bench_1B.json 2> gpurun_out/prof/bench_1B.err
 for c in tiny roadtraffic bpic2019; do timeout 300 python bench.py --config $c --steps 100 --warmup 10 --cpu-cases 300000 >> gpurun_out/prof/bench_small.jsonl 2>> gpurun_out/prof/bench_small.err; done
 ls -la gpurun_out/prof
+for r in 0 7; do timeout 600 python bench.py --config 1B --filter --emulate $r/8 --steps 10 --warmup 3 --cpu-cases 300000 > gpurun_out/prof/bench_1B_shard${r}of8.json 2>> gpurun_out/prof/bench_1B_shard.err; done
+timeout 300 python bench.py --stages --no-cpu-baseline --e2e-steps 0 > /dev/null 2> gpurun_out/prof/stages_100M.txt
