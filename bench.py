@@ -18,7 +18,8 @@ global log of N*100M events).  Inputs (1.3 GB/GPU) are larger than L2.
 Rank 0 prints ONE JSON line.  `value` = total input events of all ranks / max
 over ranks of the device time of the K timed steps.  `e2e` = the same metric
 through the C-ABI with HOST input buffers (pinned; H2D inside the call) and a
-D2H read of every result.  `roofline` = the dominant kernel (k_onesweep, the
+D2H read of every result; step k+1's ingest (H2D + validation) runs on its
+own stream and host thread under step k's compute and D2H.  `roofline` = the dominant kernel (k_onesweep, the
 radix scatter pass) -- algorithmic bytes / CUDA-event time of its launches in
 the timed region, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the
 oracle (single-threaded C++) on a bounded sample of the same workload.
@@ -27,6 +28,7 @@ oracle (single-threaded C++) on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import concurrent.futures
 import json
 import os
 import statistics
@@ -121,11 +123,18 @@ def make_shard(cfg: str, rank: int, world: int, device, strong: bool = False):
     return case.contiguous(), act.contiguous(), ts, meta, spec
 
 
-def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None, info=None):
+def ingest(pm4g, case, act, ts, meta, host=False, stream=None):
+    """pm4g_log_create: columns (device, borrowed; or pinned host, copied H2D) -> validated log."""
+    return pm4g.pm4g_log_create(case, act, ts, meta["A"], n_case_codes=meta["n_case_codes"],
+                                case_lo=meta["case_lo"], case_hi=meta["case_hi"], borrow=not host,
+                                stream=stream)
+
+
+def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None, info=None, log=None):
     tick = (lambda nm: trace.append((nm, time.perf_counter()))) if trace is not None else (lambda nm: None)
     tick("start")
-    log = pm4g.pm4g_log_create(case, act, ts, meta["A"], n_case_codes=meta["n_case_codes"],
-                               case_lo=meta["case_lo"], case_hi=meta["case_hi"], borrow=not host)
+    if log is None:
+        log = ingest(pm4g, case, act, ts, meta, host)
     tick("log_create")
     if filt is not None:
         f = log.filter_time(filt[0], filt[1], pm4g.PM4G_TIME_EVENTS)
@@ -252,7 +261,7 @@ def main():
     ap.add_argument("--config", default="100M")
     ap.add_argument("--impl", default="pm4g", choices=["pm4g", "reference"])
     ap.add_argument("--filter", action="store_true", help="events-mode time filter in the step (1B-style)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-cases", type=int, default=4_000_000)
     ap.add_argument("--ref-cases", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -349,9 +358,46 @@ def main():
         d2h = 0
         hosts = {}
 
-        def e2e_step():
+        # Ingest of step k+1 -- the H2D copy of its columns from pinned memory into one of two
+        # device column sets, then pm4g_log_create (validation) on them -- runs on its own
+        # stream and host thread while step k sorts / analyses / copies its results back: the
+        # copy engine, not the SMs, bounds this path (PCIe, 13 B/event in).  A column set is
+        # refilled only after the step that read it has drained (event on the compute stream).
+        ing_stream = torch.cuda.Stream(device=dev)
+        pool = concurrent.futures.ThreadPoolExecutor(1, initializer=torch.cuda.set_device, initargs=(dev,))
+        pending = []
+        pipelined = n_local * 13 >= (64 << 20)
+        dcols = [tuple(torch.empty_like(x, device=dev) for x in (hc, ha, ht)) for _ in range(2 if pipelined else 0)]
+        drained = [None, None]
+        n_ingest = [0]
+
+        def ingest_async():
+            slot = n_ingest[0] % 2
+            n_ingest[0] += 1
+            wait = drained[slot]
+
+            def work():
+                with torch.cuda.stream(ing_stream):
+                    if wait is not None:
+                        ing_stream.wait_event(wait)
+                    for d, h in zip(dcols[slot], (hc, ha, ht)):
+                        d.copy_(h, non_blocking=True)
+                    return slot, ingest(pm4g, *dcols[slot], meta, False, ing_stream)
+            if pipelined:
+                pending.append(pool.submit(work))
+            else:   # small steps: pm4g_log_create copies the pinned host columns itself
+                f = concurrent.futures.Future()
+                f.set_result((slot, ingest(pm4g, hc, ha, ht, meta, True)))
+                pending.append(f)
+
+        def e2e_step(prefetch):
             nonlocal d2h
-            res, v = run_step(pm4g, hc, ha, ht, meta, comm, out, filt, host=True)
+            slot, log = pending.pop(0).result()
+            if prefetch:
+                ingest_async()
+            res, v = run_step(pm4g, None, None, None, meta, comm, out, filt, log=log)
+            drained[slot] = torch.cuda.Event()
+            drained[slot].record(stream)
             tabs = v.get()
             d2h = 0
             for k in ("cnt", "dur_sum", "mean", "start", "end", "case_code", "n_events", "dur"):
@@ -366,16 +412,20 @@ def main():
                 d2h += x.numel() * x.element_size()
             v.close()
 
-        e2e_step()
+        ingest_async()
+        e2e_step(False)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
+        ing_stream.wait_event(f0)
+        ingest_async()
+        for k in range(args.e2e_steps):
+            e2e_step(k + 1 < args.e2e_steps)
         f1.record(stream)
         torch.cuda.synchronize()
+        pool.shutdown()
         ems = f0.elapsed_time(f1)
         if dist:
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
@@ -383,7 +433,9 @@ def main():
             ems = float(t.item())
         e2e = {"value": n_total * args.e2e_steps / (ems / 1e3), "unit": "events/s",
                "h2d_bytes_per_step": n_local * (4 + act.element_size() + 8), "d2h_bytes_per_step": d2h,
-               "ms_per_step": ems / args.e2e_steps}
+               "ms_per_step": ems / args.e2e_steps,
+               "overlap": ("double-buffered: step k+1's H2D + validation (own stream and host thread) "
+                           "runs under step k's sort/analyze and D2H") if pipelined else "none (small step)"}
 
     # ---------------- roofline of the dominant kernel
     peak, peak_src = _peaks()
