@@ -529,7 +529,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
 // case offsets; each case owned by this tile (head inside it) is sorted by key
 // in shared memory.  A case may run up to FMT_EXT positions past the tile end;
 // longer ones (and cases over FMT_WARP_MAX rows) go to the exact fallback.
-constexpr int FMT_THREADS = 256, FMT_IPT = 16, FMT_TILE = FMT_THREADS * FMT_IPT;
+constexpr int FMT_THREADS = 512, FMT_IPT = 8, FMT_TILE = FMT_THREADS * FMT_IPT;
 constexpr int FMT_EXT = 512, FMT_BUF = FMT_TILE + FMT_EXT;
 constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
 
