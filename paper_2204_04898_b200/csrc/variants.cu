@@ -98,15 +98,23 @@ __device__ __forceinline__ uint64_t table_slot(Slot* table, uint64_t mask, uint6
 
 // Claimed slots, counted once per warp (ctl[1]); past the load limit (3/4 of
 // the table) the table is abandoned (ctl[0] = 1), so an undersized table costs
-// O(limit) claims instead of being probed to saturation.  Called by the active
-// lanes together.
-__device__ __forceinline__ void claim_count(bool claimed, uint32_t* ctl, uint32_t limit) {
+// O(limit) claims instead of being probed to saturation.  Every claimed slot is
+// appended to clist (claim order), so the compaction visits the claimed slots
+// only, not the whole table.  Called by the active lanes together.
+__device__ __forceinline__ void claim_count(bool claimed, uint64_t g, uint32_t* ctl, uint32_t limit,
+                                            uint32_t* __restrict__ clist) {
     const uint32_t m = __activemask();
     const uint32_t b = __ballot_sync(m, claimed);
-    if (b && (threadIdx.x & 31) == __ffs(m) - 1) {
+    if (!b) return;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)(threadIdx.x & 31) == leader) {
         const uint32_t c = __popc(b);
-        if (atomicAdd(&ctl[1], c) + c > limit) atomicExch(ctl, 1u);
+        base = atomicAdd(&ctl[1], c);
+        if (base + c > limit) atomicExch(ctl, 1u);
     }
+    base = __shfl_sync(m, base, leader);
+    if (claimed) clist[base + __popc(b & lanemask_lt())] = (uint32_t)g;
 }
 
 // Items: t in [0, n_items) -> item list[t] (or t).  Each CTA first aggregates a
@@ -122,7 +130,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
     const uint64_t* __restrict__ k2, const OFF* __restrict__ off, const uint64_t* __restrict__ weight,
     const uint32_t* __restrict__ order, Slot* table, uint64_t mask, uint32_t limit, uint64_t salt,
     uint32_t* __restrict__ item_slot, uint8_t* __restrict__ pending, uint32_t* ctl,
-    const uint64_t* __restrict__ d_n) {
+    const uint64_t* __restrict__ d_n, uint32_t* __restrict__ clist) {
     extern __shared__ __align__(16) unsigned char ins_sm[];
     unsigned long long* s_k1 = (unsigned long long*)ins_sm;
     unsigned long long* s_k2 = s_k1 + INS_SLOTS;
@@ -218,7 +226,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
             const int sl = s_list[q];
             bool claimed = false;
             uint64_t g = table_slot(table, mask, s_k1[sl], s_k2[sl], ctl, &claimed);
-            claim_count(claimed, ctl, limit);
+            claim_count(claimed, g, ctl, limit, clist);
             s_g[sl] = g;
             if (g == ~0ull) continue;
             atomicAdd(&table[g].weight, (unsigned long long)s_w[sl]);
@@ -232,7 +240,7 @@ __global__ __launch_bounds__(INS_THREADS) void k_insert(
             if (direct[u]) {
                 bool claimed = false;
                 g = table_slot(table, mask, ka[u], kb[u], ctl, &claimed);
-                claim_count(claimed, ctl, limit);
+                claim_count(claimed, g, ctl, limit, clist);
                 if (g != ~0ull) {
                     atomicAdd(&table[g].weight, (unsigned long long)w[u]);
                     atomicMin(&table[g].rep, ord[u]);
@@ -324,12 +332,14 @@ __global__ void k_rep_item(const uint32_t* __restrict__ list, uint64_t n_items,
     }
 }
 
-// occupied slots with weight > 0 -> groups (append order is irrelevant: the
-// final sort is a total order)
+// claimed slots (clist) with weight > 0 -> groups (append order is irrelevant:
+// the final sort is a total order)
 // also sums the new groups' sequence lengths (one atomic per block) so the
 // host learns the total variant length with the round's counters
 template <class OFF>
 __global__ __launch_bounds__(256) void k_compact(const Slot* __restrict__ table, uint64_t cap,
+                                                 const uint32_t* __restrict__ clist,
+                                                 const uint32_t* __restrict__ n_claims,
                                                  const uint32_t* __restrict__ item_of_rep_slot,
                                                  uint32_t* __restrict__ slot_group, uint64_t* __restrict__ g_weight,
                                                  uint32_t* __restrict__ g_rep_item, uint32_t* __restrict__ g_order,
@@ -340,8 +350,10 @@ __global__ __launch_bounds__(256) void k_compact(const Slot* __restrict__ table,
     if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
     unsigned long long tl = 0;
-    for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < cap;
-         sl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t nc = min((uint64_t)*n_claims, cap);
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nc;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sl = clist[q];
         const Slot& s = table[sl];
         if ((s.k1 | s.k2) == 0 || s.weight == 0) continue;
         uint32_t g = atomicAdd(n_groups, 1u);
@@ -498,10 +510,11 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
         for (int attempt = 0;; ++attempt) {
             Scratch tab(s), aux(s);
             if ((st = tab.alloc(cap * sizeof(Slot)))) return bail(st);
-            if ((st = aux.alloc(cap * 8))) return bail(st);
+            if ((st = aux.alloc(cap * 12))) return bail(st);
             Slot* table = tab.as<Slot>();
             uint32_t* item_of_rep_slot = aux.as<uint32_t>();
             uint32_t* slot_group = item_of_rep_slot + cap;
+            uint32_t* clist = slot_group + cap;   // claimed slots, claim order
             PM4G_LAUNCH("k_variant_init", cap * 32.0, s, (k_init_table<<<gsz(cap), 256, 0, s>>>(table, cap)));
             PM4G_CK(cudaMemsetAsync(counters, 0, 12, s));
             const uint32_t limit = cap == full ? 0xffffffffu : (uint32_t)(cap / 4 * 3);
@@ -515,7 +528,7 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                 PM4G_LAUNCH("k_variant_insert", n_active * 24.0, s,
                             (k_insert<OFF><<<gi, INS_THREADS, INS_SMEM, s>>>(
                                 list, n_active, k1, k2, off, weight, order, table, cap - 1, limit, salt,
-                                item_slot, pending, counters + 1, list ? nullptr : d_n)));
+                                item_slot, pending, counters + 1, list ? nullptr : d_n, clist)));
             }
             uint32_t* ior = order ? item_of_rep_slot : nullptr;   // identity order: rep item = slot.rep
             if (order)
@@ -527,8 +540,8 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                                                                ior, table, item_slot,
                                                                pending, next_list, counters, counters + 1,
                                                                list ? nullptr : d_n)));
-            PM4G_LAUNCH("k_variant_compact", cap * 32.0, s,
-                        (k_compact<OFF><<<gsz(cap), 256, 0, s>>>(table, cap, ior, slot_group,
+            PM4G_LAUNCH("k_variant_compact", n_active * 8.0, s,
+                        (k_compact<OFF><<<gsz(n_active), 256, 0, s>>>(table, cap, clist, counters + 2, ior, slot_group,
                                                                  g.weight, g.rep_item, g.order,
                                                                  counters + 3, counters + 1, off, d_total)));
             PM4G_LAUNCH("k_variant_item_group", n_active * 12.0, s,
