@@ -310,6 +310,8 @@ pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4
 pm4g_status fetch_n_cases(const pm4g_log* L, cudaStream_t s);
 pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits,
                            cudaStream_t s);  // generic: (key, u32 payload), in place
+pm4g_status radix_sort_u64_to(const uint64_t* keys, const uint32_t* vals, uint32_t* vals_out, int64_t n,
+                              int bits, cudaStream_t s);  // payload only, to vals_out != vals
 pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s);
 
 // Variant-key hash (internal, verified): Horner polynomial mod 2^64 over

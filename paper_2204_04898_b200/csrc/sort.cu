@@ -1061,6 +1061,22 @@ pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, 
     return PM4G_OK;
 }
 
+// (key, u32 payload) sorted by key; only the payload is kept, written straight
+// to vals_out (distinct from vals): no copy-back of the result
+pm4g_status radix_sort_u64_to(const uint64_t* keys, const uint32_t* vals, uint32_t* vals_out, int64_t n,
+                              int bits, cudaStream_t s) {
+    if (n <= 0) return PM4G_OK;
+    if (n == 1) {
+        PM4G_CK(cudaMemcpyAsync(vals_out, vals, 4, cudaMemcpyDeviceToDevice, s));
+        return PM4G_OK;
+    }
+    Scratch ko(s);
+    PM4G_TRY(ko.alloc((size_t)n * 8 + 16));
+    KeyParams kp{0, 0, 0};
+    return lsd_sort<uint32_t, false>(nullptr, nullptr, keys, vals, nullptr, ko.as<uint64_t>(), vals_out, nullptr, n, 0,
+                                     std::max(1, std::min(bits, 64)), kp, s, "k_onesweep_small");
+}
+
 // ------------------------------------------------------------------ decode (formatted log view)
 template <class P>
 __global__ void k_decode(const uint64_t* __restrict__ key, const P* __restrict__ sact, int64_t n,

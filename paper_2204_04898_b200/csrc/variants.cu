@@ -575,20 +575,21 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
     g.G = G;
     // sort groups: count desc, order asc
     const int wbits = weight ? 32 : std::max(1, bit_width_u64(n_items));
-    Scratch sk(s);
-    if ((st = sk.alloc(G * 8 + 16))) return bail(st);
+    Scratch sk(s);   // keys [G] u64 | group ids [G] u32 (the radix payload)
+    if ((st = sk.alloc(G * 12 + 16))) return bail(st);
+    uint32_t* sk_val = (uint32_t*)(sk.as<uint64_t>() + G);
     if ((st = dalloc_t(&g.sorted, std::max<uint64_t>(G, 1), s))) return bail(st);
     if ((st = dalloc_t(&g.inv, std::max<uint64_t>(G, 1), s))) return bail(st);
     PM4G_LAUNCH("k_variant_sortkeys", G * 16.0, s,
                 (k_sort_keys<<<gsz(G), 256, 0, s>>>(g.weight, g.order, G, wbits, order_bits, sk.as<uint64_t>(),
-                                                     g.sorted)));
+                                                     sk_val)));
     if (G <= RANK_SORT_MAX) {
         if (G)
             PM4G_LAUNCH("k_rank_sort", G * 8.0 + G * 4.0, s,
                         (k_rank_sort<<<(unsigned)((G + 255) / 256), 256, 0, s>>>(sk.as<uint64_t>(), (uint32_t)G,
                                                                                g.sorted)));
     } else {
-        PM4G_TRY(radix_sort_u64(sk.as<uint64_t>(), g.sorted, (int64_t)G, wbits + order_bits, s));
+        PM4G_TRY(radix_sort_u64_to(sk.as<uint64_t>(), sk_val, g.sorted, (int64_t)G, wbits + order_bits, s));
     }
     PM4G_LAUNCH("k_variant_inv", G * 8.0, s, (k_inv<<<gsz(G), 256, 0, s>>>(g.sorted, G, g.inv)));
     *out = g;
