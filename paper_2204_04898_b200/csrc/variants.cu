@@ -297,37 +297,40 @@ __global__ void k_verify(const uint32_t* __restrict__ list, uint64_t n_items,
                          const uint32_t* __restrict__ overflow, const uint64_t* __restrict__ d_n) {
     if (*overflow) return;   // this attempt's table is abandoned (item_slot incomplete)
     if (d_n) n_items = min(n_items, *d_n);
-    // two items per trip, their dependent loads (slot -> rep -> offsets ->
+    // VU items per trip, their dependent loads (slot -> rep -> offsets ->
     // sequences) interleaved: the kernel is L2-latency bound
+    constexpr int VU = 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items; t += 2 * stride) {
-        const uint64_t t2 = t + stride;
-        const bool two = t2 < n_items;
-        uint32_t it[2], sl[2], ord[2], rep[2], rep_it[2];
-        it[0] = list ? list[t] : (uint32_t)t;
-        it[1] = two ? (list ? list[t2] : (uint32_t)t2) : it[0];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items; t += VU * stride) {
+        uint32_t it[VU], sl[VU], ord[VU], rep[VU], rep_it[VU];
+        bool ok[VU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < VU; ++u) {
+            const uint64_t tu = t + u * stride;
+            ok[u] = tu < n_items;
+            it[u] = ok[u] ? (list ? list[tu] : (uint32_t)tu) : (list ? list[t] : (uint32_t)t);
+        }
+#pragma unroll
+        for (int u = 0; u < VU; ++u) {
             sl[u] = item_slot[it[u]];
             ord[u] = order ? order[it[u]] : it[u];
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) rep[u] = table[sl[u]].rep;
+        for (int u = 0; u < VU; ++u) rep[u] = table[sl[u]].rep;
         // with the identity order the representative item IS the slot's rep
 #pragma unroll
-        for (int u = 0; u < 2; ++u) rep_it[u] = order ? item_of_rep_slot[sl[u]] : rep[u];
-        OFF f[2], l[2], rf[2], rl[2];
+        for (int u = 0; u < VU; ++u) rep_it[u] = order ? item_of_rep_slot[sl[u]] : rep[u];
+        OFF f[VU], l[VU], rf[VU], rl[VU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < VU; ++u) {
             f[u] = off[it[u]];
             l[u] = off[it[u] + 1];
             rf[u] = off[rep_it[u]];
             rl[u] = off[rep_it[u] + 1];
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) break;
-            if (rep[u] == ord[u]) continue;                 // the representative itself
+        for (int u = 0; u < VU; ++u) {
+            if (!ok[u] || rep[u] == ord[u]) continue;        // past the end / the representative itself
             bool same = (l[u] - f[u]) == (rl[u] - rf[u]);
             if (same) same = seq_equal(acts, (uint64_t)f[u], (uint64_t)rf[u], (uint64_t)(l[u] - f[u]));
             if (!same) {
