@@ -230,9 +230,11 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
                                                   const int64_t* __restrict__ ts, int64_t n, uint32_t lo,
                                                   uint32_t hi, uint32_t A, Meta* m, int hpasses, int hbits,
                                                   uint32_t* __restrict__ hist) {
-    __shared__ uint32_t sh[4][256];
-    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    // per-warp digit histograms (same-address atomics only within a warp)
+    __shared__ uint32_t shw[8][4][256];
+    for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&shw[0][0][0])[i] = 0;
     __syncthreads();
+    uint32_t (*sh)[256] = shw[threadIdx.x >> 5];
     long long tmin = LLONG_MAX, tmax = LLONG_MIN;
     unsigned cmin = 0xffffffffu, cmax = 0;
     unsigned long long bc = ~0ull, ba = ~0ull;
@@ -278,7 +280,9 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
     }
     __syncthreads();
     for (int i = threadIdx.x; i < hpasses * 256; i += blockDim.x) {
-        const uint32_t v = (&sh[0][0])[i];
+        uint32_t v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += (&shw[w][0][0])[i];
         if (v) atomicAdd(&hist[i], v);
     }
 }
