@@ -141,10 +141,8 @@ def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=
         log.close()
         log = f
         tick("filter_time")
-    log.sort()
-    tick("sort (async)")
-    res = log.analyze(comm=comm, out=out)
-    tick("analyze")
+    res = log.sort_analyze(comm=comm, out=out)   # pm4g_sort + pm4g_analyze in one call
+    tick("sort+analyze")
     if info is not None:
         i = log.info()
         info.update(n=int(i.n_events), C=int(i.n_cases))

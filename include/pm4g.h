@@ -234,6 +234,19 @@ typedef struct pm4g_outputs {
 pm4g_status pm4g_analyze(const pm4g_log* log, const pm4g_outputs* out, pm4g_comm* comm,
                          pm4g_stream_t stream);
 
+/* pm4g_sort then pm4g_analyze (format.apply, then the aggregates) in
+ * one call, with identical results.  The sort's host check for cases the
+ * in-shared-memory ranking cannot take (longer than 1024 rows, or running far
+ * past a tile; S:184-192 still holds for them via an exact radix sort) is
+ * folded into the analysis' own synchronisation instead of costing a separate
+ * round trip: if such cases exist, they are sorted exactly and the analysis is
+ * recomputed before the call returns.  Falls back to the two separate calls
+ * when comm != NULL, when no variants are requested (no synchronisation to
+ * share), or when the log has extra columns.  An already formatted log is only
+ * analysed.  Errors: those of pm4g_sort and pm4g_analyze. */
+pm4g_status pm4g_sort_analyze(pm4g_log* log, const pm4g_outputs* out, pm4g_comm* comm,
+                              pm4g_stream_t stream);
+
 /* ---------------------------------------------------------------- filters
  * Return a NEW log (in the state -- ingested or formatted -- of `in`) holding
  * the kept rows in their original relative order.  Kept cases keep

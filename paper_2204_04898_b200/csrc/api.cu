@@ -600,18 +600,46 @@ pm4g_status pm4g_log_info_get(const pm4g_log* L, pm4g_log_info* info) {
     return PM4G_OK;
 }
 
-pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
-    if (!L) return fail(PM4G_EINVAL, "null log");
-    if (L->sorted) return PM4G_OK;
-    cudaStream_t s = (cudaStream_t)stream;
+static pm4g_status sort_impl(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     if (L->key_bits > 64)
         return fail(PM4G_EKEYWIDTH, "case_bits + ts_bits = " + std::to_string(L->key_bits) +
                                         " > 64: composite key does not fit");
-    PM4G_TRY(sort_log(L, s));   // sort + case offsets (format kernel)
+    PM4G_TRY(sort_log(L, s, d));   // sort + case offsets (format kernel)
     free_log_cols(L, s);
     L->sorted = true;
     L->stream = s;
     return PM4G_OK;
+}
+
+pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
+    if (!L) return fail(PM4G_EINVAL, "null log");
+    if (L->sorted) return PM4G_OK;
+    return sort_impl(L, (cudaStream_t)stream, nullptr);
+}
+
+pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* comm, pm4g_stream_t stream) {
+    if (!L) return fail(PM4G_EINVAL, "null log");
+    if (!out) return fail(PM4G_EINVAL, "null outputs");
+    if (L->sorted) return pm4g_analyze(L, out, comm, stream);
+    if (comm || !out->variants) {
+        PM4G_TRY(pm4g_sort(L, stream));
+        return pm4g_analyze(L, out, comm, stream);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    FmtDeferred d(s);
+    PM4G_TRY(sort_impl(L, s, &d));
+    // the analysis synchronises (variant counters); the deferred format check
+    // then costs no extra wait
+    pm4g_status st = pm4g_analyze(L, out, comm, stream);
+    bool fixed = false;
+    const pm4g_status fs = sort_finish(&d, s, &fixed);
+    if (fs != PM4G_OK) return fs;
+    if (fixed) {   // some cases were re-sorted exactly: recompute from the final order
+        if (st == PM4G_OK && *out->variants) pm4g_variants_destroy(*out->variants);
+        *out->variants = nullptr;
+        st = pm4g_analyze(L, out, comm, stream);
+    }
+    return st;
 }
 
 }  // extern "C"

@@ -86,6 +86,12 @@ struct Scratch {
     ~Scratch() { if (p) dfree(p, s); }
     pm4g_status alloc(size_t bytes) { return dalloc(&p, bytes ? bytes : 16, s); }
     template <class T> T* as() const { return (T*)p; }
+    void take(Scratch& o) {   // ownership moves here
+        if (p) dfree(p, s);
+        p = o.p;
+        s = o.s;
+        o.p = nullptr;
+    }
 };
 
 // ------------------------------------------------------------------ the log
@@ -305,7 +311,22 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s);   // K1
 void hist_layout(const pm4g_log* L, int* hpasses, int* hbits);
 void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, uint32_t case_max,
                 int hpasses, int hbits);
-pm4g_status sort_log(pm4g_log* L, cudaStream_t s);            // A2-A4
+// A sort whose format fallback (cases k_format cannot sort in shared memory) is
+// deferred to the caller's next host synchronisation: sort_log(L, s, &d) returns
+// without waiting; sort_finish(&d, s, &fixed) then waits, runs the fallback if
+// any case needs it and says so (the caller recomputes what it derived from
+// the log meanwhile).
+struct FmtDeferred {
+    Scratch grp, st;                        // grouped keys (fallback input), format scratch
+    alignas(16) unsigned char fa_raw[256];  // the format arguments (type-erased FmtArgs<P>)
+    int act_bytes = 1;
+    bool active = false;
+    uint32_t* h_nbig = nullptr;             // pinned: fallback count, copied after k_format
+    cudaEvent_t ev = nullptr;               // recorded after that copy
+    explicit FmtDeferred(cudaStream_t s) : grp(s), st(s) {}
+};
+pm4g_status sort_log(pm4g_log* L, cudaStream_t s, FmtDeferred* d = nullptr);   // A2-A4
+pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed);
 pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4
 pm4g_status fetch_n_cases(const pm4g_log* L, cudaStream_t s);
 pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits,

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "pm4g_internal.cuh"
@@ -791,12 +792,11 @@ __global__ void k_big_gather(FmtArgs<P> a, int64_t start, int64_t len, const uin
     }
 }
 
+// launch k_format; st holds its scratch (tile status, fallback list + count)
 template <class P>
-static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
-    FmtArgs<P> fa = fa0;
+static pm4g_status format_launch(FmtArgs<P>& fa, Scratch& st, cudaStream_t s) {
     const int64_t n = fa.n;
     const int64_t tiles = (n + FMT_TILE - 1) / FMT_TILE;
-    Scratch st(s);
     const size_t words = 2 + (size_t)tiles + ((size_t)n / FMT_WARP_MAX + tiles + 2);
     PM4G_TRY(st.alloc(words * 4));
     PM4G_CK(cudaMemsetAsync(st.p, 0, (2 + tiles) * 4, s));
@@ -815,10 +815,13 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
     else
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, false><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
-    uint32_t nbig = 0;
-    PM4G_CK(cudaMemcpyAsync(&nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
-    PM4G_CK(cudaStreamSynchronize(s));
-    if (nbig == 0) return PM4G_OK;
+    return PM4G_OK;
+}
+
+// the exact fallback for the nbig cases k_format listed (too long, or running
+// too far past a tile): a stable radix sort of each such case's keys
+template <class P>
+static pm4g_status format_fallback(const FmtArgs<P>& fa, uint32_t nbig, cudaStream_t s) {
     std::vector<uint32_t> ranks(nbig);
     PM4G_CK(cudaMemcpyAsync(ranks.data(), fa.big, nbig * 4, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
@@ -840,7 +843,18 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
 }
 
 template <class P>
-static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
+static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
+    FmtArgs<P> fa = fa0;
+    Scratch st(s);
+    PM4G_TRY(format_launch<P>(fa, st, s));
+    uint32_t nbig = 0;
+    PM4G_CK(cudaMemcpyAsync(&nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    return nbig ? format_fallback<P>(fa, nbig, s) : PM4G_OK;
+}
+
+template <class P>
+static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     const int64_t n = L->n;
     const bool wi = !L->extra.empty();
     KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
@@ -873,7 +887,27 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s) {
     fa.off = L->off;
     fa.case_code = L->s_case_code;
     fa.n_cases = L->d_n_cases;
-    return format_log<P>(fa, s);
+    if (!d) return format_log<P>(fa, s);
+    // deferred: no host wait here; the caller runs sort_finish at its next
+    // synchronisation (the grouped keys stay alive for the fallback)
+    d->st.s = s;
+    PM4G_TRY(format_launch<P>(fa, d->st, s));
+    // the fallback count goes to pinned host memory now (stream order); the
+    // caller's own synchronisation later makes it readable without a wait
+    static thread_local uint32_t* h_nbig = nullptr;
+    static thread_local cudaEvent_t ev = nullptr;
+    if (!h_nbig) PM4G_CK(cudaHostAlloc((void**)&h_nbig, 4, cudaHostAllocDefault));
+    if (!ev) PM4G_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PM4G_CK(cudaMemcpyAsync(h_nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaEventRecord(ev, s));
+    d->h_nbig = h_nbig;
+    d->ev = ev;
+    d->grp.take(grp);
+    static_assert(sizeof(FmtArgs<P>) <= sizeof(d->fa_raw), "type-erased FmtArgs");
+    memcpy(d->fa_raw, &fa, sizeof(fa));
+    d->act_bytes = (int)sizeof(P);
+    d->active = true;
+    return PM4G_OK;
 }
 
 // ------------------------------------------------------------------ A4 segments
@@ -1018,7 +1052,30 @@ static pm4g_status gather_extras(pm4g_log* L, cudaStream_t s) {
     return PM4G_OK;
 }
 
-pm4g_status sort_log(pm4g_log* L, cudaStream_t s) {
+template <class P>
+static pm4g_status finish_t(FmtDeferred* d, cudaStream_t s, bool* fixed) {
+    FmtArgs<P> fa;
+    memcpy(&fa, d->fa_raw, sizeof(fa));
+    PM4G_CK(cudaEventSynchronize(d->ev));   // normally complete already: no wait
+    const uint32_t nbig = *d->h_nbig;
+    if (nbig == 0) return PM4G_OK;
+    *fixed = true;
+    return format_fallback<P>(fa, nbig, s);
+}
+
+pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed) {
+    *fixed = false;
+    if (!d->active) return PM4G_OK;
+    d->active = false;
+    switch (d->act_bytes) {
+        case 1: return finish_t<uint8_t>(d, s, fixed);
+        case 2: return finish_t<uint16_t>(d, s, fixed);
+        default: return finish_t<uint32_t>(d, s, fixed);
+    }
+}
+
+pm4g_status sort_log(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
+    if (d && !L->extra.empty()) d = nullptr;   // extra columns are gathered by the final order: no deferral
     const int64_t n = L->n;
     const bool wi = !L->extra.empty();
     // +32 rows: 16-byte aligned TMA reads of the formatted log may run one vector past n
@@ -1038,9 +1095,9 @@ pm4g_status sort_log(pm4g_log* L, cudaStream_t s) {
         return PM4G_OK;
     }
     switch (L->act_bytes) {
-        case 1: PM4G_TRY(sort_log_t<uint8_t>(L, s)); break;
-        case 2: PM4G_TRY(sort_log_t<uint16_t>(L, s)); break;
-        default: PM4G_TRY(sort_log_t<uint32_t>(L, s)); break;
+        case 1: PM4G_TRY(sort_log_t<uint8_t>(L, s, d)); break;
+        case 2: PM4G_TRY(sort_log_t<uint16_t>(L, s, d)); break;
+        default: PM4G_TRY(sort_log_t<uint32_t>(L, s, d)); break;
     }
     if (wi) PM4G_TRY(gather_extras(L, s));
     return PM4G_OK;

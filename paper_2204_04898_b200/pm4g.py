@@ -94,6 +94,7 @@ _SIGS = {
     "pm4g_variants_case_index": ([P, P, P], I32),
     "pm4g_variants_destroy": ([P], I32),
     "pm4g_analyze": ([P, ctypes.POINTER(pm4g_outputs), P, P], I32),
+    "pm4g_sort_analyze": ([P, ctypes.POINTER(pm4g_outputs), P, P], I32),
     "pm4g_filter_time": ([P, I64, I64, I32, P, ctypes.POINTER(P)], I32),
     "pm4g_filter_attr": ([P, I32, ctypes.POINTER(pm4g_pred), I32, I32, P, ctypes.POINTER(P)], I32),
     "pm4g_filter_cases": ([P, ctypes.POINTER(pm4g_case_pred), I32, P, ctypes.POINTER(P)], I32),
@@ -297,7 +298,7 @@ class Log:
         return c.value
 
     def analyze(self, comm=None, stream=None, tables=True, cases=True, variants=True, out=None,
-                minmax=False):
+                minmax=False, _entry="pm4g_analyze"):
         """Fused pass.  ``out``: optional dict of tensors, filled on first use and reused
         by later calls (per-case arrays are sized by case_capacity(), valid up to
         info().n_cases).  ``minmax``: also the per-edge min / max durations."""
@@ -327,11 +328,18 @@ class Log:
                             g("case_code"), g("n_events"), g("dur"),
                             min((o[k].numel() for k in ("case_code", "n_events", "dur") if k in want), default=0),
                             ctypes.pointer(vh) if variants else None, g("dur_min"), g("dur_max"))
-        _check(lib().pm4g_analyze(self.h, ctypes.byref(outs), _comm(comm), _stream(stream)))
+        _check(getattr(lib(), _entry)(self.h, ctypes.byref(outs), _comm(comm), _stream(stream)))
         res = {k: o[k] for k in want}
         if variants:
             res["variants"] = VariantTable(vh)
         return res
+
+    def sort_analyze(self, comm=None, stream=None, tables=True, cases=True, variants=True, out=None,
+                     minmax=False):
+        """pm4g_sort_analyze: sort() then analyze() in one call (same results; the sort's
+        host check is folded into the analysis' synchronisation)."""
+        return self.analyze(comm=comm, stream=stream, tables=tables, cases=cases, variants=variants,
+                            out=out, minmax=minmax, _entry="pm4g_sort_analyze")
 
     def filter_time(self, t1: int, t2: int, mode: int = PM4G_TIME_EVENTS, stream=None) -> "Log":
         out = ctypes.c_void_p()

@@ -26,22 +26,28 @@ def to_device_cols(case, act, ts, A, device="cuda"):
     return case_t.to(device), act_t.contiguous().to(device), ts_t.to(device)
 
 
-def gpu_run(case, act, ts, A, n_case_codes=None, case_lo=0, case_hi=0, sort=True, fused=True):
-    """Build a log on cuda:0, sort it, and return every output on the host."""
+def gpu_run(case, act, ts, A, n_case_codes=None, case_lo=0, case_hi=0, sort=True, fused=True,
+            sort_analyze=False):
+    """Build a log on cuda:0, sort it, and return every output on the host
+    (sort_analyze: one pm4g_sort_analyze call instead of pm4g_sort + pm4g_analyze)."""
     c, a, t = to_device_cols(case, act, ts, A)
     if n_case_codes is None:
         n_case_codes = (int(np.max(np.asarray(case, dtype=np.int64))) + 1) if len(case) else 1
     log = pm4g.pm4g_log_create(c, a, t, A, n_case_codes=n_case_codes, case_lo=case_lo, case_hi=case_hi)
-    log.sort()
-    out = collect(log, fused=fused)
+    if not sort_analyze:
+        log.sort()
+    out = collect(log, fused=fused, sort_analyze=sort_analyze)
     log.close()
     return out
 
 
-def collect(log, fused=True):
+def collect(log, fused=True, sort_analyze=False):
     A = log.A
     res = {}
-    if fused:
+    if sort_analyze:
+        o = log.sort_analyze()
+        vt = o.pop("variants")
+    elif fused:
         o = log.analyze()
         vt = o.pop("variants")
     else:

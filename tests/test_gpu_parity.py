@@ -268,3 +268,41 @@ def test_persistent_prefetch_key_passes(monkeypatch, act_bits):
     assert_parity(gpu_run(case, act, ts, A, n_case_codes=ncases), r)
     monkeypatch.setenv("PM4G_NO_OS_PF", "1")
     assert_parity(gpu_run(case, act, ts, A, n_case_codes=ncases), r)
+
+
+# ---------------------------------------------------------------- pm4g_sort_analyze
+@pytest.mark.parametrize("seed", range(0, 200, 20))
+def test_sort_analyze_random_tiny_logs(seed):
+    case, act, ts, A, ncodes = random_log(seed)
+    assert_parity(gpu_run(case, act, ts, A, n_case_codes=ncodes, sort_analyze=True),
+                  oracle.run(case, act, ts, A))
+
+
+@pytest.mark.parametrize("shape", ["one_long_case", "long_cases_across_tiles", "ragged"])
+def test_sort_analyze_fallback_cases(shape):
+    """Cases k_format leaves to the exact fallback (longer than 1024 rows, or running
+    far past a tile): pm4g_sort_analyze finds them at the analysis' synchronisation,
+    sorts them exactly and recomputes -- results equal the oracle's."""
+    rng = np.random.default_rng(7)
+    if shape == "one_long_case":
+        n = 5000
+        case = np.zeros(n, np.int64)
+    elif shape == "long_cases_across_tiles":
+        n = 40_000
+        case = np.repeat(np.arange(20), n // 20)[rng.permutation(n)]   # 2000-row cases
+    else:
+        n = 3 * 4096 + 17
+        case = rng.integers(0, n // 9, n)
+        case[: 3000] = 5                                               # one 3000+-row case
+        case = case[rng.permutation(n)]
+    act = rng.integers(0, 7, n)
+    ts = rng.integers(0, 10**7, n)
+    assert_parity(gpu_run(case, act, ts, 7, n_case_codes=int(case.max()) + 1, sort_analyze=True),
+                  oracle.run(case, act, ts, 7))
+
+
+def test_sort_analyze_config_bpic2019():
+    L = generate(CONFIGS["bpic2019"])
+    c, a, t = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True),
+                  oracle.run(c, a, t, L.n_activities))
