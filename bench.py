@@ -404,9 +404,11 @@ def main():
                     hosts[k] = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
                 hosts[k].copy_(x, non_blocking=True)
                 d2h += x.numel() * x.element_size()
-            for k, x in tabs.items():
-                hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-                hx.copy_(x, non_blocking=True)
+            for k, x in tabs.items():   # pinned buffers kept across steps (no host allocation in the loop)
+                hk = "v_" + k
+                if hk not in hosts or hosts[hk].dtype != x.dtype or hosts[hk].numel() < x.numel():
+                    hosts[hk] = torch.empty(max(1, 2 * x.numel()), dtype=x.dtype, pin_memory=True)
+                hosts[hk][: x.numel()].copy_(x.reshape(-1), non_blocking=True)
                 d2h += x.numel() * x.element_size()
             v.close()
 
