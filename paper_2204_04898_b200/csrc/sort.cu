@@ -108,6 +108,7 @@ struct PassArgs {
     uint32_t* status;            // [tiles * 256]
     uint32_t* tile_counter;
     bool aligned;                // every input array 16-byte aligned (TMA bulk path)
+    uint32_t* next_status;       // the next pass's look-back words (zeroed here, row per tile), or nullptr
 };
 
 // Shared-memory layout of one tile (all offsets multiples of 16):
@@ -140,6 +141,9 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)tile * SORT_TILE;
     const uint32_t dmask = (1u << a.bits) - 1;
+    // the next pass runs after this kernel: clear its status row for this tile
+    // here instead of a host memset of every pass's status up front
+    if (a.next_status && tid < RADIX) a.next_status[(size_t)tile * RADIX + tid] = 0;
     const bool gen_idx = WITH_IDX && a.in_idx == nullptr;
     // digit of a key: shift < 64 except for a single-case log (no case bits)
     const int sh = a.shift;
@@ -475,7 +479,9 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
     uint32_t* counters = status + status_words;
     uint32_t* hist = counters + passes;
     uint32_t* off = hist + MAX_PASSES * RADIX;
-    PM4G_CK(cudaMemsetAsync(status, 0, (status_words + passes + MAX_PASSES * RADIX) * 4, s));
+    // pass 0's look-back words, the tile counters and histograms; pass p zeroes pass p+1's words
+    PM4G_CK(cudaMemsetAsync(status, 0, (size_t)tiles * RADIX * 4, s));
+    PM4G_CK(cudaMemsetAsync(counters, 0, (passes + MAX_PASSES * RADIX) * 4, s));
     if (pre_hist) {   // histograms already built (by the validation pass)
         PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(pre_hist, off, passes));
     } else {
@@ -509,12 +515,14 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
             PassArgs<P, true, WI> a{nullptr, in_case, in_ts, ca, ci, ok, oa, oi, n, shift, bits, kp,
                                     off, status, counters,
                                     aligned16(in_case) && aligned16(in_ts) && aligned16(ca) &&
-                                        (!ci || aligned16(ci))};
+                                        (!ci || aligned16(ci)),
+                                    p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
             PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
         } else {
             PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, shift, bits, kp,
                                      off + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p,
-                                     aligned16(ck) && aligned16(ca) && (!ci || aligned16(ci))};
+                                     aligned16(ck) && aligned16(ca) && (!ci || aligned16(ci)),
+                                     p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
             PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr)));
         }
         ck = ok;
