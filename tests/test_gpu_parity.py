@@ -306,3 +306,24 @@ def test_sort_analyze_config_bpic2019():
     c, a, t = L.case.numpy(), L.act.numpy(), L.ts.numpy()
     assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True),
                   oracle.run(c, a, t, L.n_activities))
+
+
+@pytest.mark.parametrize("long_case", [False, True])
+def test_sort_analyze_with_extra_columns(long_case):
+    """Logs with extra columns take pm4g_sort_analyze's non-deferred path (the extra
+    columns are gathered by the final order): results equal the oracle's."""
+    from tests.parity import collect
+    rng = np.random.default_rng(11)
+    n = 20_000
+    case = rng.integers(0, 2_000, n)
+    if long_case:
+        case[:3000] = 7                                  # a 3000+-row case: the exact fallback
+        case = case[rng.permutation(n)]
+    act = rng.integers(0, 9, n)
+    ts = rng.integers(0, 10**8, n)
+    c, a, t = to_device_cols(case, act, ts, 9)
+    ex = [pm4g.Extra(pm4g.PM4G_KIND_I64, torch.as_tensor(rng.integers(0, 100, n)).cuda())]
+    log = pm4g.pm4g_log_create(c, a, t, 9, n_case_codes=2_000, extra=ex)
+    g = collect(log, sort_analyze=True)
+    log.close()
+    assert_parity(g, oracle.run(case, act, ts, 9))
