@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "pm4g_internal.cuh"
@@ -573,13 +574,19 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
                         (k_item_group<<<gs, 256, 0, s>>>(list, n_active, item_slot, pending, slot_group,
                                                          g.item_group, counters + 1, list ? nullptr : d_n)));
             // one host round trip per round: next_count, overflow, claims, n_groups
+            // (counters and the length total in one copy, into pinned staging)
             uint32_t h[4] = {0, 0, 0, 0};
             unsigned long long htot = 0;
             uint64_t hn = n_items;
-            PM4G_CK(cudaMemcpyAsync(h, counters, 16, cudaMemcpyDeviceToHost, s));
-            PM4G_CK(cudaMemcpyAsync(&htot, d_total, 8, cudaMemcpyDeviceToHost, s));
-            if (d_n && !list) PM4G_CK(cudaMemcpyAsync(&hn, d_n, 8, cudaMemcpyDeviceToHost, s));
+            static thread_local unsigned char* h_stage = nullptr;
+            if (!h_stage) PM4G_CK(cudaHostAlloc((void**)&h_stage, 64, cudaHostAllocDefault));
+            const size_t o_tot = (size_t)((const char*)d_total - (const char*)counters);   // <= 20
+            PM4G_CK(cudaMemcpyAsync(h_stage, counters, o_tot + 8, cudaMemcpyDeviceToHost, s));
+            if (d_n && !list) PM4G_CK(cudaMemcpyAsync(h_stage + 32, d_n, 8, cudaMemcpyDeviceToHost, s));
             PM4G_CK(cudaStreamSynchronize(s));
+            memcpy(h, h_stage, 16);
+            memcpy(&htot, h_stage + o_tot, 8);
+            if (d_n && !list) memcpy(&hn, h_stage + 32, 8);
             if (d_n && !list) {
                 n_items = std::min(n_items, hn);
                 if (n_true) *n_true = n_items;
