@@ -348,7 +348,11 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
     Scratch md(s);
     PM4G_TRY(md.alloc(sizeof(Meta)));
     Meta* dm = md.as<Meta>();
-    PM4G_CK(cudaMemcpyAsync(dm, &h, sizeof(Meta), cudaMemcpyHostToDevice, s));
+    // pinned staging: the init copy is a true async DMA, the result one copy + one wait
+    static thread_local Meta* hp = nullptr;
+    if (!hp) PM4G_CK(cudaHostAlloc((void**)&hp, sizeof(Meta), cudaHostAllocDefault));
+    *hp = h;
+    PM4G_CK(cudaMemcpyAsync(dm, hp, sizeof(Meta), cudaMemcpyHostToDevice, s));
     const int64_t n = L->n;
     uint32_t hi = L->case_hi;
     int hpasses, hbits;
@@ -368,8 +372,9 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
             if (c.kind == PM4G_KIND_CODES)
                 PM4G_LAUNCH("k_validate_codes", n * 4.0, s, k_validate_codes<<<g, 256, 0, s>>>((const uint32_t*)c.data, c.valid, n, c.dict_size, dm));
     }
-    PM4G_CK(cudaMemcpyAsync(&h, dm, sizeof(Meta), cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaMemcpyAsync(hp, dm, sizeof(Meta), cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
+    h = *hp;
     if (h.bad_case != ~0ull)
         return fail(PM4G_EDATA, "case code out of range [case_lo, case_hi) at row " + std::to_string(h.bad_case));
     if (h.bad_act != ~0ull)
