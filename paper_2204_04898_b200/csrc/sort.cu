@@ -129,15 +129,20 @@ struct OsLayout {
     static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
 };
 
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
 // One tile's stable rank / publish / permute / look-back / write-out.  The
 // tile's rows are in u_key (FROM_COLS: u_case, u_ts) and u_act; s_whist must
-// be zero on entry.
-template <class P, bool FROM_COLS, bool WITH_IDX, bool HI>
+// be zero on entry.  after_rank() runs (every thread) once the tile's inputs
+// other than u_act / u_key are no longer read (after the ranking barrier).
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, class Hook = NoHook>
 __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& a, const uint32_t tile,
                                         const uint32_t nvalid, uint64_t* u_key, const int64_t* u_ts,
                                         const uint32_t* u_case, const uint32_t* u_idx, const P* u_act,
                                         uint32_t* v_idx, P* v_act, uint32_t (*s_whist)[RADIX],
-                                        long long* s_gbase, uint32_t* s_scan) {
+                                        long long* s_gbase, uint32_t* s_scan, Hook after_rank = Hook()) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)tile * SORT_TILE;
     const uint32_t dmask = (1u << a.bits) - 1;
@@ -199,6 +204,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         __syncwarp();
     }
     __syncthreads();   // every key is in registers: u_key may be overwritten
+    after_rank();
 
     // ---- per-digit totals; warp bases = tile-exclusive start + warp-exclusive prefix
     const int d = tid;
@@ -424,9 +430,117 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf(PassArgs<P, fal
     }
 }
 
+// Persistent form of pass 0 (raw columns in, u8/u16 activity, no ingest row):
+// the next tile's timestamps + activities are TMA-prefetched into the second of
+// two buffers at tile start, and its case codes into the single case buffer as
+// soon as the current tile's ranking has consumed it (after_rank), so neither
+// load is exposed; 13 B/row of double buffering would not fit two CTAs per SM.
+template <class P>
+struct Os0Layout {
+    static constexpr size_t T = SORT_TILE;
+    static constexpr size_t o_act = T * 8;
+    static constexpr size_t buf = (T * 8 + T * sizeof(P) + 15) / 16 * 16;   // ts (-> keys) | act
+    static constexpr size_t o_case = 2 * buf;
+    static constexpr size_t o_vact = o_case + T * 4;
+    static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
+};
+
+template <class P, bool HI>
+__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf0(PassArgs<P, true, false> a, uint32_t n_tiles) {
+    using Lay = Os0Layout<P>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
+    P* v_act = (P*)(smem + Lay::o_vact);
+    __shared__ uint32_t s_whist[SORT_WARPS][RADIX];
+    __shared__ long long s_gbase[RADIX];
+    __shared__ uint32_t s_scan[SORT_WARPS + 1];
+    __shared__ uint32_t s_tile[2];
+    __shared__ __align__(8) uint64_t s_bar[2], s_cbar;
+
+    const int tid = threadIdx.x;
+    auto bulk = [&](uint32_t t) { return t < n_tiles && a.aligned && (int64_t)(t + 1) * SORT_TILE <= a.n; };
+    auto issue_ta = [&](uint32_t t, int b) {   // thread 0: timestamps + activities of tile t
+        unsigned char* buf = smem + b * Lay::buf;
+        mbar_expect_tx(&s_bar[b], SORT_TILE * (uint32_t)(8 + sizeof(P)));
+        tma_load_1d(buf, a.in_ts + (int64_t)t * SORT_TILE, SORT_TILE * 8, &s_bar[b]);
+        tma_load_1d(buf + Lay::o_act, a.in_act + (int64_t)t * SORT_TILE, SORT_TILE * sizeof(P), &s_bar[b]);
+    };
+    auto issue_case = [&](uint32_t t) {       // thread 0: case codes of tile t
+        mbar_expect_tx(&s_cbar, SORT_TILE * 4);
+        tma_load_1d(u_case, a.in_case + (int64_t)t * SORT_TILE, SORT_TILE * 4, &s_cbar);
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_cbar, 1);
+        const uint32_t t = atomicAdd(a.tile_counter, 1u);
+        s_tile[0] = t;
+        if (bulk(t)) {
+            issue_ta(t, 0);
+            issue_case(t);
+        }
+    }
+    uint32_t ph = 0, pc = 0;   // mbarrier parities: ts/act buffers (bit b), case buffer
+    for (int b = 0;; b ^= 1) {
+        for (int i = tid; i < SORT_WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        const uint32_t tile = s_tile[b];
+        if (tile >= n_tiles) break;
+        uint32_t next = 0;
+        if (tid == 0) {
+            next = atomicAdd(a.tile_counter, 1u);
+            s_tile[b ^ 1] = next;   // read after the next iteration's barrier
+            if (bulk(next)) issue_ta(next, b ^ 1);
+        }
+        uint64_t* u_key = (uint64_t*)(smem + b * Lay::buf);
+        int64_t* u_ts = (int64_t*)u_key;
+        P* u_act = (P*)(smem + b * Lay::buf + Lay::o_act);
+        const int64_t base = (int64_t)tile * SORT_TILE;
+        const int64_t nv64 = a.n - base;
+        const uint32_t nvalid = (uint32_t)(nv64 < SORT_TILE ? nv64 : SORT_TILE);
+        if (bulk(tile)) {
+            mbar_wait(&s_bar[b], (ph >> b) & 1u);
+            ph ^= 1u << b;
+            mbar_wait(&s_cbar, pc);
+            pc ^= 1u;
+        } else {   // the ragged last tile
+            for (uint32_t i = tid; i < nvalid; i += SORT_THREADS) {
+                u_ts[i] = a.in_ts[base + i];
+                u_case[i] = a.in_case[base + i];
+                u_act[i] = a.in_act[base + i];
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before any TMA refill
+            __syncthreads();
+        }
+        // the case buffer is free once the ranking has read it: fetch the next tile's
+        auto hook = [&]() {
+            if (tid == 0 && bulk(next)) issue_case(next);
+        };
+        os_tile<P, true, false, HI>(a, tile, nvalid, u_key, u_ts, u_case, nullptr, u_act, nullptr, v_act,
+                                    s_whist, s_gbase, s_scan, hook);
+    }
+}
+
+template <class P, bool HI>
+static pm4g_status launch_pf0(const PassArgs<P, true, false>& args, int64_t tiles, cudaStream_t s,
+                              const char* name, double bytes) {
+    const size_t smem = Os0Layout<P>::bytes;
+    PM4G_MAX_SMEM(k_onesweep_pf0<P, HI>);
+    static int per_sm = -1;
+    if (per_sm < 0)
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pf0<P, HI>, SORT_THREADS, smem));
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * num_sms());
+    PM4G_LAUNCH(name, bytes, s, (k_onesweep_pf0<P, HI><<<grid, SORT_THREADS, smem, s>>>(args, (uint32_t)tiles)));
+    return PM4G_OK;
+}
+
 template <class P, bool FC, bool WI, bool HI>
 static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                  const char* name, double bytes) {
+    if constexpr (FC && !WI && sizeof(P) == 1) {    // pass 0: persistent, prefetching form (2 CTAs/SM)
+        if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF")) return launch_pf0<P, HI>(args, tiles, s, name, bytes);
+    }
     if constexpr (!FC && !WI && sizeof(P) <= 2) {   // persistent, prefetching form (2 CTAs per SM)
         if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF")) {
             const size_t smem = OsPfLayout<P>::bytes;
