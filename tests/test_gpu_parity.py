@@ -253,8 +253,9 @@ def test_digit_shift_boundaries(ts_bits, case_bits):
 @pytest.mark.parametrize("act_bits", [8, 16])
 def test_persistent_prefetch_key_passes(monkeypatch, act_bits):
     """Key passes above 2 x SMs tiles run the persistent, prefetching onesweep
-    (k_onesweep_pf: next tile TMA-loaded into a second buffer); below, or with
-    PM4G_NO_OS_PF, the one-tile-per-CTA kernel.  Both must equal the oracle on a
+    (k_onesweep_pf: next tile TMA-loaded into a second buffer; pass 0 with a u8
+    activity: k_onesweep_pf0); below, or with PM4G_NO_OS_PF, the one-tile-per-CTA
+    kernel.  Both must equal the oracle on a
     log with 3 case digits (2 key passes), several tiles per CTA and a ragged
     last tile."""
     rng = np.random.default_rng(act_bits)

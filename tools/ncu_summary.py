@@ -38,7 +38,7 @@ def num(x):
 def base_name(k):
     k = k.replace("void ", "").replace("pm4g::", "")
     name = k.split("(")[0]
-    if name.startswith("k_onesweep_pf<"):   # persistent key passes: log sort only (u8/u16 activity)
+    if name.startswith("k_onesweep_pf<") or name.startswith("k_onesweep_pf0<"):   # persistent log-sort passes
         return "k_onesweep"
     if name.startswith("k_onesweep<"):   # log-sort passes carry the u8/u16 activity; u32 = small sorts
         return "k_onesweep" if "unsigned int" not in name.split(",")[0] else "k_onesweep_small"
