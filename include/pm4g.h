@@ -45,7 +45,8 @@ typedef enum pm4g_status {
     PM4G_ECUDA = 4,      /* a CUDA runtime error (message carries cudaGetErrorString) */
     PM4G_ENCCL = 5,      /* an NCCL error, or NCCL could not be loaded */
     PM4G_EKEYWIDTH = 6,  /* case_bits + ts_bits > 64: composite key does not fit */
-    PM4G_ECOLLISION = 7  /* cross-rank variant-key collision that could not be resolved */
+    PM4G_ECOLLISION = 7  /* reserved, never returned: variant-key collisions (local or across
+                            ranks) are always resolved exactly by verification + re-keying */
 } pm4g_status;
 
 typedef void* pm4g_stream_t; /* cudaStream_t */
@@ -119,7 +120,13 @@ pm4g_status pm4g_log_info_get(const pm4g_log* log, pm4g_log_info* info);
  * (ts - ts_min) with the activity (and a row index when extra columns exist) as
  * payload; stability realises the third criterion (R2).  Then materialises the
  * case segments (the cases dataframe's row ranges).
- * Idempotent.  PM4G_EKEYWIDTH if case_bits + ts_bits > 64. */
+ * Idempotent.  PM4G_EKEYWIDTH if case_bits + ts_bits > 64.
+ * Synchronises `stream` once: the host learns whether any case needs the exact
+ * fallback (cases longer than 1024 rows, or running > 512 rows past a 4096-row
+ * tile; they are then sorted by one batched segmented radix sort, one more
+ * round trip).  This is a deliberate deviation from SURVEY.md 8(b), which lets
+ * only log_create and variants synchronise; pm4g_sort_analyze folds this check
+ * into the analysis' own synchronisation instead. */
 pm4g_status pm4g_sort(pm4g_log* log, pm4g_stream_t stream);
 
 /* The formatted log, decoded into caller device buffers (each [n_events], any

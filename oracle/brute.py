@@ -117,3 +117,32 @@ def efg(case, act, ts):
             for y in range(x + 1, len(evs)):
                 out[(evs[x][2], evs[y][2])].append(evs[y][0] - evs[x][0])
     return dict(out)
+
+
+def variant_order(case, act, ts):
+    """Variants in the ABI order by enumeration (reading R11: count descending,
+    then the smallest case code holding the variant ascending), and each case's
+    index into that list (S:358 case_to_variant, cases in ascending code).
+    Returns (ordered [(seq, count, rep)], [variant index per case])."""
+    tr = traces(case, act, ts)
+    groups = {}
+    for c in tr:
+        seq = tuple(a for _, _, a in tr[c])
+        g = groups.setdefault(seq, [0, c])
+        g[0] += 1
+        g[1] = min(g[1], c)
+    ordered = sorted(((s, k, r) for s, (k, r) in groups.items()), key=lambda x: (-x[1], x[2]))
+    pos = {s: i for i, (s, _, _) in enumerate(ordered)}
+    return ordered, [pos[tuple(a for _, _, a in tr[c])] for c in sorted(tr)]
+
+
+def filter_range(case, col, lo, hi, valid=None, level=0, keep=True):
+    """S:447-448 numeric-in-[lo, hi] by enumeration (i64 or f64 values; nulls,
+    valid[i] == 0, never match); kept row indices in input order."""
+    m = [(valid is None or bool(valid[i])) and (lo <= col[i] <= hi) for i in range(len(col))]
+    if level == 0:
+        return [i for i in range(len(m)) if m[i] == keep]
+    anym = defaultdict(bool)
+    for c, x in zip(case, m):
+        anym[int(c)] |= x
+    return [i for i, c in enumerate(case) if anym[int(c)] == keep]

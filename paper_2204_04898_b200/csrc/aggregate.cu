@@ -420,7 +420,7 @@ static pm4g_status reduce_minmax(pm4g_comm* comm, uint64_t* mm, uint32_t A, cuda
 }
 
 static pm4g_status require_sorted(const pm4g_log* L) {
-    if (!L) return fail(PM4G_EINVAL, "null log");
+    PM4G_TRY(check_log(L));
     if (!L->sorted) return fail(PM4G_EINVAL, "log is not sorted (call pm4g_sort first)");
     return PM4G_OK;
 }

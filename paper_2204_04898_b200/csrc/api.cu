@@ -395,6 +395,13 @@ pm4g_status fetch_n_cases(const pm4g_log* Lc, cudaStream_t s) {
     return PM4G_OK;
 }
 
+pm4g_status check_log(const pm4g_log* L) {
+    if (!L) return fail(PM4G_EINVAL, "null log");
+    if (L->broken)
+        return fail(PM4G_EINVAL, "log unusable: formatting it failed in an earlier pm4g_sort_analyze call");
+    return PM4G_OK;
+}
+
 static void free_log_cols(pm4g_log* L, cudaStream_t s) {
     if (L->owns_cols) {
         dfree(L->case_, s);
@@ -617,13 +624,13 @@ static pm4g_status sort_impl(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
 }
 
 pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
-    if (!L) return fail(PM4G_EINVAL, "null log");
+    PM4G_TRY(check_log(L));
     if (L->sorted) return PM4G_OK;
     return sort_impl(L, (cudaStream_t)stream, nullptr);
 }
 
 pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* comm, pm4g_stream_t stream) {
-    if (!L) return fail(PM4G_EINVAL, "null log");
+    PM4G_TRY(check_log(L));
     if (!out) return fail(PM4G_EINVAL, "null outputs");
     if (L->sorted) return pm4g_analyze(L, out, comm, stream);
     if (comm || !out->variants) {
@@ -638,7 +645,12 @@ pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* c
     pm4g_status st = pm4g_analyze(L, out, comm, stream);
     bool fixed = false;
     const pm4g_status fs = sort_finish(&d, s, &fixed);
-    if (fs != PM4G_OK) return fs;
+    if (fs != PM4G_OK) {   // the input columns are gone and the order is provisional
+        L->broken = true;
+        if (st == PM4G_OK && *out->variants) pm4g_variants_destroy(*out->variants);
+        *out->variants = nullptr;
+        return fs;
+    }
     if (fixed) {   // some cases were re-sorted exactly: recompute from the final order
         if (st == PM4G_OK && *out->variants) pm4g_variants_destroy(*out->variants);
         *out->variants = nullptr;

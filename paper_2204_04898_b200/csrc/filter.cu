@@ -660,6 +660,7 @@ pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t
                              pm4g_stream_t stream, pm4g_log** out) {
     if (!in || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
+    PM4G_TRY(check_log(in));
     if (t1 > t2) return fail(PM4G_EINVAL, "t1 > t2 (S:414)");
     if (mode < 0 || mode > 2) return fail(PM4G_EINVAL, "bad time-filter mode");
     cudaStream_t s = (cudaStream_t)stream;
@@ -691,6 +692,7 @@ pm4g_status pm4g_filter_cases(const pm4g_log* in, const pm4g_case_pred* pred, in
                               pm4g_stream_t stream, pm4g_log** out) {
     if (!in || !pred || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
+    PM4G_TRY(check_log(in));
     if (!in->sorted) return fail(PM4G_EINVAL, "case-level filters need a formatted log (call pm4g_sort first)");
     const int kind = pred->kind;
     if (kind < PM4G_CASE_START_IN || kind > PM4G_CASE_PATHS) return fail(PM4G_EINVAL, "bad case predicate kind");
@@ -743,6 +745,7 @@ pm4g_status pm4g_filter_variants(const pm4g_log* in, const uint64_t* seq_off, co
                                  int64_t n_seqs, int32_t keep, pm4g_stream_t stream, pm4g_log** out) {
     if (!in || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
+    PM4G_TRY(check_log(in));
     if (!in->sorted) return fail(PM4G_EINVAL, "case-level filters need a formatted log (call pm4g_sort first)");
     if (n_seqs < 0 || (n_seqs > 0 && (!seq_off || !seq_act))) return fail(PM4G_EINVAL, "bad sequence list");
     cudaStream_t s = (cudaStream_t)stream;
@@ -826,6 +829,7 @@ pm4g_status pm4g_filter_attr(const pm4g_log* in, int32_t column, const pm4g_pred
                              int32_t level, int32_t keep, pm4g_stream_t stream, pm4g_log** out) {
     if (!in || !pred || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
+    PM4G_TRY(check_log(in));
     if (level != PM4G_LEVEL_EVENTS && level != PM4G_LEVEL_CASES) return fail(PM4G_EINVAL, "bad level");
     cudaStream_t s = (cudaStream_t)stream;
     AttrPred p{};

@@ -117,6 +117,7 @@ struct pm4g_log {
     // composite key ((case - case_min) << ts_bits) | (ts - ts_min)
     int case_bits = 0, ts_bits = 0, key_bits = 0, passes = 0;
     bool sorted = false;
+    bool broken = false;        // a deferred format step failed: every call on the log fails
     // ingested state
     uint32_t* case_ = nullptr;
     void* act = nullptr;
@@ -152,6 +153,10 @@ struct pm4g_variant_table {
 };
 
 namespace pm4g {
+
+// A log whose deferred format step failed (pm4g_sort_analyze) has neither its
+// ingested columns nor a correct formatted order: every call on it fails.
+pm4g_status check_log(const pm4g_log* L);
 
 // ------------------------------------------------------------------ helpers
 __host__ __device__ inline int bit_width_u64(uint64_t x) {

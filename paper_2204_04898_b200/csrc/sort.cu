@@ -895,22 +895,77 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     }
 }
 
-// fallback cases: stable radix sort of the case's keys, then gather payloads
-__global__ void k_big_keys(const uint64_t* __restrict__ gkey, int64_t start, int64_t len,
+// ---- the exact fallback, batched over every listed case (one segmented sort):
+// the rows of all listed cases are concatenated (segments ordered by start
+// row), sorted stably by key, then stably by segment, and scattered back to
+// their case's rows -- ties keep the grouped (= ingest) order inside a case.
+// seg_start[j] / seg_pre[j]: start row / concatenation offset of segment j.
+__device__ __forceinline__ uint32_t seg_of(const uint64_t* __restrict__ seg_pre, uint32_t nseg, uint64_t q) {
+    uint32_t lo = 0, hi = nseg;   // last j with seg_pre[j] <= q
+    while (hi - lo > 1) {
+        const uint32_t m = (lo + hi) >> 1;
+        if (seg_pre[m] <= q) lo = m; else hi = m;
+    }
+    return lo;
+}
+__global__ void k_big_bounds(const uint32_t* __restrict__ big, uint32_t nbig, const uint32_t* __restrict__ off,
+                             uint32_t* __restrict__ se) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nbig; j += gridDim.x * blockDim.x) {
+        se[2 * j] = off[big[j]];
+        se[2 * j + 1] = off[big[j] + 1];
+    }
+}
+__global__ void k_big_keys(const uint64_t* __restrict__ gkey, const uint64_t* __restrict__ seg_start,
+                           const uint64_t* __restrict__ seg_pre, uint32_t nseg, uint64_t T,
                            uint64_t* __restrict__ k, uint32_t* __restrict__ v) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
-        k[q] = gkey[start + q];
-        v[q] = (uint32_t)q;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < T; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = seg_of(seg_pre, nseg, q);
+        const uint64_t row = seg_start[j] + (q - seg_pre[j]);
+        k[q] = gkey[row];
+        v[q] = (uint32_t)row;
+    }
+}
+__global__ void k_big_segkeys(const uint32_t* __restrict__ v, const uint64_t* __restrict__ seg_start, uint32_t nseg,
+                              uint64_t T, uint64_t* __restrict__ k) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < T; q += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nseg;   // segment holding row v[q]
+        while (hi - lo > 1) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (seg_start[m] <= v[q]) lo = m; else hi = m;
+        }
+        k[q] = lo;
     }
 }
 template <class P>
-__global__ void k_big_gather(FmtArgs<P> a, int64_t start, int64_t len, const uint64_t* __restrict__ k,
-                             const uint32_t* __restrict__ v) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < len; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t src = start + v[q];
-        a.key_out[start + q] = k[q];
-        a.act_out[start + q] = a.gact[src];
-        if (a.perm_out) a.perm_out[start + q] = a.gidx[src];
+__global__ void k_big_gather(FmtArgs<P> a, const uint64_t* __restrict__ seg_start, const uint64_t* __restrict__ seg_pre,
+                             uint32_t nseg, uint64_t T, const uint32_t* __restrict__ v) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < T; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = seg_of(seg_pre, nseg, q);
+        const uint64_t dst = seg_start[j] + (q - seg_pre[j]);
+        const uint32_t src = v[q];
+        a.key_out[dst] = a.gkey[src];
+        a.act_out[dst] = a.gact[src];
+        if (a.perm_out) a.perm_out[dst] = a.gidx[src];
+    }
+}
+
+// Rows of the cases k_format listed for the exact fallback are not written by
+// k_format.  Before the (deferred) fallback runs, the provisional order must
+// still hold valid codes for every row: copy those cases' grouped rows through
+// unchanged (same case, ingest order), so anything derived from the provisional
+// order stays in bounds; the fallback then overwrites them with the exact order.
+template <class P>
+__global__ void k_big_identity(const uint32_t* __restrict__ big, const uint32_t* __restrict__ big_count,
+                               const uint32_t* __restrict__ off, const uint64_t* __restrict__ gkey,
+                               const P* __restrict__ gact, uint64_t* __restrict__ key_out, P* __restrict__ act_out) {
+    const uint32_t nb = *big_count;
+    for (uint32_t e = blockIdx.x; e < nb; e += gridDim.x) {
+        const uint32_t r = big[e];
+        const uint32_t a = off[r], b = off[r + 1];
+        for (uint32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+            key_out[i] = gkey[i];
+            act_out[i] = gact[i];
+        }
     }
 }
 
@@ -941,26 +996,48 @@ static pm4g_status format_launch(FmtArgs<P>& fa, Scratch& st, cudaStream_t s) {
 }
 
 // the exact fallback for the nbig cases k_format listed (too long, or running
-// too far past a tile): a stable radix sort of each such case's keys
+// too far past a tile): one batched segmented sort of all their rows (two host
+// round trips in all: the list size, then the segment bounds)
 template <class P>
 static pm4g_status format_fallback(const FmtArgs<P>& fa, uint32_t nbig, cudaStream_t s) {
-    std::vector<uint32_t> ranks(nbig);
-    PM4G_CK(cudaMemcpyAsync(ranks.data(), fa.big, nbig * 4, cudaMemcpyDeviceToHost, s));
+    Scratch se(s);
+    PM4G_TRY(se.alloc((size_t)nbig * 8));
+    const int gb = std::max(1, std::min<int>((int)((nbig + 255) / 256), num_sms()));
+    PM4G_LAUNCH("k_big_bounds", nbig * 12.0, s, (k_big_bounds<<<gb, 256, 0, s>>>(fa.big, nbig, fa.off, se.as<uint32_t>())));
+    std::vector<uint32_t> h(2 * (size_t)nbig);
+    PM4G_CK(cudaMemcpyAsync(h.data(), se.p, (size_t)nbig * 8, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
-    for (uint32_t r : ranks) {
-        uint32_t se[2];
-        PM4G_CK(cudaMemcpyAsync(se, fa.off + r, 8, cudaMemcpyDeviceToHost, s));
-        PM4G_CK(cudaStreamSynchronize(s));
-        const int64_t start = se[0], len = (int64_t)se[1] - se[0];
-        Scratch kv(s);
-        PM4G_TRY(kv.alloc((size_t)len * 12 + 16));
-        uint64_t* k = kv.as<uint64_t>();
-        uint32_t* v = (uint32_t*)(k + len);
-        const int g = std::max(1, std::min<int>((int)((len + 255) / 256), num_sms() * 4));
-        PM4G_LAUNCH("k_big_keys", len * 20.0, s, (k_big_keys<<<g, 256, 0, s>>>(fa.gkey, start, len, k, v)));
-        PM4G_TRY(radix_sort_u64(k, v, len, std::min(64, std::max(1, fa.ts_bits)), s));
-        PM4G_LAUNCH("k_big_gather", len * 30.0, s, (k_big_gather<P><<<g, 256, 0, s>>>(fa, start, len, k, v)));
+    std::vector<std::pair<uint64_t, uint64_t>> segs;   // (start, len), ascending start
+    for (uint32_t j = 0; j < nbig; ++j)
+        if (h[2 * j + 1] > h[2 * j]) segs.push_back({h[2 * j], (uint64_t)h[2 * j + 1] - h[2 * j]});
+    std::sort(segs.begin(), segs.end());
+    const uint32_t nseg = (uint32_t)segs.size();
+    if (!nseg) return PM4G_OK;
+    std::vector<uint64_t> meta(2 * (size_t)nseg + 1);   // seg_start[nseg] | seg_pre[nseg + 1]
+    uint64_t T = 0;
+    for (uint32_t j = 0; j < nseg; ++j) {
+        meta[j] = segs[j].first;
+        meta[nseg + j] = T;
+        T += segs[j].second;
     }
+    meta[2 * nseg] = T;
+    Scratch md(s), kv(s);
+    PM4G_TRY(md.alloc(meta.size() * 8));
+    PM4G_CK(cudaMemcpyAsync(md.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, s));
+    const uint64_t* seg_start = md.as<uint64_t>();
+    const uint64_t* seg_pre = seg_start + nseg;
+    PM4G_TRY(kv.alloc((size_t)T * 12 + 16));
+    uint64_t* k = kv.as<uint64_t>();
+    uint32_t* v = (uint32_t*)(k + T);
+    const int g = std::max(1, std::min<int>((int)((T + 255) / 256), num_sms() * 4));
+    PM4G_LAUNCH("k_big_keys", T * 20.0, s, (k_big_keys<<<g, 256, 0, s>>>(fa.gkey, seg_start, seg_pre, nseg, T, k, v)));
+    // by key (the case bits are equal inside a segment), then stably by segment
+    PM4G_TRY(radix_sort_u64(k, v, (int64_t)T, std::min(64, std::max(1, fa.ts_bits)), s));
+    if (nseg > 1) {
+        PM4G_LAUNCH("k_big_segkeys", T * 12.0, s, (k_big_segkeys<<<g, 256, 0, s>>>(v, seg_start, nseg, T, k)));
+        PM4G_TRY(radix_sort_u64(k, v, (int64_t)T, std::max(1, bit_width_u64(nseg - 1)), s));
+    }
+    PM4G_LAUNCH("k_big_gather", T * 30.0, s, (k_big_gather<P><<<g, 256, 0, s>>>(fa, seg_start, seg_pre, nseg, T, v)));
     return PM4G_OK;
 }
 
@@ -1014,12 +1091,22 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     // synchronisation (the grouped keys stay alive for the fallback)
     d->st.s = s;
     PM4G_TRY(format_launch<P>(fa, d->st, s));
+    // fallback cases hold their grouped rows until the fallback runs (no stale bytes)
+    PM4G_LAUNCH("k_big_identity", 0, s,
+                (k_big_identity<P><<<num_sms(), 256, 0, s>>>(fa.big, fa.big_count, fa.off, fa.gkey, fa.gact,
+                                                              fa.key_out, fa.act_out)));
     // the fallback count goes to pinned host memory now (stream order); the
-    // caller's own synchronisation later makes it readable without a wait
+    // caller's own synchronisation later makes it readable without a wait.
+    // Events belong to the device current at creation: one per device.
+    constexpr int MAXDEV = 64;
     static thread_local uint32_t* h_nbig = nullptr;
-    static thread_local cudaEvent_t ev = nullptr;
-    if (!h_nbig) PM4G_CK(cudaHostAlloc((void**)&h_nbig, 4, cudaHostAllocDefault));
-    if (!ev) PM4G_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    static thread_local cudaEvent_t evs[MAXDEV] = {};
+    int dev = 0;
+    PM4G_CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= MAXDEV) return fail(PM4G_EINVAL, "device ordinal out of range");
+    if (!h_nbig) PM4G_CK(cudaHostAlloc((void**)&h_nbig, 4, cudaHostAllocPortable));
+    if (!evs[dev]) PM4G_CK(cudaEventCreateWithFlags(&evs[dev], cudaEventDisableTiming));
+    cudaEvent_t ev = evs[dev];
     PM4G_CK(cudaMemcpyAsync(h_nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaEventRecord(ev, s));
     d->h_nbig = h_nbig;
@@ -1277,7 +1364,7 @@ using namespace pm4g;
 
 extern "C" pm4g_status pm4g_sorted_columns(const pm4g_log* L, uint32_t* case_code, uint32_t* act,
                                            int64_t* ts, pm4g_stream_t stream) {
-    if (!L) return fail(PM4G_EINVAL, "null log");
+    PM4G_TRY(check_log(L));
     if (!L->sorted) return fail(PM4G_EINVAL, "log is not sorted (call pm4g_sort)");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = L->n;

@@ -196,11 +196,13 @@ def test_variant_table_regrowth(monkeypatch, cap):
 
 @pytest.mark.parametrize("A", [92, 200, 256])
 def test_cnt16_table_flush_exact(A):
-    """91 < A <= 256 keeps DFG counts as u16 pairs in shared memory, flushed in
-    steps of 0x4000.  One case repeats a self-loop ~200k times (one oversized
-    tile, read from global memory) and another alternates two activities, so
-    single edges cross the flush step many times inside one CTA; ordinary
-    random cases fill the rest.  Counts and sums must match the oracle exactly."""
+    """A > 91 takes k_aggregate's TAB_HASH mode (a per-CTA shared-memory hash table
+    of u32 counts and u32 lo / hi duration sums, flushed once per CTA with 64-bit
+    atomics).  One case repeats a self-loop ~200k times (one oversized tile, read
+    from global memory, and a 3.2e5-row exact-fallback case in the sort) and
+    another alternates two activities, so single edges take ~1e5 increments inside
+    one CTA and the u32 duration words carry into the high word; ordinary random
+    cases fill the rest.  Counts and sums must match the oracle exactly."""
     rng = np.random.default_rng(A)
     lens = rng.integers(1, 30, 5000)
     case = np.repeat(np.arange(5000, dtype=np.int64), lens)
@@ -279,7 +281,7 @@ def test_sort_analyze_random_tiny_logs(seed):
                   oracle.run(case, act, ts, A))
 
 
-@pytest.mark.parametrize("shape", ["one_long_case", "long_cases_across_tiles", "ragged"])
+@pytest.mark.parametrize("shape", ["one_long_case", "long_cases_across_tiles", "ragged", "many_long_with_ties"])
 def test_sort_analyze_fallback_cases(shape):
     """Cases k_format leaves to the exact fallback (longer than 1024 rows, or running
     far past a tile): pm4g_sort_analyze finds them at the analysis' synchronisation,
@@ -291,13 +293,18 @@ def test_sort_analyze_fallback_cases(shape):
     elif shape == "long_cases_across_tiles":
         n = 40_000
         case = np.repeat(np.arange(20), n // 20)[rng.permutation(n)]   # 2000-row cases
-    else:
+    elif shape == "ragged":
         n = 3 * 4096 + 17
         case = rng.integers(0, n // 9, n)
         case[: 3000] = 5                                               # one 3000+-row case
         case = case[rng.permutation(n)]
+    else:   # 60 fallback cases (1100-3000 rows) among short ones, timestamps with many ties:
+        lens = np.concatenate([rng.integers(1100, 3000, 60), rng.integers(1, 20, 20_000)])
+        case = np.repeat(rng.permutation(lens.size), lens)             # the batched exact sort
+        n = case.size
+        case = case[rng.permutation(n)]
     act = rng.integers(0, 7, n)
-    ts = rng.integers(0, 10**7, n)
+    ts = rng.integers(0, 10**7 if shape != "many_long_with_ties" else 50, n)
     assert_parity(gpu_run(case, act, ts, 7, n_case_codes=int(case.max()) + 1, sort_analyze=True),
                   oracle.run(case, act, ts, 7))
 
@@ -328,3 +335,25 @@ def test_sort_analyze_with_extra_columns(long_case):
     g = collect(log, sort_analyze=True)
     log.close()
     assert_parity(g, oracle.run(case, act, ts, 9))
+
+
+def test_sort_analyze_fallback_over_stale_allocator_blocks():
+    """pm4g_sort_analyze analyses the provisional order before the exact fallback
+    runs; the rows of fallback cases must hold valid activity codes then, not the
+    previous contents of a recycled allocator block.  A first log of the same size
+    with every activity = 255 (A = 256) is sorted and destroyed, so its blocks (act
+    bytes 0xFF) return to the library's cache; the second log (A = 7, fallback
+    cases) reuses them.  Results equal the oracle's and no CUDA error is raised."""
+    rng = np.random.default_rng(3)
+    n = 40_000
+    case = np.repeat(np.arange(20), n // 20)[rng.permutation(n)]        # 2000-row cases
+    for _ in range(2):
+        c, a, t = to_device_cols(case, np.full(n, 255), rng.integers(0, 10**7, n), 256)
+        log = pm4g.pm4g_log_create(c, a, t, 256, n_case_codes=20)
+        log.sort()
+        torch.cuda.synchronize()
+        log.close()
+    act = rng.integers(0, 7, n)
+    ts = rng.integers(0, 10**7, n)
+    assert_parity(gpu_run(case, act, ts, 7, n_case_codes=20, sort_analyze=True), oracle.run(case, act, ts, 7))
+    torch.cuda.synchronize()

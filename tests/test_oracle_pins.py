@@ -47,6 +47,35 @@ def test_l1_o1_matches_spec(l1):
     assert (r.n_cases, len(case), len(r.variants())) == (rep["cases"], rep["events"], rep["variants"])
 
 
+def test_l1_variant_order_and_case_index():
+    """S:369 L1 -> {<A,B,C>: 2, <A,C>: 1}; reading R11 orders them count descending,
+    so <A,B,C> (count 2) is variant 0 and <A,C> variant 1; "c1 and c3 share
+    variant_id, c2 differs" -> case_variant = [0, 1, 0] (cases in code order)."""
+    case, act, ts = [0, 1, 2, 0, 1, 2, 0, 2], [0, 0, 0, 1, 2, 1, 2, 2], [0, 5, 0, 10, 15, 50, 20, 100]
+    r = oracle.run(case, act, ts, 3)
+    seqs = [r.v_act[r.v_off[i]:r.v_off[i + 1]].tolist() for i in range(r.v_count.size)]
+    assert seqs == [[0, 1, 2], [0, 2]]
+    assert r.v_count.tolist() == [2, 1] and r.v_len.tolist() == [3, 2]
+    assert r.v_rep.tolist() == [0, 1]                 # smallest case holding each variant
+    assert r.case_variant.tolist() == [0, 1, 0]
+
+
+def test_variant_order_ties_by_smallest_case():
+    """R11 tie-break: equal counts ordered by the smallest case code ascending (not by
+    sequence, not by first appearance in ingest order).  Case 5 holds <1> and is
+    ingested first; case 2 holds <0, 0>, case 3 holds <2>, case 9 holds <1>, case 7
+    holds <0, 0>: counts {<1>: 2, <0,0>: 2, <2>: 1}, reps {<1>: 5, <0,0>: 2, <2>: 3}."""
+    case = [5, 9, 7, 2, 3, 7, 2]
+    act = [1, 1, 0, 0, 2, 0, 0]
+    ts = [0, 0, 0, 0, 0, 1, 1]
+    r = oracle.run(case, act, ts, 3)
+    seqs = [tuple(r.v_act[r.v_off[i]:r.v_off[i + 1]].tolist()) for i in range(r.v_count.size)]
+    assert seqs == [(0, 0), (1,), (2,)]
+    assert r.v_rep.tolist() == [2, 5, 3]
+    # cases in code order 2, 3, 5, 7, 9
+    assert r.case_variant.tolist() == [0, 2, 1, 0, 1]
+
+
 def test_l1_o2_matches_spec(l1):
     case, act, ts, A = _l1_cols(l1)
     ex = l1["expected"]
@@ -114,6 +143,13 @@ def _o1_vs_o2(case, act, ts, A):
     for i in range(r.v_count.size):
         seq = tuple(r.v_act[r.v_off[i]:r.v_off[i + 1]].tolist())
         assert r.v_rep[i] == b["rep"][seq]
+    # R11 output order and the per-case variant index, by enumeration
+    ordered, cv = brute.variant_order(case, act, ts)
+    got = [(tuple(r.v_act[r.v_off[i]:r.v_off[i + 1]].tolist()), int(r.v_count[i]), int(r.v_rep[i]))
+           for i in range(r.v_count.size)]
+    assert got == ordered
+    assert r.v_len.tolist() == [len(s) for s, _, _ in ordered]
+    assert r.case_variant.tolist() == cv
     assert [(c, t, i, a) for c, t, i, a in zip(r.sorted_case.tolist(), r.sorted_ts.tolist(),
                                                r.perm.tolist(), r.sorted_act.tolist())] == b["sorted"]
     return r
@@ -303,3 +339,29 @@ def test_attr_filter_keep_remove_partition():
     valid = (val % 3 != 0)
     k = oracle.filter_attr(case, val, lo=10, hi=50, valid=valid, level=0)
     assert k.tolist() == [(10 <= v <= 50) and (v % 3 != 0) for v in val.tolist()]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_attr_range_f64_and_i64_vs_brute(seed):
+    """S:447-448 numeric-in-[lo, hi] (inclusive) with nulls, both levels, keep and
+    remove: O1's f64 and i64 range kinds against enumeration (O2)."""
+    case, act, ts, A, _ = random_log(seed)
+    if not case:
+        return
+    rng = np.random.default_rng(1000 + seed)
+    n = len(case)
+    f = rng.normal(0.0, 10.0, n)
+    f[rng.random(n) < 0.1] = 2.5          # exact hits on the bounds
+    f[rng.random(n) < 0.05] = -2.5
+    valid = rng.random(n) >= 0.15
+    iv = rng.integers(-20, 20, n)
+    for level in (0, 1):
+        for kp in (True, False):
+            k = oracle.filter_attr(case, f, lo=-2.5, hi=2.5, valid=valid, level=level, keep=kp)
+            assert [i for i, x in enumerate(k) if x] == brute.filter_range(
+                case, f.tolist(), -2.5, 2.5, valid.tolist(), level, kp)
+            k = oracle.filter_attr(case, iv, lo=-3, hi=4, valid=valid, level=level, keep=kp)
+            assert [i for i, x in enumerate(k) if x] == brute.filter_range(
+                case, iv.tolist(), -3, 4, valid.tolist(), level, kp)
+    with pytest.raises(ValueError):
+        oracle.filter_attr(case, f, lo=1.0, hi=0.0)   # S:458 min > max
