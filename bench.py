@@ -17,13 +17,20 @@ global log of N*100M events).  Inputs (1.3 GB/GPU) are larger than L2.
 
 Rank 0 prints ONE JSON line.  `value` = total input events of all ranks / max
 over ranks of the device time of the K timed steps.  `e2e` = the same metric
-through the C-ABI with HOST input buffers (pinned; H2D inside the call) and a
-D2H read of every result; step k+1's ingest (H2D + validation) runs on its
-own stream and host thread under step k's compute and D2H.  `roofline` = the dominant kernel (k_onesweep, the
-radix scatter pass) -- algorithmic bytes / CUDA-event time of its launches in
-the timed region, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the
-oracle (single-threaded C++) on a bounded sample of the same workload.
-`--impl reference` times the oracle alone (the reference arm for this tier).
+from HOST buffers (pinned) with a D2H read of every result, inside the timed
+region.  For steps of >= 64 MB the H2D copy of step k+1's columns is a torch
+copy_ into one of two device column sets on an ingest stream (own host thread),
+followed by pm4g_log_create borrowing them, all under step k's compute and D2H;
+smaller steps pass the pinned host columns to pm4g_log_create with
+PM4G_HOST_INPUT (the copy is then inside the C-ABI call).  `roofline` = the
+dominant kernel (k_onesweep, the radix scatter pass) -- algorithmic bytes /
+CUDA-event time of its launches in the timed region, against
+MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the oracle (single-threaded C++)
+timed per stage on the whole config at N = 1 (default), whose every output is
+then compared element by element with a GPU step on the same log
+(`verified.o1_whole_log_bit_exact`; a line whose outputs are not bit-exact
+carries "valid": false).  `--impl reference` times the oracle alone (the
+reference arm for this tier).
 """
 from __future__ import annotations
 
@@ -175,8 +182,17 @@ def check_invariants(pm4g, case, act, ts, meta, comm, out, filt, dist, dev, keep
         "sum_case_events_eq_events": ne == N,
         "sum_dfg_durations_eq_sum_case_durations": int(res["dur_sum"].sum()) % M == dsum % M,
     }
-    if keep is not None:
-        keep.update(n_events=res["n_events"][:C], dur=res["dur"][:C])
+    if keep is not None:   # every output of this step on the host, for the O1 comparison
+        import numpy as np
+        A = meta["A"]
+        keep.update(cnt=res["cnt"].cpu().numpy().view(np.uint64).reshape(A, A),
+                    sum=res["dur_sum"].cpu().numpy().reshape(A, A), mean=res["mean"].cpu().numpy().reshape(A, A),
+                    start=res["start"].cpu().numpy().view(np.uint64), end=res["end"].cpu().numpy().view(np.uint64),
+                    case_code=res["case_code"][:C].cpu().numpy(), n_events=res["n_events"][:C].cpu().numpy(),
+                    dur=res["dur"][:C].cpu().numpy(), v_count=tab["count"].cpu().numpy().view(np.uint64),
+                    v_len=tab["len"].cpu().numpy(), v_rep=tab["rep_case"].cpu().numpy(),
+                    v_off=tab["seq_off"].cpu().numpy().view(np.uint64), v_act=tab["seq_act"].cpu().numpy(),
+                    case_variant=v.case_index(C).cpu().numpy())
     v.close()
     return {"all": all(ok.values()), **ok}
 
@@ -192,10 +208,12 @@ def workload_config(cfg: str, n_local: int, cases: int, A: int, world: int, filt
             "step": "log_create+sort+analyze(DFG,start/end,durations,variants)" + ("+filter" if filt else "")}
 
 
-def cpu_baseline(cfg, cases: int, device, gpu_cases=None):
-    """O1 on a bounded sample (the first `cases` cases of the workload), 1 core.
-    gpu_cases: (n_events, dur) of the GPU run for the same case codes -- the
-    oracle's per-case results on the sample are compared with them."""
+def cpu_baseline(cfg, cases: int, device, gpu_out=None):
+    """O1 (single-threaded C++) on the first `cases` cases of the workload, timed
+    per stage (stable sort, then the loop).  With the whole config (cases >=
+    n_cases, the default at N = 1) and gpu_out (every output of a GPU step on
+    the same log), every output is compared element by element: SURVEY.md 8(d)
+    "each reported number is checked against O1 first"."""
     import numpy as np
     import oracle
     from gen.synth import CONFIGS, generate
@@ -203,16 +221,36 @@ def cpu_baseline(cfg, cases: int, device, gpu_cases=None):
     k = min(cases, spec.n_cases)
     L = generate(spec, 0, k, device=device)
     c, a, t = L.case.cpu().numpy(), L.act.cpu().numpy(), L.ts.cpu().numpy()
+    del L
     oracle.build()
     t0 = time.perf_counter()
     r = oracle.run(c, a, t, spec.n_activities)
     dt = time.perf_counter() - t0
+    whole = k == spec.n_cases
     out = {"value": c.size / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
-           "sample": f"first {k:,} cases ({c.size:,} events) of the {cfg} "
-                     f"workload; single-threaded O1 (stable sort + loop), {dt:.2f} s"}
-    if gpu_cases is not None:
-        ne, du = gpu_cases
-        out["per_case_parity_on_sample"] = bool(np.array_equal(ne[:k], r.n_events) and np.array_equal(du[:k], r.dur))
+           "sample": (f"the whole {cfg} workload" if whole else f"first {k:,} cases of the {cfg} workload") +
+                     f" ({c.size:,} events); single-threaded O1, {dt:.2f} s (stable sort {r.t_sort:.2f} s, "
+                     f"loop {r.t_loop:.2f} s)",
+           "stage_s": {"sort": round(r.t_sort, 3), "loop": round(r.t_loop, 3), "total": round(dt, 3)}}
+    if gpu_out:
+        g = gpu_out
+        if whole:
+            checks = {
+                "dfg_count": np.array_equal(g["cnt"], r.cnt), "dfg_sum": np.array_equal(g["sum"], r.sum),
+                "dfg_mean": np.array_equal(g["mean"], r.mean),
+                "start": np.array_equal(g["start"], r.start), "end": np.array_equal(g["end"], r.end),
+                "case_code": np.array_equal(g["case_code"], r.case_code),
+                "n_events": np.array_equal(g["n_events"], r.n_events), "dur": np.array_equal(g["dur"], r.dur),
+                "variant_count": np.array_equal(g["v_count"], r.v_count),
+                "variant_len": np.array_equal(g["v_len"], r.v_len),
+                "variant_rep": np.array_equal(g["v_rep"], r.v_rep),
+                "variant_off": np.array_equal(g["v_off"], r.v_off),
+                "variant_seq": np.array_equal(g["v_act"], r.v_act),
+                "case_variant": np.array_equal(g["case_variant"], r.case_variant)}
+            out["o1_whole_log_bit_exact"] = {"all": all(checks.values()), **checks}
+        else:
+            out["per_case_parity_on_sample"] = bool(np.array_equal(g["n_events"][:k], r.n_events) and
+                                                    np.array_equal(g["dur"][:k], r.dur))
     return out
 
 
@@ -260,7 +298,9 @@ def main():
     ap.add_argument("--impl", default="pm4g", choices=["pm4g", "reference"])
     ap.add_argument("--filter", action="store_true", help="events-mode time filter in the step (1B-style)")
     ap.add_argument("--e2e-steps", type=int, default=8)
-    ap.add_argument("--cpu-cases", type=int, default=4_000_000)
+    ap.add_argument("--cpu-cases", type=int, default=0,
+                    help="oracle sample: the first K cases (default 0 = the whole config, compared element by "
+                         "element with a GPU step)")
     ap.add_argument("--ref-cases", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stages", action="store_true", help="print the per-kernel table to stderr")
@@ -478,15 +518,22 @@ def main():
                 print(f"  {t0 - t00:9.3f} gap {t0 - prev_end:8.3f}  {d:8.3f}  {nm}", file=sys.stderr)
                 prev_end = t0 + d
 
-    kept = {}
+    # the oracle sees cases [0, k) of the config: comparable with this rank's outputs
+    # when the rank holds the config from case 0 and no filter runs
+    comparable = (rank == 0 and not args.no_cpu_baseline and filt is None and meta["case_lo"] == 0
+                  and world == 1 and shard_world == 1)
+    kept = {} if comparable else None
     verified = check_invariants(pm4g, case, act, ts, meta, comm, out, filt, dist, dev, kept)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        gpu_cases = None
-        if filt is None and meta["case_lo"] == 0:   # the oracle sample is cases [0, k) of the config
-            k = min(args.cpu_cases, meta["case_hi"] - meta["case_lo"])
-            gpu_cases = (kept["n_events"][:k].cpu().numpy(), kept["dur"][:k].cpu().numpy())
-        cpu = cpu_baseline(args.config, args.cpu_cases, dev, gpu_cases)
+        del case, act, ts
+        torch.cuda.empty_cache()
+        cpu = cpu_baseline(args.config, args.cpu_cases or 1 << 62, dev, kept)
+        if "o1_whole_log_bit_exact" in cpu:
+            verified["o1_whole_log_bit_exact"] = cpu["o1_whole_log_bit_exact"]["all"]
+            verified["all"] = verified["all"] and verified["o1_whole_log_bit_exact"]
+        if not verified["all"]:
+            print("bench: outputs NOT verified (see 'verified'); the line is flagged invalid", file=sys.stderr)
 
     if rank == 0:
         line = {
@@ -496,7 +543,7 @@ def main():
             "config": workload_config(args.config, n_local, meta["case_hi"] - meta["case_lo"], meta["A"], world,
                                       filt is not None, n_total),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "verified": verified,
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu, "valid": bool(verified["all"]),
             "hbm_pipeline": {"algorithmic_GB_per_step": step_bytes / args.steps / 1e9,
                              "achieved_GB_per_s": step_bytes / (ms / 1e3) / 1e9,
                              "frac_of_peak": step_bytes / (ms / 1e3) / 1e9 / peak},

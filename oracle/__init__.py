@@ -52,6 +52,7 @@ def _load():
             getattr(L, f).restype = I64
         L.orc_overflow.argtypes = [P]
         L.orc_overflow.restype = I32
+        L.orc_timing.argtypes = [P, P, P]
         L.orc_get_sorted.argtypes = [P, P, P, P, P]
         L.orc_get_dfg.argtypes = [P, P, P, P]
         L.orc_get_start_end.argtypes = [P, P, P]
@@ -108,6 +109,8 @@ class OracleResult:
     v_off: np.ndarray        # u64[V+1]
     v_act: np.ndarray        # u32[sum len]
     overflow: bool
+    t_sort: float = 0.0      # wall seconds of step 1 (stable sort) in O1
+    t_loop: float = 0.0      # wall seconds of steps 2 + 3 (the loop) in O1
 
     @property
     def n_cases(self) -> int:
@@ -152,10 +155,12 @@ def run(case, act, ts, n_activities: int) -> OracleResult:
                               np.empty(V + 1, np.uint64), np.empty(T, np.uint32))
         L.orc_get_variants(h, _ptr(vc), _ptr(vl), _ptr(vr), _ptr(vo), _ptr(va))
         ov = bool(L.orc_overflow(h))
+        tsort, tloop = ctypes.c_double(0), ctypes.c_double(0)
+        L.orc_timing(h, ctypes.byref(tsort), ctypes.byref(tloop))
     finally:
         L.orc_free(h)
     return OracleResult(A, sc, sa, st, pm, cnt.reshape(A, A), sm.reshape(A, A), mn.reshape(A, A),
-                        s0, e0, cc, ne, du, fr, cv, vc, vl, vr, vo, va, ov)
+                        s0, e0, cc, ne, du, fr, cv, vc, vl, vr, vo, va, ov, tsort.value, tloop.value)
 
 
 def filter_time(case, ts, t1: int, t2: int, mode: int) -> np.ndarray:

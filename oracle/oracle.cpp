@@ -36,6 +36,7 @@
 // __int128 shadow records whether any sum wrapped.
 // ============================================================================
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -83,6 +84,7 @@ struct orc_result {
     std::vector<uint32_t> v_act;
     std::vector<uint32_t> case_variant;  // per case (ascending code): output index
     int overflow = 0;
+    double t_sort = 0, t_loop = 0;       // wall seconds of step 1 / steps 2 + 3 (timing only)
 };
 
 extern "C" {
@@ -106,6 +108,7 @@ orc_result* orc_run(int64_t n, const uint32_t* case_, const uint32_t* act,
     orc_result* r = new orc_result();
     r->A = A;
     r->n = n;
+    const auto t0 = std::chrono::steady_clock::now();
 
     // ---- step 1: stable sort of row indices by (case, ts)  (R1, R2)
     std::vector<int64_t> idx(n);
@@ -123,6 +126,9 @@ orc_result* orc_run(int64_t n, const uint32_t* case_, const uint32_t* act,
         r->s_act[k] = act[idx[k]];
         r->s_ts[k] = ts[idx[k]];
     }
+
+    const auto t1 = std::chrono::steady_clock::now();
+    r->t_sort = std::chrono::duration<double>(t1 - t0).count();
 
     // ---- steps 2 + 3: one loop over the formatted log
     const size_t AA = (size_t)A * A;
@@ -199,7 +205,14 @@ orc_result* orc_run(int64_t n, const uint32_t* case_, const uint32_t* act,
         out_index[s] = (uint32_t)i;
     }
     for (auto& s : case_seq) r->case_variant.push_back(out_index[s]);
+    r->t_loop = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
     return r;
+}
+
+// per-stage wall time of the last orc_run on r (timing instrumentation only)
+void orc_timing(const orc_result* r, double* sort_s, double* loop_s) {
+    *sort_s = r->t_sort;
+    *loop_s = r->t_loop;
 }
 
 void orc_free(orc_result* r) { delete r; }

@@ -63,6 +63,25 @@ def test_time_filters_random(seed, sort_first):
         _check(out, _expect(case, act, ts, A, keep))
 
 
+@pytest.mark.parametrize("n", [2_500_003, 4_000_000])
+def test_events_filter_ring_wraps_element_by_element(n):
+    """k_filter_cols streams each CTA's 2048-row tiles through a 3-stage TMA ring;
+    with n >= 2.5M rows (> 3 x grid tiles) every CTA wraps its ring several times.
+    The filtered log, formatted, equals O1 on exactly the kept rows element by
+    element (sorted columns, ties broken by ingest order -- so a row dropped,
+    duplicated or reordered by the compaction fails), plus every aggregate."""
+    rng = np.random.default_rng(n)
+    case = rng.integers(0, n // 8, n)
+    act = rng.integers(0, 40, n)
+    ts = rng.integers(0, 2000, n)          # many timestamp ties inside a case
+    t1, t2 = 300, 1700
+    log = _log(case, act, ts, 40, n // 8)
+    out = log.filter_time(t1, t2, 0)
+    keep = oracle.filter_time(case, ts, t1, t2, 0)
+    assert out.n == int(keep.sum())
+    _check(out, _expect(case, act, ts, 40, keep))
+
+
 def test_time_filter_rejects_bad_range():
     log = _log([0, 1], [0, 0], [1, 2], 1, 2)
     with pytest.raises(pm4g.Pm4gError) as e:
