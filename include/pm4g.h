@@ -44,7 +44,8 @@ typedef enum pm4g_status {
     PM4G_ENOMEM = 3,     /* device or host allocation failed */
     PM4G_ECUDA = 4,      /* a CUDA runtime error (message carries cudaGetErrorString) */
     PM4G_ENCCL = 5,      /* an NCCL error, or NCCL could not be loaded */
-    PM4G_EKEYWIDTH = 6,  /* case_bits + ts_bits > 64: composite key does not fit */
+    PM4G_EKEYWIDTH = 6,  /* reserved, no longer returned: logs whose case_bits + ts_bits > 64
+                            take the wide path of pm4g_sort */
     PM4G_ECOLLISION = 7  /* reserved, never returned: variant-key collisions (local or across
                             ranks) are always resolved exactly by verification + re-keying */
 } pm4g_status;
@@ -120,7 +121,12 @@ pm4g_status pm4g_log_info_get(const pm4g_log* log, pm4g_log_info* info);
  * (ts - ts_min) with the activity (and a row index when extra columns exist) as
  * payload; stability realises the third criterion (R2).  Then materialises the
  * case segments (the cases dataframe's row ranges).
- * Idempotent.  PM4G_EKEYWIDTH if case_bits + ts_bits > 64.
+ * Idempotent.  Wide path (case_bits + ts_bits > 64, e.g.
+ * microsecond timestamps over years with millions of cases; S:39 fixes
+ * timestamps as full signed 64-bit): the key is ts - ts_min alone (up to 64
+ * bits), the radix passes take their case digits from the case column through
+ * the ingest-row payload, and the formatted log keeps each row's case beside
+ * it; every output is identical to the narrow path's definition.
  * Synchronises `stream` once: the host learns whether any case needs the exact
  * fallback (cases longer than 1024 rows, or running > 512 rows past a 4096-row
  * tile; they are then sorted by one batched segmented radix sort, one more

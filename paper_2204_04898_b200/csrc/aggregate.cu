@@ -109,13 +109,14 @@ __device__ __forceinline__ void smem_acc(uint32_t* cnt, uint32_t* lo, uint32_t* 
     if (h) atomicAdd(hi, h);
 }
 
-template <class P, int MODE, bool MM>
+// WIDE: the log's key is ts - ts_min alone; a row's case is rcase[row]
+template <class P, int MODE, bool MM, bool WIDE = false>
 __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
     uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
     int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak,
-    uint32_t* __restrict__ cco, uint32_t case_min) {
+    uint32_t* __restrict__ cco, uint32_t case_min, const uint32_t* __restrict__ rcase) {
     constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
     constexpr int AGG_STAGES = AggGeom<MODE>::STAGES;
     using Stage = AggStage<P, AGG_STAGE>;
@@ -208,7 +209,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                 // directly-follows pairs (r, r+1) of one case
                 for (uint32_t r = e0 + ct; r + 1 < e1; r += AGG_CONSUMERS) {
                     const uint64_t kk = K_at(r), kn = K_at(r + 1);
-                    if (!same_case(kk, kn, ts_bits)) continue;
+                    if (WIDE ? rcase[r] != rcase[r + 1] : !same_case(kk, kn, ts_bits)) continue;
                     const uint32_t e = A_at(r) * A + A_at(r + 1);
                     const uint64_t d = kn - kk;
                     if (MODE == TAB_FULL) {
@@ -268,7 +269,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                     }
                 }
                 if (n_events) n_events[c] = l - f + 1;
-                if (cco) cco[c] = case_min + case32(K_at(f), ts_bits);
+                if (cco) cco[c] = case_min + (WIDE ? rcase[f] : case32(K_at(f), ts_bits));
                 if (dur) dur[c] = (int64_t)(K_at(l) - K_at(f));
                 if (k1o) {
                     uint64_t h1 = 0, h2 = 0;
@@ -307,13 +308,13 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     }
 }
 
-template <class P, int MODE, bool MM>
-static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
+template <class P, int MODE, bool MM, bool WIDE>
+static pm4g_status launch_agg_w(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
     const size_t tab = o.tables ? (size_t)tab_words_for<P, MM>(MODE, A) * 4 : 0;
     constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
     const size_t smem = tab + AggGeom<MODE>::STAGES * sizeof(AggStage<P, AGG_STAGE>);
-    PM4G_MAX_SMEM(k_aggregate<P, MODE, MM>);
+    PM4G_MAX_SMEM(k_aggregate<P, MODE, MM, WIDE>);
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     // cases per tile: a tile's rows should fit one stage (mean length from the
     // case-code range, exact when codes are dense; a rare oversized tile is
@@ -324,14 +325,19 @@ static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s
     const int per_sm = std::max(1, (int)std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
-    const double bytes = (double)L->n * (8 + sizeof(P)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
+    const double bytes = (double)L->n * (8 + sizeof(P) + (WIDE ? 4 : 0)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
                          (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0) + (o.case_code ? cap * 4.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, MODE, MM><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
+                (k_aggregate<P, MODE, MM, WIDE><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
                     o.tables ? o.packed : nullptr, o.mm, o.n_events, o.dur, o.k1, o.k2,
-                    debug_weak_hash() ? 1 : 0, o.case_code, L->case_min)));
+                    debug_weak_hash() ? 1 : 0, o.case_code, L->case_min, L->rcase)));
     return PM4G_OK;
+}
+
+template <class P, int MODE, bool MM>
+static pm4g_status launch_agg(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
+    return L->wide ? launch_agg_w<P, MODE, MM, true>(L, o, s) : launch_agg_w<P, MODE, MM, false>(L, o, s);
 }
 
 template <class P>

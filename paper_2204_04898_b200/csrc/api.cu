@@ -333,7 +333,8 @@ void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, 
     L->case_bits = bit_width_u64((uint64_t)(L->case_max - L->case_min));
     L->ts_bits = bit_width_u64(ts_span);
     L->key_bits = L->case_bits + L->ts_bits;
-    L->passes = (std::min(L->key_bits, 64) + 7) / 8;
+    L->wide = L->key_bits > 64;
+    L->passes = L->wide ? (L->case_bits + 7) / 8 : (std::min(L->key_bits, 64) + 7) / 8;
     L->hist_passes = 0;
     const int cb = std::max(L->case_bits, 1);
     const int sp = (cb + 7) / 8, sb = (cb + sp - 1) / sp;
@@ -580,6 +581,7 @@ pm4g_status pm4g_log_destroy(pm4g_log* L) {
     dfree(L->key, s);
     dfree(L->s_act, s);
     dfree(L->perm, s);
+    dfree(L->rcase, s);
     dfree(L->off, s);
     dfree(L->s_case_code, s);
     dfree(L->d_n_cases, s);
@@ -613,9 +615,6 @@ pm4g_status pm4g_log_info_get(const pm4g_log* L, pm4g_log_info* info) {
 }
 
 static pm4g_status sort_impl(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
-    if (L->key_bits > 64)
-        return fail(PM4G_EKEYWIDTH, "case_bits + ts_bits = " + std::to_string(L->key_bits) +
-                                        " > 64: composite key does not fit");
     PM4G_TRY(sort_log(L, s, d));   // sort + case offsets (format kernel)
     free_log_cols(L, s);
     L->sorted = true;

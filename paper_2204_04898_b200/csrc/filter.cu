@@ -30,10 +30,12 @@ struct RowView {
     const uint32_t* cs;      // ingested
     const int64_t* ts;       // ingested
     const uint64_t* key;     // formatted
+    const uint32_t* rcase;   // formatted wide log: case - case_min per row
     int ts_bits;
     uint32_t case_min;
     int64_t ts_min;
     __device__ __forceinline__ uint32_t case_of(int64_t i) const {
+        if (rcase) return case_min + rcase[i];
         return key ? case_min + (uint32_t)shr64(key[i], ts_bits) : cs[i];
     }
     __device__ __forceinline__ int64_t ts_of(int64_t i) const {
@@ -46,6 +48,7 @@ static RowView view_of(const pm4g_log* L) {
     v.cs = L->sorted ? nullptr : L->case_;
     v.ts = L->sorted ? nullptr : L->ts;
     v.key = L->sorted ? L->key : nullptr;
+    v.rcase = L->sorted ? L->rcase : nullptr;
     v.ts_bits = L->ts_bits;
     v.case_min = L->case_min;
     v.ts_min = L->ts_min;
@@ -447,6 +450,10 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
             if ((st = dalloc((void**)&L->perm, N * 4, s))) return bail(st);
             add(in->perm, L->perm, 4);
         }
+        if (in->rcase) {
+            if ((st = dalloc((void**)&L->rcase, (N + 32) * 4, s))) return bail(st);
+            add(in->rcase, L->rcase, 4);
+        }
     } else {
         L->owns_cols = true;
         if ((st = dalloc((void**)&L->case_, N * 4, s))) return bail(st);
@@ -549,6 +556,7 @@ static pm4g_status compact_log(const pm4g_log* in, const uint8_t* keep, cudaStre
         L->case_bits = in->case_bits;
         L->ts_bits = in->ts_bits;
         L->key_bits = in->key_bits;
+        L->wide = in->wide;
         L->passes = in->passes;
         if ((st = segments(L, s))) return bail(st);
     } else {

@@ -114,8 +114,11 @@ struct pm4g_log {
     uint32_t case_lo = 0, case_hi = 0;
     int64_t ts_min = 0, ts_max = -1;
     uint32_t case_min = 0, case_max = 0;   // present range
-    // composite key ((case - case_min) << ts_bits) | (ts - ts_min)
+    // composite key ((case - case_min) << ts_bits) | (ts - ts_min); a WIDE log
+    // (case_bits + ts_bits > 64) keys on ts - ts_min alone and carries the case
+    // per formatted row in rcase (SURVEY.md 8(a) A2 "otherwise the wide path")
     int case_bits = 0, ts_bits = 0, key_bits = 0, passes = 0;
+    bool wide = false;
     bool sorted = false;
     bool broken = false;        // a deferred format step failed: every call on the log fails
     // ingested state
@@ -127,6 +130,7 @@ struct pm4g_log {
     uint64_t* key = nullptr;    // [n] sorted composite keys
     void* s_act = nullptr;      // [n] sorted activities
     uint32_t* perm = nullptr;   // [n] ingest row of each formatted row (only with extras)
+    uint32_t* rcase = nullptr;  // [n] case - case_min of each formatted row (wide logs only)
     uint32_t* off = nullptr;    // [n_cases + 1] case row offsets (CSR)
     uint32_t* s_case_code = nullptr;  // [n_cases] case code of each case
     uint64_t* d_n_cases = nullptr;    // device scalar

@@ -109,6 +109,11 @@ struct PassArgs {
     uint32_t* tile_counter;
     bool aligned;                // every input array 16-byte aligned (TMA bulk path)
     uint32_t* next_status;       // the next pass's look-back words (zeroed here, row per tile), or nullptr
+    // wide logs (case_bits + ts_bits > 64): the key is ts - ts_min only, the
+    // payload row is the ingest row, and a pass's digit is digit `wshift` of
+    // case_col[ingest row] - case_min (pass 0 reads the case column directly)
+    const uint32_t* case_col;
+    int wshift;
 };
 
 // Shared-memory layout of one tile (all offsets multiples of 16):
@@ -117,7 +122,7 @@ struct PassArgs {
 // After ranking every key is in registers, so the keys are permuted IN PLACE
 // (u_key holds them in digit order for the write-out); payloads are copied to
 // v_*.  (FROM_COLS builds the keys over the consumed u_ts.)
-template <class P, bool FROM_COLS, bool WITH_IDX>
+template <class P, bool FROM_COLS, bool WITH_IDX, bool WIDE = false>
 struct OsLayout {
     static constexpr size_t T = SORT_TILE;
     static constexpr size_t o_in = 0;                                   // u_key or u_ts
@@ -126,7 +131,8 @@ struct OsLayout {
     static constexpr size_t o_act = o_idx + (WITH_IDX ? T * 4 : 0);
     static constexpr size_t o_vidx = (o_act + T * sizeof(P) + 15) / 16 * 16;
     static constexpr size_t o_vact = o_vidx + (WITH_IDX ? T * 4 : 0);
-    static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
+    static constexpr size_t o_vdig = (o_vact + T * sizeof(P) + 15) / 16 * 16;   // WIDE: digits in digit order
+    static constexpr size_t bytes = (o_vdig + (WIDE ? T : 0) + 15) / 16 * 16;
 };
 
 struct NoHook {
@@ -137,12 +143,13 @@ struct NoHook {
 // tile's rows are in u_key (FROM_COLS: u_case, u_ts) and u_act; s_whist must
 // be zero on entry.  after_rank() runs (every thread) once the tile's inputs
 // other than u_act / u_key are no longer read (after the ranking barrier).
-template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, class Hook = NoHook>
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, class Hook = NoHook, bool WIDE = false>
 __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& a, const uint32_t tile,
                                         const uint32_t nvalid, uint64_t* u_key, const int64_t* u_ts,
                                         const uint32_t* u_case, const uint32_t* u_idx, const P* u_act,
                                         uint32_t* v_idx, P* v_act, uint32_t (*s_whist)[RADIX],
-                                        long long* s_gbase, uint32_t* s_scan, Hook after_rank = Hook()) {
+                                        long long* s_gbase, uint32_t* s_scan, Hook after_rank = Hook(),
+                                        uint8_t* v_dig = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)tile * SORT_TILE;
     const uint32_t dmask = (1u << a.bits) - 1;
@@ -171,7 +178,13 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         uint32_t d = dmask;
         k[j] = ~0ull;
         if (li < nvalid) {
-            if (FROM_COLS) {   // pass 0: its digit is the low bits of case - case_min (shift == ts_bits)
+            if (FROM_COLS && WIDE) {   // wide pass 0: key = ts - ts_min, digit from the case column
+                k[j] = (uint64_t)u_ts[li] - (uint64_t)a.kp.ts_min;
+                d = (u_case[li] - a.kp.case_min) & dmask;
+            } else if (WIDE) {         // wide pass p: digit of the ingest row's case
+                k[j] = u_key[li];
+                d = ((a.case_col[u_idx[li]] - a.kp.case_min) >> a.wshift) & dmask;
+            } else if (FROM_COLS) {   // pass 0: its digit is the low bits of case - case_min (shift == ts_bits)
                 const uint32_t crel = u_case[li] - a.kp.case_min;
                 k[j] = make_key(crel, u_ts[li], a.kp.ts_min, a.kp.ts_bits);
                 d = crel & dmask;
@@ -243,6 +256,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         u_key[p] = k[j];
         v_act[p] = u_act[li];
         if (WITH_IDX) v_idx[p] = gen_idx ? (uint32_t)(base + li) : u_idx[li];
+        if (WIDE) v_dig[p] = (uint8_t)(dp[j] >> 16);
     }
 
     // ---- decoupled look-back for this digit, 4 predecessors per round trip
@@ -277,7 +291,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         const uint32_t sidx = j * SORT_THREADS + tid;
         if (sidx < nvalid) {
             const uint64_t kk = u_key[sidx];
-            const long long g = s_gbase[digit(kk)] + sidx;
+            const long long g = s_gbase[WIDE ? (uint32_t)v_dig[sidx] : digit(kk)] + sidx;
             a.out_key[g] = kk;
             a.out_act[g] = v_act[sidx];
             if (WITH_IDX) a.out_idx[g] = v_idx[sidx];
@@ -287,9 +301,9 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
 
 // HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
 // the digits sit above ts_bits >= 32), extracted with one 32-bit shift
-template <class P, bool FROM_COLS, bool WITH_IDX, bool HI>
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, bool WIDE = false>
 __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
-    using Lay = OsLayout<P, FROM_COLS, WITH_IDX>;
+    using Lay = OsLayout<P, FROM_COLS, WITH_IDX, WIDE>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* u_key = (uint64_t*)(smem + Lay::o_in);
     int64_t* u_ts = (int64_t*)(smem + Lay::o_in);
@@ -347,8 +361,9 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
         __syncthreads();
     }
 
-    os_tile<P, FROM_COLS, WITH_IDX, HI>(a, tile, nvalid, u_key, u_ts, u_case, u_idx, u_act, v_idx, v_act,
-                                        s_whist, s_gbase, s_scan);
+    os_tile<P, FROM_COLS, WITH_IDX, HI, NoHook, WIDE>(a, tile, nvalid, u_key, u_ts, u_case, u_idx, u_act, v_idx,
+                                                      v_act, s_whist, s_gbase, s_scan, NoHook(),
+                                                      (uint8_t*)(smem + Lay::o_vdig));
 }
 
 // Persistent form of a key pass (keys + a u8/u16 activity, no ingest row):
@@ -566,6 +581,14 @@ static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles,
 template <class P, bool FC, bool WI>
 static pm4g_status launch_pass(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                const char* name, double bytes) {
+    if constexpr (WI) {
+        if (args.case_col) {   // wide log: one-tile-per-CTA kernel, digits from the case column
+            const size_t smem = OsLayout<P, FC, WI, true>::bytes;
+            PM4G_MAX_SMEM(k_onesweep<P, FC, WI, false, true>);
+            PM4G_LAUNCH(name, bytes, s, (k_onesweep<P, FC, WI, false, true><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
+            return PM4G_OK;
+        }
+    }
     if (args.shift >= 32 && args.shift < 64) return launch_pass_t<P, FC, WI, true>(args, tiles, s, name, bytes);
     return launch_pass_t<P, FC, WI, false>(args, tiles, s, name, bytes);
 }
@@ -580,7 +603,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
                             const P* in_act, const uint32_t* in_idx, uint64_t* key_out, P* act_out,
                             uint32_t* idx_out, int64_t n, int shift0, int bits_total, KeyParams kp,
                             cudaStream_t s, const char* pass_name = "k_onesweep",
-                            const uint32_t* pre_hist = nullptr) {
+                            const uint32_t* pre_hist = nullptr, const uint32_t* wide_case = nullptr) {
     const bool from_cols = in_case != nullptr;
     bits_total = std::max(1, bits_total);
     const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
@@ -631,13 +654,18 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
                                     aligned16(in_case) && aligned16(in_ts) && aligned16(ca) &&
                                         (!ci || aligned16(ci)),
                                     p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
+            a.case_col = wide_case;
+            a.wshift = 0;
             PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
         } else {
             PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, shift, bits, kp,
                                      off + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p,
                                      aligned16(ck) && aligned16(ca) && (!ci || aligned16(ci)),
                                      p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
-            PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr)));
+            a.case_col = wide_case;
+            a.wshift = p * bits;
+            PM4G_TRY(launch_pass(a, tiles, s, pass_name,
+                                 n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr + (wide_case ? 4.0 : 0.0))));
         }
         ck = ok;
         ca = oa;
@@ -675,13 +703,18 @@ struct FmtArgs {
     uint32_t* big;             // ranks of fallback cases
     uint32_t* big_count;
     bool aligned;              // gkey / gact / gidx 16-byte aligned (TMA bulk path)
+    // wide logs: gkey = ts - ts_min, gidx = ingest row; the case of a row is
+    // case_col[gidx] - case_min, written to rcase_out alongside the formatted row
+    const uint32_t* case_col;
+    uint32_t* rcase_out;
 };
 
 // the TMA targets (s_key at 0, s_act, s_idx) must stay 16-byte aligned
 static_assert(((FMT_BUF * 8 + FMT_BUF * 2 * 2 + (FMT_TILE + 8) * 2 + (FMT_TILE + 16)) % 16) == 0, "s_act alignment");
 
-template <class P, bool WI>
+template <class P, bool WI, bool WIDE = false>
 __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
+    static_assert(!WIDE || WI, "the wide format reads the ingest-row payload");
     extern __shared__ __align__(16) unsigned char fsm[];
     uint64_t* s_key = (uint64_t*)fsm;                              // [FMT_BUF]
     uint16_t* s_dst = (uint16_t*)(s_key + FMT_BUF);                // [FMT_BUF]
@@ -690,6 +723,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     uint8_t* s_wide = (uint8_t*)(s_head + FMT_TILE + 8);           // [FMT_TILE + 16] case needs 64-bit ranks
     P* s_act = (P*)(s_wide + FMT_TILE + 16);                       // [FMT_BUF] (16-byte aligned: TMA target)
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
+    uint32_t* s_c = s_idx + FMT_BUF;                                                      // WIDE: case of each row
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
     __shared__ uint32_t s_prefix, s_nbig, s_bigh[16];
     __shared__ int s_ext, s_wlast[FMT_THREADS / 32];
@@ -721,13 +755,21 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             if (WI) s_idx[p] = a.gidx[base + p];
         }
     }
+    // the case of global row i (case - case_min)
+    auto gcase = [&](int64_t i) -> uint32_t {
+        return WIDE ? a.case_col[a.gidx[i]] - a.case_min : case32(a.gkey[i], tb);
+    };
     uint32_t prev_case = 0;
     {
         const int64_t pi = base + warp * (32 * FMT_IPT) - 1;
-        if (pi >= 0 && pi < a.n) prev_case = case32(a.gkey[pi], tb);
+        if (pi >= 0 && pi < a.n) prev_case = gcase(pi);
     }
     __syncthreads();
     if (bulk) mbar_wait(&s_bar, 0);
+    if (WIDE) {
+        for (int p = tid; p < tn; p += FMT_THREADS) s_c[p] = a.case_col[s_idx[p]] - a.case_min;
+        __syncthreads();
+    }
     uint32_t ball[FMT_IPT], wc = 0;
     {
         uint32_t prev = prev_case;
@@ -736,7 +778,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             const int li = warp * (32 * FMT_IPT) + j * 32 + lane;
             const int64_t i = base + li;
             const bool ok = li < tn;
-            const uint32_t c = ok ? case32(s_key[li], tb) : 0u;
+            const uint32_t c = ok ? (WIDE ? s_c[li] : case32(s_key[li], tb)) : 0u;
             uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
             if (lane == 0) pc = prev;
             prev = __shfl_sync(0xffffffffu, c, 31);
@@ -797,10 +839,11 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             int ext = 0;
             if (base + tn < a.n) {
                 const uint64_t last = s_key[lastp];
+                const uint32_t lastc = WIDE ? s_c[lastp] : 0u;
                 ext = -1;
                 for (int o = 0; o <= FMT_EXT; o += 32) {
                     const int64_t i = base + tn + o + lane;
-                    const bool stop = i >= a.n || !same_case(a.gkey[i], last, tb);
+                    const bool stop = i >= a.n || (WIDE ? gcase(i) != lastc : !same_case(a.gkey[i], last, tb));
                     const uint32_t bb = __ballot_sync(0xffffffffu, stop);
                     if (bb) {
                         const int e = o + __ffs(bb) - 1;
@@ -826,6 +869,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             s_key[p] = a.gkey[i];
             s_act[p] = a.gact[i];
             if (WI) s_idx[p] = a.gidx[i];
+            if (WIDE) s_c[p] = a.case_col[s_idx[p]] - a.case_min;
             s_ci[p] = (uint16_t)(H - 1);
         }
         wsync();
@@ -876,7 +920,8 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             const int64_t g = base + dp;
             a.key_out[g] = s_key[p];
             a.act_out[g] = s_act[p];
-            if (WI) a.perm_out[g] = s_idx[p];
+            if (WI && a.perm_out) a.perm_out[g] = s_idx[p];
+            if (WIDE) a.rcase_out[g] = s_c[p];
         }
     }
     __syncthreads();
@@ -886,7 +931,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     for (uint32_t h = tid; h < H; h += FMT_THREADS) {
         const int hp = s_head[h];
         a.off[R0 + h] = (uint32_t)(base + hp);
-        a.case_code[R0 + h] = a.case_min + case32(s_key[hp], tb);
+        a.case_code[R0 + h] = a.case_min + (WIDE ? s_c[hp] : case32(s_key[hp], tb));
     }
     if (tid < min(s_nbig, 16u)) a.big[atomicAdd(a.big_count, 1u)] = R0 + s_bigh[tid];
     if (tid == 0 && base + tn >= a.n) {
@@ -946,6 +991,7 @@ __global__ void k_big_gather(FmtArgs<P> a, const uint64_t* __restrict__ seg_star
         a.key_out[dst] = a.gkey[src];
         a.act_out[dst] = a.gact[src];
         if (a.perm_out) a.perm_out[dst] = a.gidx[src];
+        if (a.rcase_out) a.rcase_out[dst] = a.case_col[a.gidx[src]] - a.case_min;
     }
 }
 
@@ -981,14 +1027,18 @@ static pm4g_status format_launch(FmtArgs<P>& fa, Scratch& st, cudaStream_t s) {
     fa.big_count = fa.counter + 1;
     fa.status = fa.counter + 2;
     fa.big = fa.status + tiles;
-    const bool wi = fa.perm_out != nullptr;
+    const bool wide = fa.rcase_out != nullptr;
+    const bool wi = fa.gidx != nullptr;
     fa.aligned = aligned16(fa.gkey) && aligned16(fa.gact) && (!wi || aligned16(fa.gidx));
     const size_t smem_base = (size_t)FMT_BUF * (8 + 2 + 2 + sizeof(P)) + (FMT_TILE + 8) * 2 + (FMT_TILE + 16) + 16;
-    const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0);
+    const size_t smem = smem_base + (wi ? (size_t)FMT_BUF * 4 : 0) + (wide ? (size_t)FMT_BUF * 4 : 0);
     PM4G_MAX_SMEM(k_format<P, false>);
     PM4G_MAX_SMEM(k_format<P, true>);
-    const double bytes = (double)n * (2.0 * (8 + sizeof(P) + (wi ? 4 : 0)));
-    if (wi)
+    PM4G_MAX_SMEM(k_format<P, true, true>);
+    const double bytes = (double)n * (2.0 * (8 + sizeof(P) + (wi ? 4 : 0)) + (wide ? 8.0 : 0.0));
+    if (wide)
+        PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
+    else if (wi)
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, true><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
     else
         PM4G_LAUNCH("k_format", bytes, s, (k_format<P, false><<<(unsigned)tiles, FMT_THREADS, smem, s>>>(fa)));
@@ -1055,7 +1105,11 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
 template <class P>
 static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     const int64_t n = L->n;
-    const bool wi = !L->extra.empty();
+    // the ingest row travels with every row when extra columns must follow the
+    // order (perm) or when the log is wide (the row's case is looked up by it)
+    const bool wide = L->wide;
+    const bool extras = !L->extra.empty();
+    const bool wi = extras || wide;
     KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
     // 1. stable LSD passes over the case bits of the composite key (built on the fly)
     Scratch grp(s);
@@ -1068,7 +1122,8 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     const uint32_t* pre = L->hist_passes > 0 ? L->hist : nullptr;
     if (wi)
         PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, gidx, n,
-                                    L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre)));
+                                    wide ? 0 : L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre,
+                                    wide ? L->case_ : nullptr)));
     else
         PM4G_TRY((lsd_sort<P, false>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, nullptr,
                                      n, L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre)));
@@ -1082,7 +1137,9 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     fa.case_min = L->case_min;
     fa.key_out = L->key;
     fa.act_out = (P*)L->s_act;
-    fa.perm_out = wi ? L->perm : nullptr;
+    fa.perm_out = extras ? L->perm : nullptr;
+    fa.case_col = wide ? L->case_ : nullptr;
+    fa.rcase_out = wide ? L->rcase : nullptr;
     fa.off = L->off;
     fa.case_code = L->s_case_code;
     fa.n_cases = L->d_n_cases;
@@ -1126,6 +1183,7 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
 constexpr int SEG_THREADS = 256, SEG_IPT = 16, SEG_TILE = SEG_THREADS * SEG_IPT;
 
 __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __restrict__ key,
+                                                          const uint32_t* __restrict__ rcase,
                                                           int64_t n, int ts_bits, uint32_t case_min,
                                                           uint32_t* __restrict__ off,
                                                           uint32_t* __restrict__ case_code,
@@ -1144,14 +1202,14 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
     uint32_t prev_last = 0;
     {
         int64_t pi = wbase - 1;
-        if (pi >= 0 && pi < n) prev_last = case32(key[pi], ts_bits);
+        if (pi >= 0 && pi < n) prev_last = rcase ? rcase[pi] : case32(key[pi], ts_bits);
     }
     uint32_t wcount = 0;
 #pragma unroll
     for (int j = 0; j < SEG_IPT; ++j) {
         int64_t i = wbase + j * 32 + lane;
         bool ok = i < n;
-        uint32_t c = ok ? case32(key[i], ts_bits) : 0u;
+        uint32_t c = ok ? (rcase ? rcase[i] : case32(key[i], ts_bits)) : 0u;
         uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
         if (lane == 0) pc = prev_last;
         prev_last = __shfl_sync(0xffffffffu, c, 31);
@@ -1218,7 +1276,7 @@ pm4g_status segments(pm4g_log* L, cudaStream_t s) {
     PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * 4, s));
     uint32_t* status = st.as<uint32_t>();
     PM4G_LAUNCH("k_segments", n * 8.0, s,
-                k_segments<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(L->key, n, L->ts_bits, L->case_min,
+                k_segments<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(L->key, L->rcase, n, L->ts_bits, L->case_min,
                                                                   L->off, L->s_case_code,
                                                                   L->d_n_cases, status + 1, status));
     return PM4G_OK;
@@ -1284,13 +1342,16 @@ pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed) {
 }
 
 pm4g_status sort_log(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
-    if (d && !L->extra.empty()) d = nullptr;   // extra columns are gathered by the final order: no deferral
+    // extra columns are gathered by the final order, and a wide log's format reads
+    // the ingest columns: no deferral
+    if (d && (!L->extra.empty() || L->wide)) d = nullptr;
     const int64_t n = L->n;
     const bool wi = !L->extra.empty();
     // +32 rows: 16-byte aligned TMA reads of the formatted log may run one vector past n
     PM4G_TRY(dalloc_t(&L->key, (size_t)n + 32, s));
     PM4G_TRY(dalloc(&L->s_act, ((size_t)n + 32) * L->act_bytes, s));
     if (wi) PM4G_TRY(dalloc_t(&L->perm, std::max<int64_t>(n, 1), s));
+    if (L->wide) PM4G_TRY(dalloc_t(&L->rcase, (size_t)n + 32, s));
     // offsets: number of cases <= min(n, case range)
     dfree(L->off, s);
     dfree(L->s_case_code, s);
@@ -1345,14 +1406,15 @@ pm4g_status radix_sort_u64_to(const uint64_t* keys, const uint32_t* vals, uint32
 
 // ------------------------------------------------------------------ decode (formatted log view)
 template <class P>
-__global__ void k_decode(const uint64_t* __restrict__ key, const P* __restrict__ sact, int64_t n,
+__global__ void k_decode(const uint64_t* __restrict__ key, const uint32_t* __restrict__ rcase,
+                         const P* __restrict__ sact, int64_t n,
                          int ts_bits, uint32_t case_min, int64_t ts_min, uint32_t* __restrict__ oc,
                          uint32_t* __restrict__ oa, int64_t* __restrict__ ot) {
     const uint64_t m = low_mask(ts_bits);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = key[i];
-        if (oc) oc[i] = case_min + (uint32_t)shr64(k, ts_bits);
+        if (oc) oc[i] = case_min + (rcase ? rcase[i] : (uint32_t)shr64(k, ts_bits));
         if (oa) oa[i] = (uint32_t)sact[i];
         if (ot) ot[i] = (int64_t)((uint64_t)ts_min + (k & m));
     }
@@ -1371,9 +1433,9 @@ extern "C" pm4g_status pm4g_sorted_columns(const pm4g_log* L, uint32_t* case_cod
     if (n == 0) return PM4G_OK;
     int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 8));
     switch (L->act_bytes) {
-        case 1: PM4G_LAUNCH("k_decode", n * 25.0, s, k_decode<uint8_t><<<g, 256, 0, s>>>(L->key, (const uint8_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
-        case 2: PM4G_LAUNCH("k_decode", n * 26.0, s, k_decode<uint16_t><<<g, 256, 0, s>>>(L->key, (const uint16_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
-        default: PM4G_LAUNCH("k_decode", n * 28.0, s, k_decode<uint32_t><<<g, 256, 0, s>>>(L->key, (const uint32_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
+        case 1: PM4G_LAUNCH("k_decode", n * 25.0, s, k_decode<uint8_t><<<g, 256, 0, s>>>(L->key, L->rcase, (const uint8_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
+        case 2: PM4G_LAUNCH("k_decode", n * 26.0, s, k_decode<uint16_t><<<g, 256, 0, s>>>(L->key, L->rcase, (const uint16_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
+        default: PM4G_LAUNCH("k_decode", n * 28.0, s, k_decode<uint32_t><<<g, 256, 0, s>>>(L->key, L->rcase, (const uint32_t*)L->s_act, n, L->ts_bits, L->case_min, L->ts_min, case_code, act, ts)); break;
     }
     return PM4G_OK;
 }

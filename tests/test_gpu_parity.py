@@ -118,13 +118,62 @@ def test_all_ones_key_ties():
     check_log([3, 2, 3, 3, 2, 3], [0, 1, 2, 1, 0, 2], [m, -(2**62), m, 0, m, m], 3)
 
 
-def test_key_too_wide_is_reported():
-    """case_bits + ts_bits > 64 -> PM4G_EKEYWIDTH (wide-key path is future work)."""
-    c, a, t = to_device_cols([0, 2**31, 5], [0, 0, 0], [-(2**62), 2**62, 0], 1)
-    log = pm4g.pm4g_log_create(c, a, t, 1, n_case_codes=2**32 - 1)
-    with pytest.raises(pm4g.Pm4gError) as e:
-        log.sort()
-    assert e.value.status == pm4g.PM4G_EKEYWIDTH
+def test_wide_key_small():
+    """case_bits + ts_bits > 64 (here 32 + 64): the wide path
+    keys on ts - ts_min alone and carries the case per row; results equal O1."""
+    c, a, t = [0, 2**31, 5, 2**31, 0, 5, 5], [0, 1, 0, 2, 1, 1, 0], [-(2**62), 2**62, 0, -7, 3, 0, 0]
+    g, r = check_log(c, a, t, 3, n_case_codes=2**32 - 1)
+    c2, a2, t2 = to_device_cols(c, a, t, 3)
+    log = pm4g.pm4g_log_create(c2, a2, t2, 3, n_case_codes=2**32 - 1)
+    info = log.info()
+    assert info.key_bits > 64 and info.case_bits == 32
+    log.close()
+
+
+def test_wide_key_with_extra_columns_and_filters():
+    """A wide log with an extra column (ingest-row perm and case payload both
+    travel) and the formatted-log filters / re-segmentation on a wide log."""
+    from tests.parity import collect
+    rng = np.random.default_rng(5)
+    n = 30_000
+    case = rng.integers(0, 40_000, n) * 97            # codes up to ~3.9e6: 22 case bits
+    act = rng.integers(0, 6, n)
+    ts = rng.integers(-(2**50), 2**50, n)             # 51 ts bits: 73-bit composite key
+    ts[::7] = ts[3]                                   # ties
+    c, a, t = to_device_cols(case, act, ts, 6)
+    ex = [pm4g.Extra(pm4g.PM4G_KIND_I64, torch.as_tensor(rng.integers(0, 100, n)).cuda())]
+    log = pm4g.pm4g_log_create(c, a, t, 6, n_case_codes=int(case.max()) + 1, extra=ex)
+    assert log.info().key_bits > 64
+    log.sort()
+    assert_parity(collect(log), oracle.run(case, act, ts, 6))
+    # formatted wide log -> events-mode time filter -> re-segmented wide log
+    t1, t2 = -(2**49), 2**49
+    f = log.filter_time(t1, t2, pm4g.PM4G_TIME_EVENTS)
+    keep = oracle.filter_time(case, ts, t1, t2, oracle.EVENTS)
+    assert_parity(collect(f), oracle.run(case[keep], act[keep], ts[keep], 6))
+    # case-level attribute filter on the wide formatted log
+    g = log.filter_attr(codes=[2], level=pm4g.PM4G_LEVEL_CASES)
+    keep = oracle.filter_attr(case, act, codes=[2], level=1)
+    assert_parity(collect(g), oracle.run(case[keep], act[keep], ts[keep], 6))
+
+
+@pytest.mark.parametrize("long_case", [False, True])
+def test_wide_key_fallback_and_sort_analyze(long_case):
+    """Wide logs through pm4g_sort_analyze (non-deferred for wide) including cases
+    longer than 1024 rows (the batched exact fallback with 64-bit keys)."""
+    rng = np.random.default_rng(17)
+    n = 50_000
+    case = rng.integers(0, 2**24, n)
+    if long_case:
+        case[:5000] = 12345
+        case[5000:7000] = 2**24 - 1
+    ts = rng.integers(-(2**60), 2**60, n)
+    ts[:5000:3] = 42                                   # ties inside the long case
+    act = rng.integers(0, 9, n)
+    p = rng.permutation(n)
+    case, act, ts = case[p], act[p], ts[p]
+    assert_parity(gpu_run(case, act, ts, 9, n_case_codes=2**24, sort_analyze=True),
+                  oracle.run(case, act, ts, 9))
 
 
 def test_validation_errors():
@@ -224,7 +273,8 @@ def test_cnt16_table_flush_exact(A):
 
 
 @pytest.mark.parametrize("ts_bits,case_bits", [(0, 12), (1, 20), (24, 8), (31, 9), (32, 10), (33, 18),
-                                               (40, 24), (56, 8), (62, 2), (63, 1), (64, 0), (20, 32)])
+                                               (40, 24), (56, 8), (62, 2), (63, 1), (64, 0), (20, 32),
+                                               (45, 24), (64, 24), (40, 32), (64, 32), (57, 8), (33, 32)])
 def test_digit_shift_boundaries(ts_bits, case_bits):
     """Onesweep digits sit at shift = ts_bits + 8p: the 64-bit path (shift < 32),
     the high-word path (32 <= shift < 64) and the single-case guard (shift 64);
@@ -247,8 +297,7 @@ def test_digit_shift_boundaries(ts_bits, case_bits):
         if ts_bits == 64:
             ts[3] = 2**63 - 1
     act = rng.integers(0, 5, n)
-    if case_bits + ts_bits > 64:
-        pytest.skip("key wider than 64 bits")
+    # case_bits + ts_bits > 64 takes the wide path (key = ts - ts_min, case per row)
     check_log(case.tolist(), act.tolist(), ts.tolist(), 5, n_case_codes=int(case.max()) + 1)
 
 
