@@ -683,6 +683,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
 constexpr int FMT_THREADS = 512, FMT_IPT = 8, FMT_TILE = FMT_THREADS * FMT_IPT;
 constexpr int FMT_EXT = 512, FMT_BUF = FMT_TILE + FMT_EXT;
 constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
+constexpr int FMT_TIES = 512;       // tie groups listed per tile (more: laid out in place)
 
 template <class P>
 struct FmtArgs {
@@ -717,15 +718,16 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     static_assert(!WIDE || WI, "the wide format reads the ingest-row payload");
     extern __shared__ __align__(16) unsigned char fsm[];
     uint64_t* s_key = (uint64_t*)fsm;                              // [FMT_BUF]
-    uint16_t* s_dst = (uint16_t*)(s_key + FMT_BUF);                // [FMT_BUF]
-    uint16_t* s_ci = s_dst + FMT_BUF;                              // [FMT_BUF] case of each row
+    uint16_t* s_perm = (uint16_t*)(s_key + FMT_BUF);               // [FMT_BUF] slot -> row
+    uint16_t* s_ci = s_perm + FMT_BUF;                              // [FMT_BUF] case of each row
     uint16_t* s_head = s_ci + FMT_BUF;                             // [FMT_TILE + 8]
     uint8_t* s_wide = (uint8_t*)(s_head + FMT_TILE + 8);           // [FMT_TILE + 16] case needs 64-bit ranks
     P* s_act = (P*)(s_wide + FMT_TILE + 16);                       // [FMT_BUF] (16-byte aligned: TMA target)
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
     uint32_t* s_c = s_idx + FMT_BUF;                                                      // WIDE: case of each row
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
-    __shared__ uint32_t s_prefix, s_nbig, s_bigh[16];
+    __shared__ uint32_t s_prefix, s_nbig, s_bigh[16], s_ntie;
+    __shared__ uint16_t s_tie[FMT_TIES];   // slots starting a group of equal keys
     __shared__ int s_ext, s_wlast[FMT_THREADS / 32];
     __shared__ __align__(8) uint64_t s_bar;
 
@@ -796,14 +798,24 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         s_wlast[warp] = lasth;
     }
     __syncthreads();
-    uint32_t H = 0, wex = 0;
-    int lastp = -1;
+    // warp-exclusive head count, total heads H and the tile's last head, by
+    // lane-parallel scans over the 16 warp entries (every warp computes them)
+    uint32_t H, wex;
+    int lastp;
+    {
+        constexpr int NWF = FMT_THREADS / 32;
+        const uint32_t cw = lane < NWF ? s_wt[lane] : 0u;
+        int lw = lane < NWF ? s_wlast[lane] : -1;
+        uint32_t inc = cw;
 #pragma unroll
-    for (int w = 0; w < FMT_THREADS / 32; ++w) {
-        const uint32_t c = s_wt[w];
-        wex += (w < warp) ? c : 0u;
-        H += c;
-        lastp = max(lastp, s_wlast[w]);
+        for (int o = 1; o < NWF; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+            lw = max(lw, __shfl_xor_sync(0xffffffffu, lw, o));
+        }
+        H = __shfl_sync(0xffffffffu, inc, NWF - 1);
+        wex = __shfl_sync(0xffffffffu, inc - cw, warp);
+        lastp = __shfl_sync(0xffffffffu, lw, 0);   // the max over lanes 0..15
     }
 
     // ---- 2. concurrently: every warp writes its heads and row->case indices;
@@ -876,53 +888,89 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
 
         // ---- 4a. narrow cases: every key within +-2^30 of the case's first key,
         // so any two keys of the case differ by < 2^31 and a comparison is the
-        // sign of their 32-bit low-word difference (exact, modular)
-        for (int p = h0 + wt; p < oend; p += NW) {
-            const uint32_t h = s_ci[p];
-            const int64_t d = (int64_t)(s_key[p] - s_key[s_head[h]]);
-            if (d < -(1ll << 30) || d >= (1ll << 30)) s_wide[h] = 1;
-        }
-        wsync();
-
-        // ---- 4. rank each row inside its case: #(key_j < key_p) + #(j < p with key_j == key_p).
-        // Event-parallel with one uniform loop per case (a warp mostly reads one
-        // case -> broadcast smem reads, equal trip counts).
+        // sign of their 32-bit low-word difference (exact, modular).  Slots
+        // (= output positions, the case's own row range) start empty (0xffff);
+        // rows of a fallback case mark theirs 0xfffe.
         for (int p = h0 + wt; p < oend; p += NW) {
             const uint32_t h = s_ci[p];
             const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
-            if (e0 - s0 > FMT_WARP_MAX) {      // long case: exact fallback
-                s_dst[p] = 0xffff;
-                if (p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
-                continue;
-            }
-            // #(key_j < key_p) + #(j < p with key_j == key_p) = #(key_j < key_p + [j < p]):
-            // one 64-bit compare per element; the all-ones key (key_bits = 64)
-            // has no successor and takes the two-compare form
+            const bool big = e0 - s0 > FMT_WARP_MAX;   // long case: exact fallback
+            s_perm[p] = big ? (uint16_t)0xfffe : (uint16_t)0xffff;
+            if (big && p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
+            const int64_t d = (int64_t)(s_key[p] - s_key[s0]);
+            if (d < -(1ll << 30) || d >= (1ll << 30)) s_wide[h] = 1;
+        }
+        if (wt == 0) s_ntie = 0;
+        wsync();
+
+        // ---- 4. rank each row inside its case and claim slot s0 + rank.
+        // Narrow cases: rank = #(key_j < key_p), one 32-bit subtract + sign per
+        // element; rows with equal keys (ties) claim the same slot, leaving
+        // empty slots behind it, and phase 5 lays the tied rows out in ingest
+        // order.  Wide cases: the exact stable rank #(key_j < key_p) + #(j < p
+        // with key_j == key_p) (unique slots).  Event-parallel with one loop per
+        // case (a warp mostly reads one case -> broadcast smem reads).
+        for (int p = h0 + wt; p < oend; p += NW) {
+            const uint32_t h = s_ci[p];
+            const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
+            if (e0 - s0 > FMT_WARP_MAX) continue;
             int r = 0;
             const uint64_t ki = s_key[p], ki1 = ki + 1;
-            if (!s_wide[h]) {   // 32-bit: r += sign(lo_j - lo_T), T = ki + [j < p]
-                const uint32_t* lo = (const uint32_t*)s_key;   // low word of key j at lo[2 j]
-                const uint32_t ti = (uint32_t)ki, ti1 = ti + 1u;
-                for (int j = s0; j < e0; ++j) r += (int)((lo[2 * j] - (j < p ? ti1 : ti)) >> 31);
-            } else if (ki1 != 0) {
+            if (!s_wide[h]) {
+                const uint32_t* lo = (const uint32_t*)(s_key + s0);   // low word of key s0 + j at lo[2 j]
+                const uint32_t ti = (uint32_t)ki;
+                const int m = e0 - s0;
+                // four elements per trip, the < 4 left over predicated (no
+                // remainder loops: lanes of one warp have different m)
+                int j = 0;
+#pragma unroll 1
+                for (; j + 4 <= m; j += 4)
+                    r += (int)(((lo[2 * j] - ti) >> 31) + ((lo[2 * j + 2] - ti) >> 31) +
+                               ((lo[2 * j + 4] - ti) >> 31) + ((lo[2 * j + 6] - ti) >> 31));
+                if (j < m) r += (int)((lo[2 * j] - ti) >> 31);
+                if (j + 1 < m) r += (int)((lo[2 * j + 2] - ti) >> 31);
+                if (j + 2 < m) r += (int)((lo[2 * j + 4] - ti) >> 31);
+            } else if (ki1 != 0) {   // the all-ones key (key_bits = 64) has no successor
                 for (int j = s0; j < e0; ++j) r += s_key[j] < (j < p ? ki1 : ki);
             } else {
                 for (int j = s0; j < e0; ++j) r += (s_key[j] < ki) | ((s_key[j] == ki) & (j < p));
             }
-            s_dst[p] = (uint16_t)(s0 + r);
+            s_perm[s0 + r] = (uint16_t)p;
         }
         wsync();
 
-        // ---- 5. write the formatted rows of the owned range
-        for (int p = h0 + wt; p < oend; p += NW) {
-            const uint32_t dp = s_dst[p];
-            if (dp == 0xffff) continue;   // rows of a fallback case
-            const int64_t g = base + dp;
-            a.key_out[g] = s_key[p];
-            a.act_out[g] = s_act[p];
-            if (WI && a.perm_out) a.perm_out[g] = s_idx[p];
-            if (WIDE) a.rcase_out[g] = s_c[p];
+        // ---- 5. write the formatted rows of the owned range, slot by slot
+        // (consecutive threads, consecutive output rows).  A slot followed by
+        // an empty one starts a group of equal keys: those are listed and laid
+        // out in ingest order after the loop.
+        auto put = [&](int src, int slot) {
+            const int64_t g = base + slot;
+            a.key_out[g] = s_key[src];
+            a.act_out[g] = s_act[src];
+            if (WI && a.perm_out) a.perm_out[g] = s_idx[src];
+            if (WIDE) a.rcase_out[g] = s_c[src];
+        };
+        auto ties = [&](int q) {   // slots q, q+1, ... <- the rows of key(s_perm[q]), ascending row
+            const int p = s_perm[q];
+            const uint32_t h = s_ci[p];
+            const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
+            const uint64_t kq = s_key[p];
+            for (int j = s0, o = q; j < e0; ++j)
+                if (s_key[j] == kq) put(j, o++);
+        };
+        for (int q = h0 + wt; q < oend; q += NW) {
+            const uint32_t p = s_perm[q];
+            if (p >= 0xfffe) continue;   // a fallback case's row, or an empty slot after a tie
+            if (q + 1 < oend && s_perm[q + 1] == 0xffff) {
+                const uint32_t t = atomicAdd(&s_ntie, 1u);
+                if (t < FMT_TIES) s_tie[t] = (uint16_t)q;
+                else ties(q);
+                continue;
+            }
+            put((int)p, q);
         }
+        wsync();
+        for (uint32_t t = wt; t < min(s_ntie, (uint32_t)FMT_TIES); t += NW) ties(s_tie[t]);
     }
     __syncthreads();
 

@@ -406,3 +406,36 @@ def test_sort_analyze_fallback_over_stale_allocator_blocks():
     ts = rng.integers(0, 10**7, n)
     assert_parity(gpu_run(case, act, ts, 7, n_case_codes=20, sort_analyze=True), oracle.run(case, act, ts, 7))
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("ts_range", [1, 3, 40, 10**4])
+@pytest.mark.parametrize("extras", [False, True])
+def test_format_tie_groups(ts_range, extras):
+    """k_format ranks rows of narrow cases by #(smaller keys) only: rows with
+    equal keys claim one slot and are laid out in ingest order afterwards (a
+    per-tile list of tie groups, or in place once the list is full).  Cases of
+    1-300 rows with timestamps from a small range give from a few tie groups per
+    tile (listed) to thousands (list overflow); results equal the oracle's
+    (ties keep the absolute index order)."""
+    rng = np.random.default_rng(ts_range)
+    lens = np.concatenate([rng.integers(1, 30, 15_000), rng.integers(100, 300, 300)])
+    case = np.repeat(rng.permutation(lens.size), lens)
+    n = case.size
+    case = case[rng.permutation(n)]
+    act = rng.integers(0, 9, n)
+    ts = rng.integers(0, ts_range, n) * 1000 - 7
+    if extras:   # the ingest-row payload orders an extra column: an event-level range
+        # filter on it after the sort must keep exactly the oracle's rows
+        from tests.parity import collect
+        c, a, t = to_device_cols(case, act, ts, 9)
+        x = rng.integers(0, 100, n)
+        log = pm4g.pm4g_log_create(c, a, t, 9, n_case_codes=int(case.max()) + 1,
+                                   extra=[pm4g.Extra(pm4g.PM4G_KIND_I64, torch.as_tensor(x).cuda())])
+        log.sort()
+        assert_parity(collect(log), oracle.run(case, act, ts, 9))
+        f = log.filter_attr(column=0, lo=20, hi=60)
+        keep = oracle.filter_attr(case, x, lo=20, hi=60)
+        assert_parity(collect(f), oracle.run(case[keep], act[keep], ts[keep], 9))
+    else:
+        assert_parity(gpu_run(case, act, ts, 9, n_case_codes=int(case.max()) + 1),
+                      oracle.run(case, act, ts, 9))
