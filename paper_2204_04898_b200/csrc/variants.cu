@@ -733,6 +733,415 @@ void free_variants(pm4g_variant_table* v) {
     delete v;
 }
 
+// ------------------------------------------------------------------ the case grouping, one pass
+// The usual call (items = the cases of one log, weight 1, order = case rank,
+// full-strength hash) groups, counts, finds representatives and verifies in
+// ONE persistent kernel, k_vgroup:
+//   * the global open-addressing table maps a key (k1, k2) to a dense group id
+//     (claim order) and the group's canonical case (its claimer): one 128-bit
+//     CAS claims a slot, the claimer then publishes (gid, case) in one 64-bit
+//     store that finders wait for;
+//   * every CTA keeps a shared-memory cache of the keys it has met (key, gid,
+//     canonical offset / length, local count, local min case) across its chunks,
+//     so a Zipf-hot variant costs shared-memory work only; the cache is flushed
+//     into the dense per-group arrays once at the end;
+//   * every case is verified against its group's canonical sequence on the
+//     spot (sequence equality is an equivalence, so any member serves as the
+//     reference); a mismatch (a hash collision) is counted, and the host then
+//     reruns the general round-based engine (group_items) from scratch.
+// Result: item_group[c] = dense gid, per-group count / min case / total length,
+// i.e. the Groups of group_items without a compaction or item pass.
+constexpr int VG_THREADS = 256, VG_IPT = 4, VG_TASK = 32 * VG_IPT;   // a warp's task: 128 consecutive cases
+constexpr int VG_CACHE = 2048, VG_FILL = VG_CACHE / 2, VG_PROBES = 8, VG_GBLOCK = 8;
+constexpr size_t VG_SMEM = (size_t)VG_CACHE * (8 + 8 + 4 + 4 + 4 + 4 + 4);
+constexpr unsigned long long VG_NOMETA = ~0ull;
+
+// global slot: key, then (gid << 32 | canonical offset, canonical length)
+// published by the claimer in one 16-byte atomic
+struct alignas(32) VSlot {
+    unsigned long long k1, k2;
+    alignas(16) unsigned long long meta;
+    unsigned long long len;
+};
+
+__global__ void k_vinit(VSlot* table, uint64_t cap, uint32_t* g_w, uint32_t* g_rep, uint64_t gcap) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap || i < gcap;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < cap) {
+            VSlot z;
+            z.k1 = 0;
+            z.k2 = 0;
+            z.meta = VG_NOMETA;
+            z.len = 0;
+            table[i] = z;
+        }
+        if (i < gcap) {
+            g_w[i] = 0;
+            g_rep[i] = 0xffffffffu;
+        }
+    }
+}
+
+// exact equality of two activity sequences of length len (u8: aligned 8-byte
+// words, the first five of each issued together -- 33+ rows take the loop)
+template <class ACT>
+__device__ __forceinline__ bool seq_same(const ACT* acts, uint32_t f, uint32_t rf, uint32_t len) {
+    if (f == rf) return true;
+    if constexpr (sizeof(ACT) == 1) {
+        if (len <= 32) {
+            const uint64_t* wa = (const uint64_t*)((const uint8_t*)acts + (f & ~7u));
+            const uint64_t* wb = (const uint64_t*)((const uint8_t*)acts + (rf & ~7u));
+            const uint32_t sa = (f & 7) * 8, sb = (rf & 7) * 8;
+            uint64_t a[5], b[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const bool need = 8u * i < len + 8u;
+                a[i] = need ? wa[i] : 0;
+                b[i] = need ? wb[i] : 0;
+            }
+            uint64_t diff = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (8u * i >= len) break;
+                const uint64_t x = sa ? (a[i] >> sa) | (a[i + 1] << (64 - sa)) : a[i];
+                const uint64_t y = sb ? (b[i] >> sb) | (b[i + 1] << (64 - sb)) : b[i];
+                const uint64_t m = (len - 8u * i >= 8) ? ~0ull : ((1ull << (8 * (len - 8u * i))) - 1);
+                diff |= (x ^ y) & m;
+            }
+            return diff == 0;
+        }
+    }
+    return seq_equal(acts, (uint64_t)f, (uint64_t)rf, (uint64_t)len);
+}
+
+// ctl: [0] overflow, [1] gids reserved (the warps' blocks), [2] collisions, [3] groups claimed
+template <class ACT>
+__global__ __launch_bounds__(VG_THREADS) void k_vgroup(
+    uint64_t n_items, const uint64_t* __restrict__ d_n, const uint64_t* __restrict__ k1,
+    const uint64_t* __restrict__ k2, const uint32_t* __restrict__ off, const ACT* __restrict__ acts,
+    VSlot* table, uint64_t mask, uint32_t gcap, uint32_t* __restrict__ g_w, uint32_t* __restrict__ g_rep,
+    uint32_t* __restrict__ item_gid, uint32_t* ctl, unsigned long long* total_len, uint32_t* task_counter) {
+    extern __shared__ __align__(16) unsigned char vg_sm[];
+    unsigned long long* c_k1 = (unsigned long long*)vg_sm;   // claim word (0: free)
+    unsigned long long* c_k2 = c_k1 + VG_CACHE;              // written last: the entry is ready
+    uint32_t* c_gid = (uint32_t*)(c_k2 + VG_CACHE);
+    uint32_t* c_off = c_gid + VG_CACHE;   // canonical sequence: offset and length
+    uint32_t* c_len = c_off + VG_CACHE;
+    uint32_t* c_cnt = c_len + VG_CACHE;   // local count / min case of the entry
+    uint32_t* c_rep = c_cnt + VG_CACHE;
+    __shared__ uint32_t s_fill, s_claims;
+    __shared__ unsigned long long s_len;
+    for (int i = threadIdx.x; i < VG_CACHE; i += VG_THREADS) {
+        c_k1[i] = 0;
+        c_k2[i] = 0;
+        c_cnt[i] = 0;
+        c_rep[i] = 0xffffffffu;
+    }
+    if (threadIdx.x == 0) {
+        s_fill = 0;
+        s_claims = 0;
+        s_len = 0;
+    }
+    __syncthreads();
+    if (d_n) n_items = min(n_items, *d_n);
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    auto chash = [](uint64_t a) { return (uint32_t)(a ^ (a >> 29)) & (VG_CACHE - 1); };
+    uint32_t claims = 0, gnext = 0, gend = 0;   // gend - gnext: the warp's unused reserved gids
+    unsigned long long lensum = 0;
+    for (;;) {
+        uint64_t task = 0;
+        if (lane == 0) task = atomicAdd((unsigned long long*)task_counter, 1ull);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task * VG_TASK >= n_items) break;
+        uint32_t f[VG_IPT], l[VG_IPT], gid[VG_IPT], cof[VG_IPT], cln[VG_IPT];
+        uint64_t ka[VG_IPT], kb[VG_IPT];
+        int hit[VG_IPT];   // cache entry, -1: miss, -2: none (past the end / abandoned / collision)
+#pragma unroll
+        for (int u = 0; u < VG_IPT; ++u) {
+            const uint64_t t = task * VG_TASK + u * 32 + lane;
+            hit[u] = -2;
+            if (t >= n_items) continue;
+            hit[u] = -1;
+            ka[u] = k1[t];
+            kb[u] = k2[t];
+            f[u] = off[t];
+            l[u] = off[t + 1];
+        }
+        // A: the CTA's cache (an entry is used once its k2 is written)
+#pragma unroll
+        for (int u = 0; u < VG_IPT; ++u) {
+            if (hit[u] != -1) continue;
+            uint32_t h = chash(ka[u]);
+            for (int p = 0; p < VG_PROBES; ++p) {
+                const unsigned long long c = ld_volatile(&c_k1[h]);
+                if (c == 0) break;
+                if (c == ka[u] && ld_volatile(&c_k2[h]) == kb[u]) {
+                    __threadfence_block();
+                    hit[u] = (int)h;
+                    gid[u] = c_gid[h];
+                    cof[u] = c_off[h];
+                    cln[u] = c_len[h];
+                    break;
+                }
+                h = (h + 1) & (VG_CACHE - 1);
+            }
+        }
+        // B: misses find or claim their global slot (key and meta read together).
+        // A claimer takes its gid from the warp's block of reserved gids and
+        // publishes (gid, canonical offset, length) in one 16-byte atomic;
+        // finders wait for that.
+#pragma unroll
+        for (int u = 0; u < VG_IPT; ++u) {
+            const bool miss = hit[u] == -1;
+            VSlot* sp = nullptr;
+            bool mine = false;
+            K128 m{VG_NOMETA, 0};
+            if (miss) {
+                uint64_t h = (ka[u] ^ (ka[u] >> 29) ^ (kb[u] * 0x9E3779B97F4A7C15ull)) & mask;
+                for (uint64_t probes = 0;; ++probes) {
+                    sp = &table[h];
+                    K128 cur = ld_k128(sp);
+                    m = ld_k128(&sp->meta);
+                    if (cur.a == 0 && cur.b == 0) {
+                        K128 exp{0, 0}, des{ka[u], kb[u]};
+                        cur = atomicCAS((K128*)sp, exp, des);
+                        mine = cur.a == 0 && cur.b == 0;
+                    }
+                    if (mine || (cur.a == ka[u] && cur.b == kb[u])) break;
+                    if (probes >= mask || ((probes & 31) == 31 && ld_volatile(&ctl[0]))) {
+                        atomicExch(&ctl[0], 1u);
+                        sp = nullptr;
+                        break;
+                    }
+                    h = (h + 1) & mask;
+                }
+            }
+            const uint32_t cm = __ballot_sync(0xffffffffu, mine);
+            if (cm) {
+                const uint32_t nc = __popc(cm);
+                if (gnext + nc > gend) {   // refill the warp's gid block
+                    const uint32_t take = max(nc, (uint32_t)VG_GBLOCK);
+                    uint32_t b = 0;
+                    if (lane == 0) b = atomicAdd(&ctl[1], take);
+                    gnext = __shfl_sync(0xffffffffu, b, 0);
+                    gend = gnext + take;
+                }
+                if (mine) {
+                    const uint32_t g = gnext + __popc(cm & lt);
+                    if (g >= gcap) atomicExch(&ctl[0], 1u);
+                    K128 exp{VG_NOMETA, 0}, des{((unsigned long long)g << 32) | f[u], (unsigned long long)(l[u] - f[u])};
+                    atomicCAS((K128*)&sp->meta, exp, des);
+                    gid[u] = g;
+                    cof[u] = f[u];
+                    cln[u] = l[u] - f[u];
+                    ++claims;
+                    lensum += l[u] - f[u];
+                    if (g >= gcap) hit[u] = -2;
+                }
+                gnext += nc;
+            }
+            if (miss && !mine) {
+                if (sp) {
+                    while (m.a == VG_NOMETA && !ld_volatile(&ctl[0])) {
+                        __nanosleep(16);
+                        m = ld_k128(&sp->meta);
+                    }
+                }
+                if (m.a == VG_NOMETA || (uint32_t)(m.a >> 32) >= gcap) {   // table abandoned
+                    hit[u] = -2;
+                } else {
+                    gid[u] = (uint32_t)(m.a >> 32);
+                    cof[u] = (uint32_t)m.a;
+                    cln[u] = (uint32_t)m.b;
+                }
+            }
+        }
+        // C: verify against the canonical sequence, count, and cache the misses
+#pragma unroll
+        for (int u = 0; u < VG_IPT; ++u) {
+            if (hit[u] == -2) continue;
+            const uint32_t t = (uint32_t)(task * VG_TASK + u * 32 + lane);
+            const uint32_t len = l[u] - f[u];
+            if (len != cln[u] || !seq_same(acts, f[u], cof[u], len)) {   // hash collision: rerun exactly
+                atomicAdd(&ctl[2], 1u);
+                continue;
+            }
+            item_gid[t] = gid[u];
+            if (hit[u] >= 0) {
+                atomicAdd(&c_cnt[hit[u]], 1u);
+                atomicMin(&c_rep[hit[u]], t);
+                continue;
+            }
+            bool cached = false;
+            if (ld_volatile(&s_fill) < VG_FILL) {
+                uint32_t h = chash(ka[u]);
+                for (int p = 0; p < VG_PROBES; ++p) {
+                    if (ld_volatile(&c_k1[h]) == 0 && atomicCAS(&c_k1[h], 0ull, (unsigned long long)ka[u]) == 0ull) {
+                        atomicAdd(&s_fill, 1u);
+                        c_gid[h] = gid[u];
+                        c_off[h] = cof[u];
+                        c_len[h] = cln[u];
+                        atomicAdd(&c_cnt[h], 1u);
+                        atomicMin(&c_rep[h], t);
+                        __threadfence_block();
+                        st_volatile(&c_k2[h], (unsigned long long)kb[u]);
+                        cached = true;
+                        break;
+                    }
+                    h = (h + 1) & (VG_CACHE - 1);
+                }
+            }
+            if (!cached) {
+                atomicAdd(&g_w[gid[u]], 1u);
+                atomicMin(&g_rep[gid[u]], t);
+            }
+        }
+    }
+    if (claims) atomicAdd(&s_claims, claims);
+    if (lensum) atomicAdd(&s_len, lensum);
+    __syncthreads();
+    // flush the cache's counts and minimum cases into the dense group arrays
+    for (int i = threadIdx.x; i < VG_CACHE; i += VG_THREADS) {
+        if (c_cnt[i]) {
+            atomicAdd(&g_w[c_gid[i]], c_cnt[i]);
+            atomicMin(&g_rep[c_gid[i]], c_rep[i]);
+        }
+    }
+    if (threadIdx.x == 0) {
+        if (s_claims) atomicAdd(&ctl[3], s_claims);
+        if (s_len) atomicAdd(total_len, s_len);
+    }
+}
+
+// dense groups -> Groups arrays (u64 weight, rep item = min case = order) and
+// the sort key ((Wmax - weight) << order_bits) | rep of each group
+__global__ void k_vfinal(const uint32_t* __restrict__ g_w, const uint32_t* __restrict__ g_rep, uint64_t G,
+                         int wbits, int order_bits, uint64_t* __restrict__ weight, uint32_t* __restrict__ rep_item,
+                         uint32_t* __restrict__ order, uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+    const uint64_t wmax = (1ull << wbits) - 1;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G; g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = g_w[g];
+        const uint32_t r = g_rep[g];
+        weight[g] = w;
+        rep_item[g] = r;
+        order[g] = r;
+        // an empty (reserved, unused) gid sorts after every group
+        key[g] = w ? ((wmax - min(w, wmax)) << order_bits) | r : low_mask(wbits + order_bits);
+        val[g] = (uint32_t)g;
+    }
+}
+
+// The one-pass grouping of a log's cases.  *fallback = true when the general
+// engine must run instead (a hash collision); otherwise *out holds the groups
+// in output order (sorted, inv) exactly as group_items leaves them.
+template <class ACT>
+static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const uint64_t* k2, const uint32_t* off,
+                                    const ACT* acts, int order_bits, cudaStream_t s, Groups* out,
+                                    const uint64_t* d_n, uint64_t* n_true, bool* fallback) {
+    *fallback = false;
+    if (n_true) *n_true = n_items;
+    Groups g;
+    auto bail = [&](pm4g_status st) {
+        g.free(s);
+        return st;
+    };
+    pm4g_status st;
+    const uint64_t N = std::max<uint64_t>(n_items, 1);
+    if ((st = dalloc_t(&g.item_group, N, s))) return bail(st);
+    if (n_items == 0) {
+        *out = g;
+        return PM4G_OK;
+    }
+    const uint64_t full = pow2_at_least(std::max<uint64_t>(1024, 2 * n_items));
+    uint64_t cap = std::min<uint64_t>(full, std::max<uint64_t>(1ull << 19, pow2_at_least(n_items / 8)));
+    if (const uint64_t dc = debug_variant_cap()) cap = std::min<uint64_t>(full, pow2_at_least(std::max<uint64_t>(dc, 64)));
+    uint64_t G = 0, Ga = 0, htot = 0, gcap = 0;
+    Scratch gw(s);
+    PM4G_MAX_SMEM(k_vgroup<ACT>);
+    static int per_sm = -1;
+    if (per_sm < 0)
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgroup<ACT>, VG_THREADS, VG_SMEM));
+    const uint64_t tasks = (n_items + VG_TASK - 1) / VG_TASK;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((tasks + VG_THREADS / 32 - 1) / (VG_THREADS / 32),
+                                                                    (uint64_t)std::max(per_sm, 1) * num_sms()));
+    const uint64_t slack = (uint64_t)grid * (VG_THREADS / 32) * 2 * VG_GBLOCK;   // unused reserved gids
+    for (int attempt = 0;; ++attempt) {
+        // groups never exceed the items; the table's claims stop near 3/4 load
+        // (reserved gids past gcap abandon the table)
+        gcap = std::min<uint64_t>(n_items, cap == full ? cap : cap / 4 * 3) + slack;
+        Scratch tab(s);
+        if ((st = tab.alloc(cap * sizeof(VSlot)))) return bail(st);
+        if ((st = gw.alloc(gcap * 8 + 64))) return bail(st);
+        uint32_t* g_w = gw.as<uint32_t>();
+        uint32_t* g_rep = g_w + gcap;
+        uint32_t* ctl = g_rep + gcap;   // [0] overflow [1] reserved gids [2] collisions [3] groups
+        unsigned long long* d_tot = (unsigned long long*)(ctl + 4);
+        uint32_t* d_task = ctl + 6;     // u64 task counter
+        PM4G_CK(cudaMemsetAsync(ctl, 0, 32, s));
+        PM4G_LAUNCH("k_variant_init", cap * 32.0 + gcap * 8.0, s,
+                    (k_vinit<<<gsz(std::max(cap, gcap)), 256, 0, s>>>(tab.as<VSlot>(), cap, g_w, g_rep, gcap)));
+        PM4G_LAUNCH("k_variant_group", n_items * 36.0, s,
+                    (k_vgroup<ACT><<<grid, VG_THREADS, VG_SMEM, s>>>(n_items, d_n, k1, k2, off, acts, tab.as<VSlot>(),
+                                                                     cap - 1, (uint32_t)gcap, g_w, g_rep,
+                                                                     g.item_group, ctl, d_tot, d_task)));
+        // one host round trip: overflow, gids, collisions, groups, total length (+ the case count)
+        static thread_local unsigned char* h_stage = nullptr;
+        if (!h_stage) PM4G_CK(cudaHostAlloc((void**)&h_stage, 64, cudaHostAllocDefault));
+        PM4G_CK(cudaMemcpyAsync(h_stage, ctl, 24, cudaMemcpyDeviceToHost, s));
+        if (d_n) PM4G_CK(cudaMemcpyAsync(h_stage + 32, d_n, 8, cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaStreamSynchronize(s));
+        uint32_t h[4];
+        memcpy(h, h_stage, 16);
+        memcpy(&htot, h_stage + 16, 8);
+        if (d_n) {
+            uint64_t hn;
+            memcpy(&hn, h_stage + 32, 8);
+            n_items = std::min(n_items, hn);
+            if (n_true) *n_true = n_items;
+        }
+        if (h[2]) {   // a collision: the general engine handles it exactly
+            *fallback = true;
+            return bail(PM4G_OK);
+        }
+        if (h[0]) {
+            if (cap >= full || attempt > 16) return bail(fail(PM4G_ENOMEM, "variant table overflow"));
+            cap = std::min<uint64_t>(full, cap * 4);
+            continue;
+        }
+        Ga = h[1];   // reserved gids: the groups plus the warps' unused ones (empty, sorted last)
+        G = h[3];
+        if (G > Ga) return bail(fail(PM4G_ECUDA, "variant grouping: gid count mismatch"));
+        break;
+    }
+    g.G = G;
+    g.total_len = htot;
+    const uint64_t Ga1 = std::max<uint64_t>(Ga, 1);
+    if ((st = dalloc_t(&g.weight, Ga1, s))) return bail(st);
+    if ((st = dalloc_t(&g.rep_item, Ga1, s))) return bail(st);
+    if ((st = dalloc_t(&g.order, Ga1, s))) return bail(st);
+    if ((st = dalloc_t(&g.sorted, Ga1, s))) return bail(st);
+    if ((st = dalloc_t(&g.inv, Ga1, s))) return bail(st);
+    const int wbits = std::max(1, bit_width_u64(n_items));
+    Scratch sk(s);   // keys [Ga] u64 | group ids [Ga] u32 (the radix payload)
+    if ((st = sk.alloc(Ga * 12 + 16))) return bail(st);
+    uint32_t* sk_val = (uint32_t*)(sk.as<uint64_t>() + Ga);
+    const uint32_t* g_w = gw.as<uint32_t>();
+    if (Ga) {
+        PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
+                    (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight, g.rep_item,
+                                                      g.order, sk.as<uint64_t>(), sk_val)));
+        if (Ga <= RANK_SORT_MAX)
+            PM4G_LAUNCH("k_rank_sort", Ga * 12.0, s,
+                        (k_rank_sort<<<(unsigned)((Ga + 255) / 256), 256, 0, s>>>(sk.as<uint64_t>(), (uint32_t)Ga, g.sorted)));
+        else if ((st = radix_sort_u64_to(sk.as<uint64_t>(), sk_val, g.sorted, (int64_t)Ga, wbits + order_bits, s)))
+            return bail(st);
+        PM4G_LAUNCH("k_variant_inv", Ga * 8.0, s, (k_inv<<<gsz(Ga), 256, 0, s>>>(g.sorted, Ga, g.inv)));
+    }
+    *out = g;
+    return PM4G_OK;
+}
+
 template <class OFF, class ACT>
 static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const uint64_t* k2,
                                   const OFF* off, const ACT* acts, const uint64_t* weight,
@@ -741,7 +1150,21 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
                                   const uint64_t* d_n = nullptr, uint64_t* n_true = nullptr) {
     Groups g;
     uint64_t nt = n_items;
-    PM4G_TRY((group_items<OFF, ACT>(n_items, k1, k2, off, acts, weight, order, order_bits, s, &g, d_n, &nt)));
+    bool general = true;
+    const uint64_t* dn = d_n;
+    if constexpr (sizeof(OFF) == 4) {   // a log's cases: the one-pass grouping unless it meets a collision
+        if (!weight && !order) {   // (weak debug keys collide: they exercise the fallback)
+            PM4G_TRY((group_cases_fast<ACT>(n_items, k1, k2, (const uint32_t*)off, acts, order_bits, s, &g, d_n, &nt,
+                                            &general)));
+            if (general) {   // the case count is known now
+                n_items = nt;
+                dn = nullptr;
+            }
+        }
+    }
+    if (general)
+        PM4G_TRY((group_items<OFF, ACT>(n_items, k1, k2, off, acts, weight, order, order_bits, s, &g,
+                                        dn, &nt)));
     n_items = nt;
     if (n_true) *n_true = nt;
     pm4g_variant_table* v = new pm4g_variant_table();
