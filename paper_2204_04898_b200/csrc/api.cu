@@ -403,12 +403,21 @@ pm4g_status check_log(const pm4g_log* L) {
     return PM4G_OK;
 }
 
-static void free_log_cols(pm4g_log* L, cudaStream_t s) {
+void free_log_cols(pm4g_log* L, cudaStream_t s) {
     if (L->owns_cols) {
         dfree(L->case_, s);
         dfree(L->act, s);
         dfree(L->ts, s);
     }
+    if (L->hold) {   // shared with a parent / child log: the last holder frees them
+        if (L->hold.use_count() == 1) {
+            dfree(L->hold->case_, s);
+            dfree(L->hold->act, s);
+            dfree(L->hold->ts, s);
+        }
+        L->hold.reset();
+    }
+    L->tf_n = -1;
     L->case_ = nullptr;
     L->act = nullptr;
     L->ts = nullptr;

@@ -658,6 +658,184 @@ static int case_grid(uint64_t C) {
     return (int)std::max<uint64_t>(1, std::min<uint64_t>((C + 255) / 256, (uint64_t)num_sms() * 8));
 }
 
+// ------------------------------------------------------------------ A1 fused into the sort
+// Events-mode time filter on an ingested log (the usual filter -> sort step,
+// P:126): the filtered log is created lazily.  One scan of the case and ts
+// columns (12 B/row) counts the kept rows and builds their metadata and
+// case-digit histograms; the rows themselves are not copied -- the sort's
+// first radix pass reads the shared raw columns and ranks only the kept rows
+// (sort.cu, PassArgs::tf).  Saves the compaction's 13 B/row read + 13 B/kept
+// row write + the sort's 13 B/kept row re-read.
+__global__ __launch_bounds__(256) void k_tf_scan(const uint32_t* __restrict__ cs, const int64_t* __restrict__ ts,
+                                                 int64_t n, int64_t t1, int64_t t2, uint32_t lo, FilterMeta* m,
+                                                 unsigned long long* kept, int hpasses, int hbits,
+                                                 uint32_t* __restrict__ hist) {
+    __shared__ uint32_t shw[8][4][256];   // per-warp digit histograms
+    for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&shw[0][0][0])[i] = 0;
+    __syncthreads();
+    uint32_t (*sh)[256] = shw[threadIdx.x >> 5];
+    long long tmin = LLONG_MAX, tmax = LLONG_MIN;
+    unsigned cmin = 0xffffffffu, cmax = 0, cnt = 0;
+    const uint32_t hmask = (1u << hbits) - 1;
+    auto row = [&](uint32_t c, long long t) {
+        if (t < t1 || t > t2) return;
+        ++cnt;
+        tmin = min(tmin, t);
+        tmax = max(tmax, t);
+        cmin = min(cmin, c);
+        cmax = max(cmax, c);
+        const uint32_t f = c - lo;
+        for (int p = 0; p < hpasses; ++p) atomicAdd(&sh[p][(f >> (p * hbits)) & hmask], 1u);
+    };
+    const bool vec = (((uintptr_t)cs | (uintptr_t)ts) & 15) == 0;
+    const int64_t nq = vec ? n / 4 : 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 c4 = ((const uint4*)cs)[q];
+        const longlong2 t01 = ((const longlong2*)ts)[2 * q], t23 = ((const longlong2*)ts)[2 * q + 1];
+        row(c4.x, t01.x);
+        row(c4.y, t01.y);
+        row(c4.z, t23.x);
+        row(c4.w, t23.y);
+    }
+    for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        row(cs[i], ts[i]);
+    for (int o = 16; o; o >>= 1) {
+        tmin = min(tmin, __shfl_xor_sync(~0u, tmin, o));
+        tmax = max(tmax, __shfl_xor_sync(~0u, tmax, o));
+        cmin = min(cmin, __shfl_xor_sync(~0u, cmin, o));
+        cmax = max(cmax, __shfl_xor_sync(~0u, cmax, o));
+        cnt += __shfl_xor_sync(~0u, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicMin(&m->ts_min, tmin);
+        atomicMax(&m->ts_max, tmax);
+        atomicMin(&m->case_min, cmin);
+        atomicMax(&m->case_max, cmax);
+        atomicAdd(kept, (unsigned long long)cnt);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < hpasses * 256; i += blockDim.x) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += (&shw[w][0][0])[i];
+        if (v) atomicAdd(&hist[i], v);
+    }
+}
+
+// an ingested log's header (no columns, no state) for a derived log on stream s
+static pm4g_log* derived_header(const pm4g_log* in, cudaStream_t s) {
+    pm4g_log* L = new pm4g_log();
+    L->A = in->A;
+    L->act_bytes = in->act_bytes;
+    L->n_case_codes = in->n_case_codes;
+    L->case_lo = in->case_lo;
+    L->case_hi = in->case_hi;
+    L->stream = s;
+    return L;
+}
+
+// The lazily filtered log over `in`'s columns (in is unsorted, has no extra
+// columns; a lazy `in` is filtered on its own parent rows with the
+// intersected time range).
+static pm4g_status filter_time_lazy(const pm4g_log* in, int64_t t1, int64_t t2, cudaStream_t s, pm4g_log** out) {
+    pm4g_log* L = derived_header(in, s);
+    LogGuard guard(L);
+    PM4G_TRY(dalloc((void**)&L->d_n_cases, 8, s));
+    pm4g_log* P = const_cast<pm4g_log*>(in);   // the parent's observable state does not change
+    if (P->owns_cols) {                        // its columns become shared
+        P->hold = std::make_shared<ColHold>();
+        P->hold->case_ = P->case_;
+        P->hold->act = P->act;
+        P->hold->ts = P->ts;
+        P->owns_cols = false;
+    }
+    L->hold = P->hold;
+    L->case_ = P->case_;
+    L->act = P->act;
+    L->ts = P->ts;
+    L->tf_n = in->tf_n >= 0 ? in->tf_n : in->n;
+    L->tf_t1 = in->tf_n >= 0 ? std::max(t1, in->tf_t1) : t1;
+    L->tf_t2 = in->tf_n >= 0 ? std::min(t2, in->tf_t2) : t2;
+    int hpasses = 0, hbits = 0;
+    hist_layout(L, &hpasses, &hbits);
+    PM4G_TRY(dalloc_t(&L->hist, 4 * 256, s));
+    PM4G_CK(cudaMemsetAsync(L->hist, 0, 4 * 256 * 4, s));
+    struct Stage {
+        FilterMeta fm;
+        unsigned long long kept;
+    };
+    static thread_local Stage* hp = nullptr;   // pinned: one async init copy, one result copy
+    if (!hp) PM4G_CK(cudaHostAlloc((void**)&hp, sizeof(Stage), cudaHostAllocDefault));
+    hp->fm = FilterMeta{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u};
+    hp->kept = 0;
+    Scratch md(s);
+    PM4G_TRY(md.alloc(sizeof(Stage)));
+    Stage* dm = md.as<Stage>();
+    PM4G_CK(cudaMemcpyAsync(dm, hp, sizeof(Stage), cudaMemcpyHostToDevice, s));
+    const int64_t n = L->tf_n;
+    if (n > 0) {
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, (int64_t)num_sms() * 4));
+        PM4G_LAUNCH("k_tf_scan", n * 12.0, s,
+                    (k_tf_scan<<<g, 256, 0, s>>>(L->case_, L->ts, n, L->tf_t1, L->tf_t2, L->case_lo, &dm->fm,
+                                                 &dm->kept, hpasses, hbits, L->hist)));
+    }
+    PM4G_CK(cudaMemcpyAsync(hp, dm, sizeof(Stage), cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaStreamSynchronize(s));
+    L->n = (int64_t)hp->kept;
+    apply_meta(L, hp->fm.ts_min, hp->fm.ts_max, hp->fm.case_min, hp->fm.case_max, hpasses, hbits);
+    // only the narrow first pass of a non-empty log keeps rows on the fly
+    if (L->n == 0 || L->wide) PM4G_TRY(materialize(L, s));
+    *out = guard.release();
+    return PM4G_OK;
+}
+
+pm4g_status materialize(pm4g_log* L, cudaStream_t s) {
+    if (L->tf_n < 0) return PM4G_OK;
+    pm4g_log view;   // the parent rows the lazy log filters (columns borrowed)
+    view.n = L->tf_n;
+    view.A = L->A;
+    view.act_bytes = L->act_bytes;
+    view.n_case_codes = L->n_case_codes;
+    view.case_lo = L->case_lo;
+    view.case_hi = L->case_hi;
+    view.case_ = L->case_;
+    view.act = L->act;
+    view.ts = L->ts;
+    view.stream = s;
+    pm4g_log* M = nullptr;
+    const TimePred tp{L->tf_t1, L->tf_t2};
+    PM4G_TRY(compact_log(&view, nullptr, s, &M, &tp));
+    free_log_cols(L, s);   // drops the shared columns (and clears tf_n)
+    L->case_ = M->case_;
+    L->act = M->act;
+    L->ts = M->ts;
+    L->owns_cols = true;
+    M->case_ = nullptr;
+    M->act = nullptr;
+    M->ts = nullptr;
+    M->owns_cols = false;
+    std::swap(L->hist, M->hist);
+    L->n = M->n;
+    L->ts_min = M->ts_min;
+    L->ts_max = M->ts_max;
+    L->case_min = M->case_min;
+    L->case_max = M->case_max;
+    L->case_bits = M->case_bits;
+    L->ts_bits = M->ts_bits;
+    L->key_bits = M->key_bits;
+    L->wide = M->wide;
+    L->passes = M->passes;
+    L->hist_passes = M->hist_passes;
+    L->hist_bits = M->hist_bits;
+    pm4g_log_destroy(M);
+    return PM4G_OK;
+}
+
+static bool lazy_filter_off() {
+    const char* e = getenv("PM4G_NO_LAZY_FILTER");
+    return e && e[0] == '1';
+}
+
 }  // namespace pm4g
 
 using namespace pm4g;
@@ -673,6 +851,9 @@ pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t
     if (mode < 0 || mode > 2) return fail(PM4G_EINVAL, "bad time-filter mode");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = in->n;
+    if (mode == PM4G_TIME_EVENTS && !in->sorted && in->extra.empty() && !lazy_filter_off())
+        return filter_time_lazy(in, t1, t2, s, out);
+    PM4G_TRY(materialize(const_cast<pm4g_log*>(in), s));
     Scratch mask(s), span(s);
     RowView v = view_of(in);
     if (mode == PM4G_TIME_EVENTS && !in->sorted) {
@@ -840,6 +1021,7 @@ pm4g_status pm4g_filter_attr(const pm4g_log* in, int32_t column, const pm4g_pred
     PM4G_TRY(check_log(in));
     if (level != PM4G_LEVEL_EVENTS && level != PM4G_LEVEL_CASES) return fail(PM4G_EINVAL, "bad level");
     cudaStream_t s = (cudaStream_t)stream;
+    PM4G_TRY(materialize(const_cast<pm4g_log*>(in), s));
     AttrPred p{};
     p.kind = pred->kind;
     int col_kind;

@@ -7,6 +7,7 @@
 
 #include <functional>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/pm4g.h"
@@ -104,6 +105,14 @@ struct ExtraCol {
     bool owned = false;
 };
 
+// Ingested columns shared by a parent log and its lazily time-filtered child
+// (pm4g_filter_time, events mode): freed by whichever log releases them last.
+struct ColHold {
+    uint32_t* case_ = nullptr;
+    void* act = nullptr;
+    int64_t* ts = nullptr;
+};
+
 }  // namespace pm4g
 
 struct pm4g_log {
@@ -126,6 +135,12 @@ struct pm4g_log {
     void* act = nullptr;
     int64_t* ts = nullptr;
     bool owns_cols = false;
+    std::shared_ptr<pm4g::ColHold> hold;   // shared ownership of case_ / act / ts (then owns_cols = false)
+    // lazily time-filtered log (A1 fused into the sort's first pass): its rows
+    // are the tf_n rows of case_ / act / ts with tf_t1 <= ts <= tf_t2, in
+    // order; n, the metadata and the histograms describe the kept rows.  Only
+    // pm4g_sort reads it in this form; every other consumer materialises it.
+    int64_t tf_n = -1, tf_t1 = 0, tf_t2 = 0;
     // formatted state
     uint64_t* key = nullptr;    // [n] sorted composite keys
     void* s_act = nullptr;      // [n] sorted activities
@@ -161,6 +176,10 @@ namespace pm4g {
 // A log whose deferred format step failed (pm4g_sort_analyze) has neither its
 // ingested columns nor a correct formatted order: every call on it fails.
 pm4g_status check_log(const pm4g_log* L);
+// release a log's ingested columns (owned, shared or borrowed) on stream s
+void free_log_cols(pm4g_log* L, cudaStream_t s);
+// a lazily time-filtered log -> an ordinary ingested log (its kept rows compacted)
+pm4g_status materialize(pm4g_log* L, cudaStream_t s);
 
 // ------------------------------------------------------------------ helpers
 __host__ __device__ inline int bit_width_u64(uint64_t x) {

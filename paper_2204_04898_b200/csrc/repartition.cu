@@ -80,6 +80,7 @@ void log_columns(const pm4g_log* L, std::vector<const void*>* cols, std::vector<
 }
 
 pm4g_status partition_rows(const pm4g_log* in, const uint32_t* bounds, int R, cudaStream_t s, PartitionedRows* out) {
+    PM4G_TRY(materialize(const_cast<pm4g_log*>(in), s));   // a lazily filtered log: its kept rows
     PM4G_TRY(check_log(in));
     if (in->sorted) return fail(PM4G_EINVAL, "repartition needs an ingested (unsorted) log");
     if (R < 1 || R > 1024) return fail(PM4G_EINVAL, "1 <= R <= 1024 destinations");
@@ -216,6 +217,7 @@ pm4g_status pm4g_log_concat(const pm4g_log* const* logs, int32_t n_logs, uint32_
         const pm4g_log* L = logs[i];
         PM4G_TRY(check_log(L));
         if (L->sorted) return fail(PM4G_EINVAL, "concat needs ingested (unsorted) logs");
+        PM4G_TRY(materialize(const_cast<pm4g_log*>(L), s));
         if (L->A != logs[0]->A || L->act_bytes != logs[0]->act_bytes || L->extra.size() != logs[0]->extra.size())
             return fail(PM4G_EINVAL, "logs differ in activity dictionary or columns");
         for (size_t e = 0; e < L->extra.size(); ++e)

@@ -49,6 +49,11 @@ struct KeyParams {
     int ts_bits;
 };
 
+// A1 fused into the sort: pass 0 reads n_scan raw rows, keeps t1 <= ts <= t2
+struct TimeFilt {
+    int64_t n_scan, t1, t2;
+};
+
 __host__ __device__ inline uint64_t make_key(uint64_t case_rel, int64_t t, int64_t ts_min, int ts_bits) {
     return (ts_bits >= 64 ? 0 : (case_rel << ts_bits)) | ((uint64_t)t - (uint64_t)ts_min);
 }
@@ -59,13 +64,15 @@ __host__ __device__ inline uint64_t make_key(uint64_t case_rel, int64_t t, int64
 template <bool FROM_COLS>
 __global__ __launch_bounds__(256) void k_hist(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ cs,
                                               int64_t n, uint32_t case_min, int shift0, int bits,
-                                              int passes, uint32_t* __restrict__ hist) {
+                                              int passes, uint32_t* __restrict__ hist,
+                                              const int64_t* __restrict__ tf_ts = nullptr, int64_t t1 = 0, int64_t t2 = 0) {
     __shared__ uint32_t sh[MAX_PASSES][RADIX];
     for (int i = threadIdx.x; i < MAX_PASSES * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
     const uint32_t mask = (1u << bits) - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        if (FROM_COLS && tf_ts && (tf_ts[i] < t1 || tf_ts[i] > t2)) continue;   // dropped by a fused time filter
         const uint64_t f = FROM_COLS ? (uint64_t)(cs[i] - case_min) : shr64(keys[i], shift0);
         for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(f >> (p * bits)) & mask], 1u);
     }
@@ -114,6 +121,10 @@ struct PassArgs {
     // case_col[ingest row] - case_min (pass 0 reads the case column directly)
     const uint32_t* case_col;
     int wshift;
+    // pass 0 of a lazily time-filtered log (A1 fused into the key build): only
+    // raw rows with tf_t1 <= ts <= tf_t2 are ranked and written (tf != 0)
+    int tf = 0;
+    int64_t tf_t1 = 0, tf_t2 = 0;
 };
 
 // Shared-memory layout of one tile (all offsets multiples of 16):
@@ -170,14 +181,16 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
     // Peers (lanes holding the same digit) from one ballot per digit bit.
     // dp[j] = digit << 16 | rank of the key among its warp's keys of that digit.
     uint64_t k[SORT_IPT];
-    uint32_t dp[SORT_IPT];
+    uint32_t dp[SORT_IPT];   // 0xffffffff: a row dropped by the time filter (tf)
     const uint32_t lt = lanemask_lt();
+    const bool tf = FROM_COLS && a.tf;
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
         uint32_t d = dmask;
         k[j] = ~0ull;
-        if (li < nvalid) {
+        bool ok = li < nvalid;
+        if (ok) {
             if (FROM_COLS && WIDE) {   // wide pass 0: key = ts - ts_min, digit from the case column
                 k[j] = (uint64_t)u_ts[li] - (uint64_t)a.kp.ts_min;
                 d = (u_case[li] - a.kp.case_min) & dmask;
@@ -185,8 +198,10 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
                 k[j] = u_key[li];
                 d = ((a.case_col[u_idx[li]] - a.kp.case_min) >> a.wshift) & dmask;
             } else if (FROM_COLS) {   // pass 0: its digit is the low bits of case - case_min (shift == ts_bits)
+                const int64_t t = u_ts[li];
+                if (tf) ok = t >= a.tf_t1 && t <= a.tf_t2;
                 const uint32_t crel = u_case[li] - a.kp.case_min;
-                k[j] = make_key(crel, u_ts[li], a.kp.ts_min, a.kp.ts_bits);
+                k[j] = make_key(crel, t, a.kp.ts_min, a.kp.ts_bits);
                 d = crel & dmask;
             } else {
                 k[j] = u_key[li];
@@ -206,14 +221,15 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
                 : "r"(d), "r"(1u << b));
             peers &= ~(bal ^ m);
         }
-        const int leader = __ffs(peers) - 1;
+        if (tf) peers &= __ballot_sync(0xffffffffu, ok);   // dropped rows are nobody's peers
+        const int leader = (__ffs(peers) - 1) & 31;
         uint32_t bse = 0;
-        if (lane == leader) {
+        if (lane == leader && (!tf || ok)) {
             bse = s_whist[warp][d];
             s_whist[warp][d] = bse + __popc(peers);
         }
         bse = __shfl_sync(0xffffffffu, bse, leader);
-        dp[j] = (d << 16) | (bse + __popc(peers & lt));
+        dp[j] = (tf && !ok) ? 0xffffffffu : (d << 16) | (bse + __popc(peers & lt));
         __syncwarp();
     }
     __syncthreads();   // every key is in registers: u_key may be overwritten
@@ -235,13 +251,15 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         // invalid items (only in the last tile) carry the all-ones digit and
         // rank last; they are not part of the published counts
         pub = tot;
-        if (d == (int)dmask) pub -= (SORT_TILE - nvalid);
+        if (!tf && d == (int)dmask) pub -= (SORT_TILE - nvalid);
         if (dig) {
             if (tile == 0) st_volatile(st, ST_INC | pub);
             else st_volatile(st, ST_AGG | pub);
         }
     }
-    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, nullptr);
+    uint32_t ranked = 0;   // rows placed: nvalid, or the kept rows of a filtered pass 0
+    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, &ranked);
+    const uint32_t nout = tf ? ranked : nvalid;
     if (tid < RADIX) {
 #pragma unroll
         for (int w = 0; w < SORT_WARPS; ++w) s_whist[w][d] += start;
@@ -252,6 +270,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
+        if (tf && dp[j] == 0xffffffffu) continue;
         const uint32_t p = (dp[j] & 0xffffu) + s_whist[warp][dp[j] >> 16];
         u_key[p] = k[j];
         v_act[p] = u_act[li];
@@ -289,7 +308,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
 #pragma unroll 4
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t sidx = j * SORT_THREADS + tid;
-        if (sidx < nvalid) {
+        if (sidx < nout) {
             const uint64_t kk = u_key[sidx];
             const long long g = s_gbase[WIDE ? (uint32_t)v_dig[sidx] : digit(kk)] + sidx;
             a.out_key[g] = kk;
@@ -603,12 +622,16 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
                             const P* in_act, const uint32_t* in_idx, uint64_t* key_out, P* act_out,
                             uint32_t* idx_out, int64_t n, int shift0, int bits_total, KeyParams kp,
                             cudaStream_t s, const char* pass_name = "k_onesweep",
-                            const uint32_t* pre_hist = nullptr, const uint32_t* wide_case = nullptr) {
+                            const uint32_t* pre_hist = nullptr, const uint32_t* wide_case = nullptr,
+                            const TimeFilt* tfilt = nullptr) {
     const bool from_cols = in_case != nullptr;
     bits_total = std::max(1, bits_total);
     const int passes = std::max(1, std::min(MAX_PASSES, (bits_total + 7) / 8));
     const int bits = (bits_total + passes - 1) / passes;
-    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    // a time-filtered pass 0 scans tfilt->n_scan raw rows and writes the n kept ones
+    const int64_t n0 = tfilt ? tfilt->n_scan : n;
+    const int64_t tiles0 = (n0 + SORT_TILE - 1) / SORT_TILE;
+    const int64_t tiles = std::max<int64_t>((n + SORT_TILE - 1) / SORT_TILE, tiles0);   // look-back rows per pass
     Scratch aux(s), tmp(s);
     const size_t status_words = (size_t)tiles * RADIX * passes;
     PM4G_TRY(aux.alloc((status_words + passes + 2 * MAX_PASSES * RADIX) * 4));
@@ -624,8 +647,10 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
     } else {
         const int g = std::max(1, std::min<int>((int)((n + 255) / 256), num_sms() * 4));
         if (from_cols)
-            PM4G_LAUNCH("k_hist", n * 4.0, s,
-                        (k_hist<true><<<g, 256, 0, s>>>(nullptr, in_case, n, kp.case_min, 0, bits, passes, hist)));
+            PM4G_LAUNCH("k_hist", n0 * (tfilt ? 12.0 : 4.0), s,
+                        (k_hist<true><<<g, 256, 0, s>>>(nullptr, in_case, n0, kp.case_min, 0, bits, passes, hist,
+                                                        tfilt ? in_ts : nullptr, tfilt ? tfilt->t1 : 0,
+                                                        tfilt ? tfilt->t2 : 0)));
         else
             PM4G_LAUNCH("k_hist", n * 8.0, s,
                         (k_hist<false><<<g, 256, 0, s>>>(in_key, nullptr, n, 0, shift0, bits, passes, hist)));
@@ -649,14 +674,19 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
         const int shift = shift0 + p * bits;
         const double wr = 8.0 + sizeof(P) + (WI ? 4 : 0);
         if (p == 0 && from_cols) {
-            PassArgs<P, true, WI> a{nullptr, in_case, in_ts, ca, ci, ok, oa, oi, n, shift, bits, kp,
+            PassArgs<P, true, WI> a{nullptr, in_case, in_ts, ca, ci, ok, oa, oi, n0, shift, bits, kp,
                                     off, status, counters,
                                     aligned16(in_case) && aligned16(in_ts) && aligned16(ca) &&
                                         (!ci || aligned16(ci)),
                                     p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
             a.case_col = wide_case;
             a.wshift = 0;
-            PM4G_TRY(launch_pass(a, tiles, s, pass_name, n * (12.0 + sizeof(P) + (ci ? 4 : 0) + wr)));
+            if (tfilt) {
+                a.tf = 1;
+                a.tf_t1 = tfilt->t1;
+                a.tf_t2 = tfilt->t2;
+            }
+            PM4G_TRY(launch_pass(a, tiles0, s, pass_name, n0 * (12.0 + sizeof(P) + (ci ? 4 : 0)) + n * wr));
         } else {
             PassArgs<P, false, WI> a{ck, nullptr, nullptr, ca, ci, ok, oa, oi, n, shift, bits, kp,
                                      off + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p,
@@ -664,7 +694,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
                                      p + 1 < passes ? status + (size_t)(p + 1) * tiles * RADIX : nullptr};
             a.case_col = wide_case;
             a.wshift = p * bits;
-            PM4G_TRY(launch_pass(a, tiles, s, pass_name,
+            PM4G_TRY(launch_pass(a, (n + SORT_TILE - 1) / SORT_TILE, s, pass_name,
                                  n * ((ci ? wr : wr - (WI ? 4 : 0)) + wr + (wide_case ? 4.0 : 0.0))));
         }
         ck = ok;
@@ -1158,6 +1188,7 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     const bool wide = L->wide;
     const bool extras = !L->extra.empty();
     const bool wi = extras || wide;
+    if (wi && L->tf_n >= 0) PM4G_TRY(materialize(L, s));   // (the lazy filter never leaves these)
     KeyParams kp{L->case_min, L->ts_min, L->ts_bits};
     // 1. stable LSD passes over the case bits of the composite key (built on the fly)
     Scratch grp(s);
@@ -1172,9 +1203,13 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
         PM4G_TRY((lsd_sort<P, true>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, gidx, n,
                                     wide ? 0 : L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre,
                                     wide ? L->case_ : nullptr)));
-    else
+    else {
+        // a lazily time-filtered log: pass 0 scans the shared raw rows and keeps the filter's
+        const TimeFilt tfv{L->tf_n, L->tf_t1, L->tf_t2};
         PM4G_TRY((lsd_sort<P, false>(L->case_, L->ts, nullptr, (const P*)L->act, nullptr, gkey, gact, nullptr,
-                                     n, L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre)));
+                                     n, L->ts_bits, L->case_bits, kp, s, "k_onesweep", pre, nullptr,
+                                     L->tf_n >= 0 ? &tfv : nullptr)));
+    }
     // 2. per-case timestamp order + case offsets
     FmtArgs<P> fa{};
     fa.gkey = gkey;

@@ -63,13 +63,16 @@ def test_time_filters_random(seed, sort_first):
         _check(out, _expect(case, act, ts, A, keep))
 
 
+@pytest.mark.parametrize("lazy", [True, False])
 @pytest.mark.parametrize("n", [2_500_003, 4_000_000])
-def test_events_filter_ring_wraps_element_by_element(n):
+def test_events_filter_ring_wraps_element_by_element(n, lazy, monkeypatch):
     """k_filter_cols streams each CTA's 2048-row tiles through a 3-stage TMA ring;
     with n >= 2.5M rows (> 3 x grid tiles) every CTA wraps its ring several times.
     The filtered log, formatted, equals O1 on exactly the kept rows element by
     element (sorted columns, ties broken by ingest order -- so a row dropped,
     duplicated or reordered by the compaction fails), plus every aggregate."""
+    if not lazy:   # the materialised compaction (k_filter_cols) instead of the sort's fused pass 0
+        monkeypatch.setenv("PM4G_NO_LAZY_FILTER", "1")
     rng = np.random.default_rng(n)
     case = rng.integers(0, n // 8, n)
     act = rng.integers(0, 40, n)
@@ -184,3 +187,72 @@ def test_contained_subset_of_intersecting():
         ca = set(a.case_durations()[0].cpu().tolist())
         cb = set(b.case_durations()[0].cpu().tolist())
         assert ca <= cb
+
+
+# ---------------------------------------------------------------- the lazy events-mode filter
+def _lazy_case(seed, n=300_000):
+    rng = np.random.default_rng(seed)
+    case = rng.integers(0, n // 7, n)
+    act = rng.integers(0, 12, n)
+    ts = rng.integers(-10**9, 10**9, n)
+    ts[::5] = ts[1]                                    # ties
+    return case, act, ts
+
+
+def test_lazy_filter_chain_and_materialise():
+    """pm4g_filter_time (events mode) on an ingested log is lazy: the kept rows
+    are selected by the sort's first radix pass over the shared raw columns.
+    Filtering it again intersects the ranges; an attribute filter, a case-level
+    time filter or a partition materialises it first -- every path equals the
+    oracle on exactly the kept rows."""
+    case, act, ts = _lazy_case(1)
+    A, nc = 12, int(case.max()) + 1
+    t1, t2, u1, u2 = -6 * 10**8, 7 * 10**8, -9 * 10**8, 3 * 10**8
+    k1 = oracle.filter_time(case, ts, t1, t2, 0)
+    k12 = k1 & oracle.filter_time(case, ts, u1, u2, 0)
+    # lazy -> lazy (intersected) -> sort
+    f = _log(case, act, ts, A, nc).filter_time(t1, t2, 0).filter_time(u1, u2, 0)
+    _check(f, _expect(case, act, ts, A, k12))
+    # lazy -> attribute filter at case level (materialises)
+    f = _log(case, act, ts, A, nc).filter_time(t1, t2, 0)
+    g = f.filter_attr(codes=[3, 5], level=pm4g.PM4G_LEVEL_CASES)
+    sub = lambda x: np.asarray(x)[k1]  # noqa: E731
+    kk = oracle.filter_attr(sub(case), sub(act), codes=[3, 5], level=1)
+    assert_parity((g.sort(), collect(g))[1], oracle.run(sub(case)[kk], sub(act)[kk], sub(ts)[kk], A))
+    # lazy -> case-level time filter (materialises)
+    h = f.filter_time(u1, u2, pm4g.PM4G_TIME_CASES_INTERSECTING)
+    kh = oracle.filter_time(sub(case), sub(ts), u1, u2, 2)
+    _check(h, oracle.run(sub(case)[kh], sub(act)[kh], sub(ts)[kh], A))
+    # the lazy log itself still sorts after all that
+    _check(f, _expect(case, act, ts, A, k1))
+
+
+def test_lazy_filter_outlives_parent_and_edge_ranges():
+    """The lazy child shares the parent's (copied, owned) columns: destroying
+    the parent first leaves them alive until the child is sorted.  An empty
+    range and a range keeping every row work too."""
+    case, act, ts = _lazy_case(2)
+    A, nc = 12, int(case.max()) + 1
+    for t1, t2 in ((-5 * 10**8, 5 * 10**8), (10**9 + 1, 10**9 + 5), (-10**9, 10**9)):
+        log = _log(case, act, ts, A, nc)
+        f = log.filter_time(t1, t2, 0)
+        log.close()
+        torch.cuda.synchronize()
+        _check(f, _expect(case, act, ts, A, oracle.filter_time(case, ts, t1, t2, 0)))
+
+
+def test_lazy_filter_then_partition_and_sort_analyze():
+    """A lazy log partitioned by case range (materialised) and a lazy log through
+    pm4g_sort_analyze: both equal the oracle on the kept rows."""
+    case, act, ts = _lazy_case(3)
+    A, nc = 12, int(case.max()) + 1
+    t1, t2 = -2 * 10**8, 9 * 10**8
+    keep = oracle.filter_time(case, ts, t1, t2, 0)
+    f = _log(case, act, ts, A, nc).filter_time(t1, t2, 0)
+    assert_parity(collect(f, sort_analyze=True), _expect(case, act, ts, A, keep))
+    f = _log(case, act, ts, A, nc).filter_time(t1, t2, 0)
+    bounds = [0, nc // 3, nc]
+    parts = f.partition_by_case(bounds)
+    for r, p in enumerate(parts):
+        m = keep & (case >= bounds[r]) & (case < bounds[r + 1])
+        _check(p, oracle.run(case[m], act[m], ts[m], A))
