@@ -49,11 +49,23 @@ enum { TAB_FULL = 1, TAB_HASH = 2 };
 
 // Stage geometry per table mode (measured): the dense table leaves room for a
 // second CTA per SM with 3 stages of 2048 rows (0.68 -> 0.53 ms at 100M); the
-// hash table keeps one CTA per SM and prefers 2 stages of 4096 rows.
+// hash table takes 4096 slots and 2 stages of 2048 rows, so two CTAs share an
+// SM too (1B/8 shard, A = 256, ~1,000 distinct edges: 8192 slots + 2 x 4096
+// rows, one CTA per SM, 0.97 ms -> 0.80 ms; 2048 slots 0.86, 1024 rows x 4
+// stages 1.12).  The PM4G_AGG_H* macros are the sweep's knobs.
+#ifndef PM4G_AGG_HROWS
+#define PM4G_AGG_HROWS 2048
+#endif
+#ifndef PM4G_AGG_HSTAGES
+#define PM4G_AGG_HSTAGES 2
+#endif
+#ifndef PM4G_AGG_HSLOTS
+#define PM4G_AGG_HSLOTS 4096
+#endif
 template <int MODE>
 struct AggGeom {
-    static constexpr uint32_t ROWS = MODE == TAB_FULL ? 2048 : 4096;   // rows of a staged case tile
-    static constexpr int STAGES = MODE == TAB_FULL ? 3 : 2;
+    static constexpr uint32_t ROWS = MODE == TAB_FULL ? 2048 : PM4G_AGG_HROWS;   // rows of a staged case tile
+    static constexpr int STAGES = MODE == TAB_FULL ? 3 : PM4G_AGG_HSTAGES;
 };
 
 // One pipeline stage: the tile's case offsets and its rows (keys, activities).
@@ -69,9 +81,9 @@ struct alignas(128) AggStage {
 constexpr int HASH_PROBES = 16;
 constexpr uint32_t HASH_EMPTY = 0xffffffffu;
 
-// shared-memory hash slots: as many as fit next to the two 4096-row stages
+// shared-memory hash slots: 4096 (two CTAs per SM next to two 2048-row stages)
 template <class P, bool MM>
-__host__ __device__ constexpr uint32_t hash_slots() { return (sizeof(P) == 1 && !MM) ? 8192u : 4096u; }
+__host__ __device__ constexpr uint32_t hash_slots() { return (sizeof(P) == 1 && !MM) ? (uint32_t)PM4G_AGG_HSLOTS : 4096u; }
 
 // start/end counters are privatised when A is small enough
 constexpr uint32_t SE_SMEM_MAX_A = 2048;
