@@ -499,8 +499,8 @@ pm4g_status pm4g_log_create(const pm4g_log_desc* d, pm4g_stream_t stream, pm4g_l
     *out = nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     if (d->n_events < 0) return fail(PM4G_EINVAL, "n_events < 0");
-    if (d->n_events > (int64_t)ST_VAL)
-        return fail(PM4G_EINVAL, "n_events exceeds 2^30-1 per shard; shard the log across ranks");
+    if (d->n_events > MAX_SHARD_EVENTS)
+        return fail(PM4G_EINVAL, "n_events exceeds 2^31-2 per shard; shard the log across ranks");
     if (d->act_bytes != 1 && d->act_bytes != 2 && d->act_bytes != 4)
         return fail(PM4G_EINVAL, "act_bytes must be 1, 2 or 4");
     if (d->n_activities == 0) return fail(PM4G_EINVAL, "n_activities must be >= 1");

@@ -295,7 +295,7 @@ pm4g_status pm4g_repartition(const pm4g_log* in, const uint32_t* bounds, pm4g_co
         roff[p] = n_recv;
         n_recv += M[(size_t)p * R + me];
     }
-    if (n_recv > (uint64_t)ST_VAL) return fail(PM4G_EINVAL, "a destination shard exceeds 2^30-1 events");
+    if (n_recv > (uint64_t)MAX_SHARD_EVENTS) return fail(PM4G_EINVAL, "a destination shard exceeds 2^31-2 events");
     auto fill = [&](const std::vector<void*>& dst) -> pm4g_status {
         if (R == 1) {
             for (size_t k = 0; k < dst.size(); ++k)

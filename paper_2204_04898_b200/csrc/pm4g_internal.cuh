@@ -249,10 +249,18 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
         : "memory");
 }
 
-// Decoupled look-back (single value per tile), status word = flag(2) | value(30).
-constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1;
+// Decoupled look-back status word (32 bits): 0 = not ready, 2 v + 2 = the
+// tile's own aggregate v, 2 v + 3 = its inclusive prefix v.  Values up to
+// 2^31 - 2 fit, which bounds the events of one log shard (MAX_SHARD_EVENTS).
+// (A 64-bit word costs a radix pass ~6%: twice the look-back traffic.)
+typedef uint32_t st_t;
+__host__ __device__ __forceinline__ st_t st_agg(uint32_t v) { return 2u * v + 2u; }
+__host__ __device__ __forceinline__ st_t st_inc(uint32_t v) { return 2u * v + 3u; }
+__host__ __device__ __forceinline__ bool st_is_inc(st_t w) { return (w & 1u) != 0; }
+__host__ __device__ __forceinline__ uint32_t st_val(st_t w) { return (w - 2u) >> 1; }
+constexpr int64_t MAX_SHARD_EVENTS = (1ll << 31) - 2;
 
-// Decoupled look-back (one value per tile, status word = flag(2) | value(30)),
+// Decoupled look-back (one value per tile),
 // warp-cooperative, reading K predecessors per lane (32 K per L2 round trip:
 // with T tiles in flight the newest tile's walk spans ~T predecessors, so the
 // window width bounds a single-pass kernel's steady state).  Called by all 32
@@ -260,38 +268,38 @@ constexpr uint32_t ST_AGG = 1u << 30, ST_INC = 2u << 30, ST_VAL = (1u << 30) - 1
 // inclusive prefix, publishes its own.  Lane l covers predecessors
 // end - (l K + j), j = 0..K-1, nearest first.  Returns the exclusive prefix.
 template <int K>
-__device__ __forceinline__ uint32_t lookback_warp_k(uint32_t* status, uint32_t tile, uint32_t aggregate) {
+__device__ __forceinline__ uint32_t lookback_warp_k(st_t* status, uint32_t tile, uint32_t aggregate) {
     const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        if (lane == 0) st_volatile(&status[0], ST_INC | aggregate);
+        if (lane == 0) st_volatile(&status[0], st_inc(aggregate));
         return 0;
     }
-    if (lane == 0) st_volatile(&status[tile], ST_AGG | aggregate);
+    if (lane == 0) st_volatile(&status[tile], st_agg(aggregate));
     uint32_t prefix = 0;
     int64_t end = (int64_t)tile - 1;
     while (true) {
-        uint32_t v[K];
+        st_t v[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const int64_t idx = end - (lane * K + j);
-            v[j] = idx >= 0 ? ld_volatile(&status[idx]) : ST_INC;
+            v[j] = idx >= 0 ? ld_volatile(&status[idx]) : st_inc(0);
         }
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const int64_t idx = end - (lane * K + j);
-            while ((v[j] >> 30) == 0) v[j] = ld_volatile(&status[idx]);
+            while (v[j] == 0) v[j] = ld_volatile(&status[idx]);
         }
         int fj = K;   // this lane's nearest inclusive entry
 #pragma unroll
         for (int j = K - 1; j >= 0; --j)
-            if ((v[j] >> 30) == 2) fj = j;
+            if (st_is_inc(v[j])) fj = j;
         const uint32_t inc = __ballot_sync(0xffffffffu, fj < K);
         const int stop = inc ? __ffs(inc) - 1 : 31;
         uint32_t x = 0;
         if (lane <= stop) {
 #pragma unroll
             for (int j = 0; j < K; ++j)
-                if (lane < stop || j <= fj) x += v[j] & ST_VAL;
+                if (lane < stop || j <= fj) x += st_val(v[j]);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -299,7 +307,7 @@ __device__ __forceinline__ uint32_t lookback_warp_k(uint32_t* status, uint32_t t
         if (inc) break;
         end -= 32 * K;
     }
-    if (lane == 0) st_volatile(&status[tile], ST_INC | (prefix + aggregate));
+    if (lane == 0) st_volatile(&status[tile], st_inc(prefix + aggregate));
     return prefix;
 }
 

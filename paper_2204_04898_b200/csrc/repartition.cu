@@ -225,7 +225,7 @@ pm4g_status pm4g_log_concat(const pm4g_log* const* logs, int32_t n_logs, uint32_
                 return fail(PM4G_EINVAL, "logs differ in extra columns");
         n += L->n;
     }
-    if (n > (int64_t)ST_VAL) return fail(PM4G_EINVAL, "n_events exceeds 2^30-1 per shard");
+    if (n > MAX_SHARD_EVENTS) return fail(PM4G_EINVAL, "n_events exceeds 2^31-2 per shard");
     auto fill = [&](const std::vector<void*>& dst) -> pm4g_status {
         uint64_t at = 0;
         std::vector<const void*> cols;

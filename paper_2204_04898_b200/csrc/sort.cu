@@ -112,10 +112,10 @@ struct PassArgs {
     int shift, bits;
     KeyParams kp;
     const uint32_t* bucket_off;  // [256]
-    uint32_t* status;            // [tiles * 256]
+    st_t* status;                // [tiles * 256]
     uint32_t* tile_counter;
     bool aligned;                // every input array 16-byte aligned (TMA bulk path)
-    uint32_t* next_status;       // the next pass's look-back words (zeroed here, row per tile), or nullptr
+    st_t* next_status;           // the next pass's look-back words (zeroed here, row per tile), or nullptr
     // wide logs (case_bits + ts_bits > 64): the key is ts - ts_min only, the
     // payload row is the ingest row, and a pass's digit is digit `wshift` of
     // case_col[ingest row] - case_min (pass 0 reads the case column directly)
@@ -154,7 +154,7 @@ struct NoHook {
 // tile's rows are in u_key (FROM_COLS: u_case, u_ts) and u_act; s_whist must
 // be zero on entry.  after_rank() runs (every thread) once the tile's inputs
 // other than u_act / u_key are no longer read (after the ranking barrier).
-template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, class Hook = NoHook, bool WIDE = false>
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, bool TF, class Hook = NoHook, bool WIDE = false>
 __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& a, const uint32_t tile,
                                         const uint32_t nvalid, uint64_t* u_key, const int64_t* u_ts,
                                         const uint32_t* u_case, const uint32_t* u_idx, const P* u_act,
@@ -183,7 +183,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
     uint64_t k[SORT_IPT];
     uint32_t dp[SORT_IPT];   // 0xffffffff: a row dropped by the time filter (tf)
     const uint32_t lt = lanemask_lt();
-    const bool tf = FROM_COLS && a.tf;
+    constexpr bool tf = FROM_COLS && TF;   // a time-filtered pass 0 (a separate instantiation)
 #pragma unroll
     for (int j = 0; j < SORT_IPT; ++j) {
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
@@ -222,7 +222,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
             peers &= ~(bal ^ m);
         }
         if (tf) peers &= __ballot_sync(0xffffffffu, ok);   // dropped rows are nobody's peers
-        const int leader = (__ffs(peers) - 1) & 31;
+        const int leader = tf ? ((__ffs(peers) - 1) & 31) : __ffs(peers) - 1;   // (a dropped lane may have no peers)
         uint32_t bse = 0;
         if (lane == leader && (!tf || ok)) {
             bse = s_whist[warp][d];
@@ -239,7 +239,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
     const int d = tid;
     const bool dig = tid < RADIX && d <= (int)dmask;
     uint32_t tot = 0;
-    uint32_t* st = a.status + (size_t)tile * RADIX + d;
+    st_t* st = a.status + (size_t)tile * RADIX + d;
     uint32_t pub = 0;
     if (tid < RADIX) {
 #pragma unroll
@@ -253,12 +253,12 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         pub = tot;
         if (!tf && d == (int)dmask) pub -= (SORT_TILE - nvalid);
         if (dig) {
-            if (tile == 0) st_volatile(st, ST_INC | pub);
-            else st_volatile(st, ST_AGG | pub);
+            if (tile == 0) st_volatile(st, st_inc(pub));
+            else st_volatile(st, st_agg(pub));
         }
     }
     uint32_t ranked = 0;   // rows placed: nvalid, or the kept rows of a filtered pass 0
-    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, &ranked);
+    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, tf ? &ranked : nullptr);
     const uint32_t nout = tf ? ranked : nvalid;
     if (tid < RADIX) {
 #pragma unroll
@@ -285,20 +285,20 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
             int64_t p = (int64_t)tile - 1;
             bool done = false;
             while (!done) {
-                uint32_t w[4];
+                st_t w[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : ST_INC;
+                    w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : st_inc(0);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (done) break;
-                    while ((w[q] >> 30) == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
-                    prefix += w[q] & ST_VAL;
-                    if ((w[q] >> 30) == 2) done = true;
+                    while (w[q] == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
+                    prefix += st_val(w[q]);
+                    if (st_is_inc(w[q])) done = true;
                 }
                 p -= 4;
             }
-            st_volatile(st, ST_INC | (prefix + pub));
+            st_volatile(st, st_inc(prefix + pub));
         }
         s_gbase[d] = (long long)a.bucket_off[d] + prefix - start;
     }
@@ -320,7 +320,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
 
 // HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
 // the digits sit above ts_bits >= 32), extracted with one 32-bit shift
-template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, bool WIDE = false>
+template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, bool WIDE = false, bool TF = false>
 __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
     using Lay = OsLayout<P, FROM_COLS, WITH_IDX, WIDE>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -380,7 +380,7 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_C
         __syncthreads();
     }
 
-    os_tile<P, FROM_COLS, WITH_IDX, HI, NoHook, WIDE>(a, tile, nvalid, u_key, u_ts, u_case, u_idx, u_act, v_idx,
+    os_tile<P, FROM_COLS, WITH_IDX, HI, TF, NoHook, WIDE>(a, tile, nvalid, u_key, u_ts, u_case, u_idx, u_act, v_idx,
                                                       v_act, s_whist, s_gbase, s_scan, NoHook(),
                                                       (uint8_t*)(smem + Lay::o_vdig));
 }
@@ -459,7 +459,7 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf(PassArgs<P, fal
             }
             __syncthreads();
         }
-        os_tile<P, false, false, HI>(a, tile, nvalid, u_key, nullptr, nullptr, nullptr, u_act, nullptr, v_act,
+        os_tile<P, false, false, HI, false>(a, tile, nvalid, u_key, nullptr, nullptr, nullptr, u_act, nullptr, v_act,
                                      s_whist, s_gbase, s_scan);
     }
 }
@@ -479,7 +479,7 @@ struct Os0Layout {
     static constexpr size_t bytes = (o_vact + T * sizeof(P) + 15) / 16 * 16;
 };
 
-template <class P, bool HI>
+template <class P, bool HI, bool TF>
 __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf0(PassArgs<P, true, false> a, uint32_t n_tiles) {
     using Lay = Os0Layout<P>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -551,21 +551,21 @@ __global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf0(PassArgs<P, tr
         auto hook = [&]() {
             if (tid == 0 && bulk(next)) issue_case(next);
         };
-        os_tile<P, true, false, HI>(a, tile, nvalid, u_key, u_ts, u_case, nullptr, u_act, nullptr, v_act,
+        os_tile<P, true, false, HI, TF>(a, tile, nvalid, u_key, u_ts, u_case, nullptr, u_act, nullptr, v_act,
                                     s_whist, s_gbase, s_scan, hook);
     }
 }
 
-template <class P, bool HI>
+template <class P, bool HI, bool TF>
 static pm4g_status launch_pf0(const PassArgs<P, true, false>& args, int64_t tiles, cudaStream_t s,
                               const char* name, double bytes) {
     const size_t smem = Os0Layout<P>::bytes;
-    PM4G_MAX_SMEM(k_onesweep_pf0<P, HI>);
+    PM4G_MAX_SMEM((k_onesweep_pf0<P, HI, TF>));
     static int per_sm = -1;
     if (per_sm < 0)
-        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pf0<P, HI>, SORT_THREADS, smem));
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pf0<P, HI, TF>, SORT_THREADS, smem));
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * num_sms());
-    PM4G_LAUNCH(name, bytes, s, (k_onesweep_pf0<P, HI><<<grid, SORT_THREADS, smem, s>>>(args, (uint32_t)tiles)));
+    PM4G_LAUNCH(name, bytes, s, (k_onesweep_pf0<P, HI, TF><<<grid, SORT_THREADS, smem, s>>>(args, (uint32_t)tiles)));
     return PM4G_OK;
 }
 
@@ -573,7 +573,18 @@ template <class P, bool FC, bool WI, bool HI>
 static pm4g_status launch_pass_t(const PassArgs<P, FC, WI>& args, int64_t tiles, cudaStream_t s,
                                  const char* name, double bytes) {
     if constexpr (FC && !WI && sizeof(P) == 1) {    // pass 0: persistent, prefetching form (2 CTAs/SM)
-        if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF")) return launch_pf0<P, HI>(args, tiles, s, name, bytes);
+        if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF"))
+            return args.tf ? launch_pf0<P, HI, true>(args, tiles, s, name, bytes)
+                           : launch_pf0<P, HI, false>(args, tiles, s, name, bytes);
+    }
+    if constexpr (FC && !WI) {   // a time-filtered pass 0, one tile per CTA
+        if (args.tf) {
+            const size_t smem = OsLayout<P, FC, WI>::bytes;
+            PM4G_MAX_SMEM((k_onesweep<P, FC, WI, HI, false, true>));
+            PM4G_LAUNCH(name, bytes, s,
+                        (k_onesweep<P, FC, WI, HI, false, true><<<(unsigned)tiles, SORT_THREADS, smem, s>>>(args)));
+            return PM4G_OK;
+        }
     }
     if constexpr (!FC && !WI && sizeof(P) <= 2) {   // persistent, prefetching form (2 CTAs per SM)
         if (tiles > 2 * num_sms() && !getenv("PM4G_NO_OS_PF")) {
@@ -634,13 +645,13 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
     const int64_t tiles = std::max<int64_t>((n + SORT_TILE - 1) / SORT_TILE, tiles0);   // look-back rows per pass
     Scratch aux(s), tmp(s);
     const size_t status_words = (size_t)tiles * RADIX * passes;
-    PM4G_TRY(aux.alloc((status_words + passes + 2 * MAX_PASSES * RADIX) * 4));
-    uint32_t* status = aux.as<uint32_t>();
-    uint32_t* counters = status + status_words;
+    PM4G_TRY(aux.alloc(status_words * sizeof(st_t) + (passes + 2 * MAX_PASSES * RADIX) * 4));
+    st_t* status = aux.as<st_t>();
+    uint32_t* counters = (uint32_t*)(status + status_words);
     uint32_t* hist = counters + passes;
     uint32_t* off = hist + MAX_PASSES * RADIX;
     // pass 0's look-back words, the tile counters and histograms; pass p zeroes pass p+1's words
-    PM4G_CK(cudaMemsetAsync(status, 0, (size_t)tiles * RADIX * 4, s));
+    PM4G_CK(cudaMemsetAsync(status, 0, (size_t)tiles * RADIX * sizeof(st_t), s));
     PM4G_CK(cudaMemsetAsync(counters, 0, (passes + MAX_PASSES * RADIX) * 4, s));
     if (pre_hist) {   // histograms already built (by the validation pass)
         PM4G_LAUNCH("k_hist_scan", 0, s, k_hist_scan<<<1, RADIX, 0, s>>>(pre_hist, off, passes));
@@ -729,7 +740,7 @@ struct FmtArgs {
     uint32_t* off;
     uint32_t* case_code;
     uint64_t* n_cases;
-    uint32_t* status;
+    st_t* status;
     uint32_t* counter;
     uint32_t* big;             // ranks of fallback cases
     uint32_t* big_count;
@@ -1098,13 +1109,14 @@ template <class P>
 static pm4g_status format_launch(FmtArgs<P>& fa, Scratch& st, cudaStream_t s) {
     const int64_t n = fa.n;
     const int64_t tiles = (n + FMT_TILE - 1) / FMT_TILE;
-    const size_t words = 2 + (size_t)tiles + ((size_t)n / FMT_WARP_MAX + tiles + 2);
-    PM4G_TRY(st.alloc(words * 4));
-    PM4G_CK(cudaMemsetAsync(st.p, 0, (2 + tiles) * 4, s));
-    fa.counter = st.as<uint32_t>();
+    // [status st_t: tiles] [counter, big_count] [big list]
+    const size_t words = 2 + ((size_t)n / FMT_WARP_MAX + tiles + 2);
+    PM4G_TRY(st.alloc((size_t)tiles * sizeof(st_t) + words * 4));
+    PM4G_CK(cudaMemsetAsync(st.p, 0, (size_t)tiles * sizeof(st_t) + 8, s));
+    fa.status = st.as<st_t>();
+    fa.counter = (uint32_t*)(fa.status + tiles);
     fa.big_count = fa.counter + 1;
-    fa.status = fa.counter + 2;
-    fa.big = fa.status + tiles;
+    fa.big = fa.counter + 2;
     const bool wide = fa.rcase_out != nullptr;
     const bool wi = fa.gidx != nullptr;
     fa.aligned = aligned16(fa.gkey) && aligned16(fa.gact) && (!wi || aligned16(fa.gidx));
@@ -1271,7 +1283,7 @@ __global__ __launch_bounds__(SEG_THREADS) void k_segments(const uint64_t* __rest
                                                           uint32_t* __restrict__ off,
                                                           uint32_t* __restrict__ case_code,
                                                           uint64_t* __restrict__ n_cases,
-                                                          uint32_t* status, uint32_t* counter) {
+                                                          st_t* status, uint32_t* counter) {
     __shared__ uint32_t s_tile, s_warp_tot[SEG_THREADS / 32], s_scan[SEG_THREADS / 32 + 1];
     __shared__ uint32_t s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1355,13 +1367,13 @@ pm4g_status segments(pm4g_log* L, cudaStream_t s) {
     }
     const int64_t tiles = (n + SEG_TILE - 1) / SEG_TILE;
     Scratch st(s);
-    PM4G_TRY(st.alloc((tiles + 1) * 4));
-    PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * 4, s));
-    uint32_t* status = st.as<uint32_t>();
+    PM4G_TRY(st.alloc((tiles + 1) * sizeof(st_t)));
+    PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * sizeof(st_t), s));
+    st_t* status = st.as<st_t>();
     PM4G_LAUNCH("k_segments", n * 8.0, s,
                 k_segments<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(L->key, L->rcase, n, L->ts_bits, L->case_min,
                                                                   L->off, L->s_case_code,
-                                                                  L->d_n_cases, status + 1, status));
+                                                                  L->d_n_cases, status + 1, (uint32_t*)status));
     return PM4G_OK;
 }
 

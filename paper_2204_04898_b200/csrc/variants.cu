@@ -634,7 +634,7 @@ constexpr int SCAN_THREADS = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_THREADS * SCAN_
 
 __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __restrict__ in,
                                                             uint64_t* __restrict__ out, int64_t n,
-                                                            uint32_t* status, uint32_t* counter) {
+                                                            st_t* status, uint32_t* counter) {
     __shared__ uint32_t s_tile, s_scan[SCAN_THREADS / 32 + 1], s_prefix;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
     __syncthreads();
@@ -662,7 +662,7 @@ __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __re
     if (threadIdx.x == 0 && (int64_t)(tile + 1) * SCAN_TILE >= n) out[n] = (uint64_t)s_prefix + total;
 }
 
-// out[0..n] = exclusive prefix sums of in[0..n), out[n] = total (< 2^30)
+// out[0..n] = exclusive prefix sums of in[0..n), out[n] = total (< 2^31)
 pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
     if (n == 0) {
         PM4G_CK(cudaMemsetAsync(out, 0, 8, s));
@@ -670,10 +670,10 @@ pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, c
     }
     const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     Scratch st(s);
-    PM4G_TRY(st.alloc((tiles + 1) * 4));
-    PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * 4, s));
+    PM4G_TRY(st.alloc((tiles + 1) * sizeof(st_t)));
+    PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * sizeof(st_t), s));
     PM4G_LAUNCH("k_excl_scan", n * 12.0, s,
-                (k_excl_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, st.as<uint32_t>() + 1,
+                (k_excl_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, st.as<st_t>() + 1,
                                                                      st.as<uint32_t>())));
     return PM4G_OK;
 }

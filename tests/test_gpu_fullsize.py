@@ -77,7 +77,13 @@ def _sample_check(L, log, o, spec, k=1500, seed=0):
     C = log.info().n_cases
     rng = np.random.default_rng(seed)
     pick = np.sort(rng.choice(spec.n_cases, size=min(k, spec.n_cases), replace=False))
-    sel = torch.isin(L.case, torch.as_tensor(pick, device=L.case.device))
+
+    def member(codes):   # rows whose case is in `codes` (a lookup table: torch.isin sorts n values)
+        m = torch.zeros(spec.n_cases, dtype=torch.bool, device=L.case.device)
+        m[torch.as_tensor(codes, device=L.case.device)] = True
+        return m[L.case.to(torch.int64)]
+
+    sel = member(pick)
     c, a, t = L.case[sel].cpu().numpy(), L.act[sel].cpu().numpy(), L.ts[sel].cpu().numpy()
     r = oracle.run(c, a, t, A)
     # GPU per-case outputs are in case-code order; the workload's codes are dense
@@ -86,16 +92,17 @@ def _sample_check(L, log, o, spec, k=1500, seed=0):
     assert np.array_equal(o["n_events"][:C].cpu().numpy()[pick], r.n_events)
     assert np.array_equal(o["dur"][:C].cpu().numpy()[pick], r.dur)
     # formatted rows of the sampled cases
-    sc, sa, st = (x.to(torch.int64) for x in log.sorted_columns())
+    sc, sa, st = log.sorted_columns()
     offs = torch.cumsum(o["n_events"][:C].to(torch.int64), 0) - o["n_events"][:C].to(torch.int64)
     rows = torch.cat([torch.arange(int(offs[p]), int(offs[p]) + int(o["n_events"][p]), device=sc.device)
                       for p in pick[:200]])
-    sub = oracle.run(L.case[torch.isin(L.case, torch.as_tensor(pick[:200], device=L.case.device))].cpu().numpy(),
-                     L.act[torch.isin(L.case, torch.as_tensor(pick[:200], device=L.case.device))].cpu().numpy(),
-                     L.ts[torch.isin(L.case, torch.as_tensor(pick[:200], device=L.case.device))].cpu().numpy(), A)
-    assert np.array_equal(sa[rows].cpu().numpy(), sub.sorted_act)
+    s200 = member(pick[:200])
+    sub = oracle.run(L.case[s200].cpu().numpy(), L.act[s200].cpu().numpy(), L.ts[s200].cpu().numpy(), A)
+    # (u32 columns viewed as i32 to gather: codes < 2^31)
+    assert np.array_equal(sa.view(torch.int32)[rows].to(torch.int64).cpu().numpy(), sub.sorted_act)
     assert np.array_equal(st[rows].cpu().numpy(), sub.sorted_ts)
-    assert np.array_equal(sc[rows].cpu().numpy(), sub.sorted_case)
+    assert np.array_equal(sc.view(torch.int32)[rows].to(torch.int64).cpu().numpy(), sub.sorted_case)
+    del sc, sa, st
     # variant of each sampled case = its exact sequence (the oracle's per-case sequence)
     vt = o["variants"].get()
     ci = o["variants"].case_index(C).cpu().numpy()
@@ -164,3 +171,27 @@ def test_1b_single_gpu_with_time_filter():
     r = oracle.run(L.case[sel].cpu().numpy(), L.act[sel].cpu().numpy(), L.ts[sel].cpu().numpy(), spec.n_activities)
     assert np.array_equal(o["n_events"][:C].cpu().numpy()[pick_idx], r.n_events)
     assert np.array_equal(o["dur"][:C].cpu().numpy()[pick_idx], r.dur)
+
+
+def test_shard_above_2_30_events():
+    """A single shard past the former 2^30 - 1 limit (1.2e9 events, 60M cases, 256
+    activities): the look-back status words carry 31-bit counts, so every radix
+    pass, the format's case ranks and the scans stay exact.  Invariants at full
+    size and 1,000 sampled cases vs O1 (logs replicated to scale)."""
+    import types
+    if torch.cuda.get_device_properties(0).total_memory < 120e9:
+        pytest.skip("needs a 180 GB B200")
+    spec = CONFIGS["1B"].with_(n_cases=60_000_000, n_events=1_200_000_000)
+    assert spec.n_events > (1 << 30)
+    G = generate(spec, device="cuda")
+    # keep only compact columns (the generator's int64 temporaries would crowd out the sort)
+    case = G.case.to(torch.uint32)
+    L = types.SimpleNamespace(case=case.view(torch.int32), act=G.act.to(torch.uint8), ts=G.ts, n=G.n)
+    del G
+    torch.cuda.empty_cache()
+    log = pm4g.pm4g_log_create(case, L.act, L.ts, spec.n_activities, n_case_codes=spec.n_cases, borrow=True)
+    log.sort()
+    o = log.analyze()
+    assert log.n == spec.n_events
+    _invariants(L, log, o, spec)
+    _sample_check(L, log, o, spec, k=1000, seed=3)
