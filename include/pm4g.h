@@ -390,6 +390,14 @@ const char* pm4g_last_error(void);
 const char* pm4g_version(void);
 /* Number of kernels this library has launched (process-wide counter). */
 uint64_t pm4g_launch_count(void);
+/* Device memory held by the library (process-wide): blocks / bytes owned by
+ * live handles and scratch, and bytes of freed blocks kept in its reuse cache.
+ * After every handle is destroyed, live_blocks == 0 (the leak check of
+ * tests/test_gpu_sanitizer.py).  Any pointer may be NULL. */
+pm4g_status pm4g_mem_stats(uint64_t* live_blocks, uint64_t* live_bytes, uint64_t* cached_bytes);
+/* Return every cached (freed) block to the CUDA memory pool; synchronises the
+ * device first.  Live blocks are untouched. */
+pm4g_status pm4g_mem_release(void);
 /* Per-kernel timing with CUDA events recorded around every launch on the
  * launching stream (enable -> run -> collect).  collect synchronises. */
 pm4g_status pm4g_prof_enable(int32_t on);

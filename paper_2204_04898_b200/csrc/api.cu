@@ -435,6 +435,26 @@ const char* pm4g_last_error(void) { return g_err.c_str(); }
 const char* pm4g_version(void) { return "pm4g 0.1 (sm_100a)"; }
 uint64_t pm4g_launch_count(void) { return g_launches.load(); }
 
+pm4g_status pm4g_mem_stats(uint64_t* live_blocks, uint64_t* live_bytes, uint64_t* cached_bytes) {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    uint64_t b = 0;
+    for (auto& x : g_live_blocks) b += x.second;
+    if (live_blocks) *live_blocks = g_live_blocks.size();
+    if (live_bytes) *live_bytes = b;
+    if (cached_bytes) *cached_bytes = g_cached_bytes;
+    return PM4G_OK;
+}
+
+pm4g_status pm4g_mem_release(void) {
+    PM4G_CK(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    for (auto& fb : g_free_blocks) cudaFreeAsync(fb.second.p, fb.second.s);
+    g_free_blocks.clear();
+    g_cached_bytes = 0;
+    PM4G_CK(cudaDeviceSynchronize());
+    return PM4G_OK;
+}
+
 pm4g_status pm4g_prof_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof_on = on != 0;

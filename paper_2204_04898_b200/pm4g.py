@@ -109,6 +109,8 @@ _SIGS = {
     "pm4g_last_error": ([], ctypes.c_char_p),
     "pm4g_version": ([], ctypes.c_char_p),
     "pm4g_launch_count": ([], U64),
+    "pm4g_mem_stats": ([ctypes.POINTER(U64), ctypes.POINTER(U64), ctypes.POINTER(U64)], I32),
+    "pm4g_mem_release": ([], I32),
     "pm4g_prof_enable": ([I32], I32),
     "pm4g_prof_reset": ([], I32),
     "pm4g_prof_collect": ([ctypes.POINTER(I32)], I32),
@@ -529,6 +531,17 @@ def _comm(c):
 # ================================================================ diagnostics
 def pm4g_launch_count() -> int:
     return int(lib().pm4g_launch_count())
+
+
+def pm4g_mem_stats() -> dict:
+    """Device memory the library holds: live blocks / bytes and cached bytes."""
+    b, n, c = U64(0), U64(0), U64(0)
+    _check(lib().pm4g_mem_stats(ctypes.byref(b), ctypes.byref(n), ctypes.byref(c)))
+    return {"live_blocks": int(b.value), "live_bytes": int(n.value), "cached_bytes": int(c.value)}
+
+
+def pm4g_mem_release():
+    _check(lib().pm4g_mem_release())
 
 
 def pm4g_prof_enable(on: bool = True):
