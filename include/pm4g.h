@@ -271,7 +271,15 @@ enum { PM4G_TIME_EVENTS = 0, PM4G_TIME_CASES_CONTAINED = 1, PM4G_TIME_CASES_INTE
  * EVENTS: keep rows with t1 <= ts <= t2 (cases may become partial; adjacency
  * is re-derived by the next format, R13).  CASES_CONTAINED: keep every row of
  * cases with first ts >= t1 and last ts <= t2.  CASES_INTERSECTING: keep every
- * row of cases with first ts <= t2 and last ts >= t1.  EINVAL if t1 > t2. */
+ * row of cases with first ts <= t2 and last ts >= t1.  EINVAL if t1 > t2.
+ * EVENTS on an ingested (unsorted) log without extra columns is LAZY (SURVEY.md
+ * 8(a) A1 "fused with A2 when unsorted"): one scan of the case / ts columns
+ * counts the kept rows and builds their metadata; the new log shares `in`'s
+ * columns (kept alive past pm4g_log_destroy(in); borrowed columns must stay
+ * valid until the new log is sorted) and pm4g_sort's first radix pass keeps
+ * the rows in range while it builds the composite key.  Any other consumer of
+ * the new log (filters, partition, concat, repartition) first compacts it.
+ * Every filter synchronises `stream` once (the kept-row count). */
 pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t mode,
                              pm4g_stream_t stream, pm4g_log** out);
 
