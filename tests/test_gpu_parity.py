@@ -244,7 +244,7 @@ def test_variant_table_regrowth(monkeypatch, cap):
 
 
 @pytest.mark.parametrize("A", [92, 200, 256])
-def test_cnt16_table_flush_exact(A):
+def test_hash_table_flush_exact(A):
     """A > 91 takes k_aggregate's TAB_HASH mode (a per-CTA shared-memory hash table
     of u32 counts and u32 lo / hi duration sums, flushed once per CTA with 64-bit
     atomics).  One case repeats a self-loop ~200k times (one oversized tile, read
