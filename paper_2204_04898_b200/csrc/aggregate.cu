@@ -62,10 +62,16 @@ enum { TAB_FULL = 1, TAB_HASH = 2 };
 #ifndef PM4G_AGG_HSLOTS
 #define PM4G_AGG_HSLOTS 4096
 #endif
+#ifndef PM4G_AGG_FROWS
+#define PM4G_AGG_FROWS 2048
+#endif
+#ifndef PM4G_AGG_FSTAGES
+#define PM4G_AGG_FSTAGES 3
+#endif
 template <int MODE>
 struct AggGeom {
-    static constexpr uint32_t ROWS = MODE == TAB_FULL ? 2048 : PM4G_AGG_HROWS;   // rows of a staged case tile
-    static constexpr int STAGES = MODE == TAB_FULL ? 3 : PM4G_AGG_HSTAGES;
+    static constexpr uint32_t ROWS = MODE == TAB_FULL ? PM4G_AGG_FROWS : PM4G_AGG_HROWS;   // rows of a staged case tile
+    static constexpr int STAGES = MODE == TAB_FULL ? PM4G_AGG_FSTAGES : PM4G_AGG_HSTAGES;
 };
 
 // One pipeline stage: the tile's case offsets and its rows (keys, activities).
