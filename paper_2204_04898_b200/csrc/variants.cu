@@ -449,6 +449,7 @@ __global__ __launch_bounds__(256) void k_rank_sort(const uint64_t* __restrict__ 
 
 struct Groups {
     uint64_t G = 0;
+    uint64_t Ga = 0;                // group ids (>= G: the one-pass grouping's unused reserved ids)
     uint64_t total_len = 0;         // sum of the groups' sequence lengths
     uint64_t* weight = nullptr;     // [G]
     uint32_t* rep_item = nullptr;   // [G]
@@ -751,8 +752,10 @@ void free_variants(pm4g_variant_table* v) {
 //     reruns the general round-based engine (group_items) from scratch.
 // Result: item_group[c] = dense gid, per-group count / min case / total length,
 // i.e. the Groups of group_items without a compaction or item pass.
-constexpr int VG_THREADS = 256, VG_IPT = 4, VG_TASK = 32 * VG_IPT;   // a warp's task: 128 consecutive cases
-constexpr int VG_CACHE = 2048, VG_FILL = VG_CACHE / 2, VG_PROBES = 8, VG_GBLOCK = 8;
+// a warp's task: 32 * IPT consecutive cases (IPT = 4; IPT = 1 for small logs, so their few
+// tasks spread over more warps and CTAs instead of one CTA's latency chain)
+constexpr int VG_THREADS = 256;
+constexpr int VG_CACHE = 2048, VG_FILL = VG_CACHE / 2, VG_PROBES = 8;
 constexpr size_t VG_SMEM = (size_t)VG_CACHE * (8 + 8 + 4 + 4 + 4 + 4 + 4);
 constexpr unsigned long long VG_NOMETA = ~0ull;
 
@@ -815,7 +818,7 @@ __device__ __forceinline__ bool seq_same(const ACT* acts, uint32_t f, uint32_t r
 }
 
 // ctl: [0] overflow, [1] gids reserved (the warps' blocks), [2] collisions, [3] groups claimed
-template <class ACT>
+template <class ACT, int VG_IPT, int VG_GBLOCK>
 __global__ __launch_bounds__(VG_THREADS) void k_vgroup(
     uint64_t n_items, const uint64_t* __restrict__ d_n, const uint64_t* __restrict__ k1,
     const uint64_t* __restrict__ k2, const uint32_t* __restrict__ off, const ACT* __restrict__ acts,
@@ -847,6 +850,9 @@ __global__ __launch_bounds__(VG_THREADS) void k_vgroup(
     const int lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
     auto chash = [](uint64_t a) { return (uint32_t)(a ^ (a >> 29)) & (VG_CACHE - 1); };
+    constexpr int VG_TASK = 32 * VG_IPT;
+    // VG_GBLOCK: gids reserved per warp at a time (one by one for logs whose table
+    // may take the single-CTA emission: no empty gids)
     uint32_t claims = 0, gnext = 0, gend = 0;   // gend - gnext: the warp's unused reserved gids
     unsigned long long lensum = 0;
     for (;;) {
@@ -1026,9 +1032,183 @@ __global__ void k_vfinal(const uint32_t* __restrict__ g_w, const uint32_t* __res
         weight[g] = w;
         rep_item[g] = r;
         order[g] = r;
+        if (!key) continue;   // small tables: ordered by k_small_variants
         // an empty (reserved, unused) gid sorts after every group
         key[g] = w ? ((wmax - min(w, wmax)) << order_bits) | r : low_mask(wbits + order_bits);
         val[g] = (uint32_t)g;
+    }
+}
+
+// ------------------------------------------------------------------ small variant tables, one launch
+// Up to SV_MAX groups (e.g. the RoadTraffic shape's 231 variants, PAPER.md
+// Table 1; one SM's instruction throughput makes the spread-out path below
+// faster beyond ~2k groups): ONE CTA orders the groups by (count desc, rep asc) with a
+// shared-memory LSD radix sort of a compacted key ((maxw - w) << rbits | rep),
+// then emits count / len / rep_case / keys, scans the lengths and copies the
+// representatives' sequences -- instead of ~11 launches (sort keys, histogram,
+// scan, radix passes, inverse, emit, scan, gather), each a few microseconds of
+// latency at these sizes.
+constexpr int SV_THREADS = 1024, SV_WARPS = SV_THREADS / 32, SV_MAX = 2048, SV_IPT = SV_MAX / SV_THREADS;
+constexpr size_t SV_SMEM = (size_t)SV_MAX * 8 + 2 * (size_t)SV_MAX * 2 + (size_t)SV_WARPS * 256 * 4;
+
+template <class ACT>
+__global__ __launch_bounds__(SV_THREADS) void k_small_variants(
+    const uint64_t* __restrict__ weight, const uint32_t* __restrict__ rep, uint32_t Ga, uint32_t G,
+    const uint32_t* __restrict__ off, const ACT* __restrict__ acts, const uint32_t* __restrict__ rep_code,
+    const uint64_t* __restrict__ k1, const uint64_t* __restrict__ k2, uint64_t* __restrict__ count,
+    uint32_t* __restrict__ len, uint32_t* __restrict__ rep_case, uint64_t* __restrict__ seq_off,
+    uint32_t* __restrict__ seq_act, uint64_t* __restrict__ ok1, uint64_t* __restrict__ ok2,
+    uint32_t* __restrict__ inv) {
+    extern __shared__ __align__(16) unsigned char sv_sm[];
+    uint64_t* s_key = (uint64_t*)sv_sm;                        // [SV_MAX] in gid order
+    uint16_t* s_idx = (uint16_t*)(s_key + SV_MAX);             // [2][SV_MAX] gid at each position
+    uint32_t(*s_whist)[256] = (uint32_t(*)[256])(s_idx + 2 * SV_MAX);   // [SV_WARPS][256]
+    __shared__ uint32_t s_scan[SV_WARPS + 1];
+    __shared__ unsigned long long s_maxw;
+    __shared__ uint32_t s_maxr;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_maxw = 0;
+        s_maxr = 0;
+    }
+    __syncthreads();
+    unsigned long long mw = 0;
+    uint32_t mr = 0;
+    for (uint32_t g = tid; g < Ga; g += SV_THREADS)
+        if (weight[g]) {
+            mw = max(mw, (unsigned long long)weight[g]);
+            mr = max(mr, rep[g]);
+        }
+    for (int o = 16; o; o >>= 1) {
+        mw = max(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+        mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    }
+    if (lane == 0) {
+        atomicMax(&s_maxw, mw);
+        atomicMax(&s_maxr, mr);
+    }
+    __syncthreads();
+    const int rbits = max(1, bit_width_u64(s_maxr)), bits = rbits + max(1, bit_width_u64(s_maxw));
+    for (uint32_t g = tid; g < Ga; g += SV_THREADS) {
+        const uint64_t w = weight[g];
+        // an empty (reserved, unused) gid sorts after every group
+        s_key[g] = w ? ((s_maxw - w) << rbits) | rep[g] : low_mask(bits);
+        s_idx[g] = (uint16_t)g;
+    }
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    int cur = 0;
+    for (int shift = 0; shift < bits; shift += 8) {
+        for (int i = tid; i < SV_WARPS * 256; i += SV_THREADS) (&s_whist[0][0])[i] = 0;
+        __syncthreads();
+        const uint16_t* src = s_idx + cur * SV_MAX;
+        uint16_t* dst = s_idx + (cur ^ 1) * SV_MAX;
+        uint32_t dp[SV_IPT];
+        uint16_t gv[SV_IPT];
+#pragma unroll
+        for (int j = 0; j < SV_IPT; ++j) {   // striped: (warp, j, lane) is position order (stable)
+            const uint32_t pos = warp * (32 * SV_IPT) + j * 32 + lane;
+            uint32_t d = 255;
+            gv[j] = 0;
+            if (pos < Ga) {
+                gv[j] = src[pos];
+                d = (uint32_t)(s_key[gv[j]] >> shift) & 255u;
+            }
+            uint32_t peers = 0xffffffffu;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bal : ~bal;
+            }
+            const int leader = __ffs(peers) - 1;
+            uint32_t bse = 0;
+            if (lane == leader) {
+                bse = s_whist[warp][d];
+                s_whist[warp][d] = bse + __popc(peers);
+            }
+            bse = __shfl_sync(0xffffffffu, bse, leader);
+            dp[j] = (d << 16) | (bse + __popc(peers & lt));
+            __syncwarp();
+        }
+        __syncthreads();
+        // digit-major, warp-minor exclusive offsets (digit d = thread d of the first 256)
+        uint32_t tot = 0;
+        if (tid < 256)
+            for (int w = 0; w < SV_WARPS; ++w) {
+                const uint32_t c = s_whist[w][tid];
+                s_whist[w][tid] = tot;
+                tot += c;
+            }
+        const uint32_t start = block_excl_scan<SV_THREADS>(tid < 256 ? tot : 0u, s_scan, nullptr);
+        if (tid < 256)
+            for (int w = 0; w < SV_WARPS; ++w) s_whist[w][tid] += start;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < SV_IPT; ++j) {
+            const uint32_t pos = warp * (32 * SV_IPT) + j * 32 + lane;
+            if (pos < Ga) dst[(dp[j] & 0xffffu) + s_whist[warp][dp[j] >> 16]] = gv[j];
+        }
+        __syncthreads();
+        cur ^= 1;
+    }
+    // emit position p (< G: the real groups come first) and scan the lengths.  The
+    // keys' shared memory now holds s_it (the representative item, then its first
+    // row) and s_len (lengths, then their exclusive prefix).
+    const uint16_t* ord = s_idx + cur * SV_MAX;
+    uint32_t* s_it = (uint32_t*)s_key;
+    uint32_t* s_len = s_it + SV_MAX;
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t p = tid; p < Ga; p += SV_THREADS) {
+        const uint32_t g = ord[p];
+        inv[g] = p;
+        s_it[p] = rep[g];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t p = tid; p < SV_MAX; p += SV_THREADS) {
+        uint32_t L = 0;
+        if (p < G) {
+            const uint32_t it = s_it[p], f = off[it];
+            L = off[it + 1] - f;
+            count[p] = weight[ord[p]];
+            len[p] = L;
+            rep_case[p] = rep_code[it];
+            ok1[p] = k1[it];
+            ok2[p] = k2[it];
+            s_it[p] = f;
+        }
+        s_len[p] = L;
+    }
+    __syncthreads();
+    // exclusive scan of s_len[0..SV_MAX): SV_IPT consecutive entries per thread
+    uint32_t loc[SV_IPT], sum = 0;
+#pragma unroll
+    for (int j = 0; j < SV_IPT; ++j) {
+        loc[j] = s_len[tid * SV_IPT + j];
+        sum += loc[j];
+    }
+    uint32_t total = 0;
+    uint32_t ex = block_excl_scan<SV_THREADS>(sum, s_scan, &total);
+#pragma unroll
+    for (int j = 0; j < SV_IPT; ++j) {
+        const uint32_t p = tid * SV_IPT + j;
+        if (p < G) seq_off[p] = ex;
+        s_len[p] = ex;   // in place: each thread rewrites only its own entries
+        ex += loc[j];
+    }
+    if (tid == 0) seq_off[G] = total;
+    __syncthreads();
+    // the representatives' sequences, flattened: element i belongs to the last
+    // variant p with s_len[p] <= i (binary search over the G prefix sums)
+#pragma unroll 4
+    for (uint32_t i = tid; i < total; i += SV_THREADS) {
+        uint32_t lo = 0, hi = G;
+        while (hi - lo > 1) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (s_len[m] <= i) lo = m; else hi = m;
+        }
+        seq_act[i] = (uint32_t)acts[s_it[lo] + (i - s_len[lo])];
     }
 }
 
@@ -1058,14 +1238,19 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     if (const uint64_t dc = debug_variant_cap()) cap = std::min<uint64_t>(full, pow2_at_least(std::max<uint64_t>(dc, 64)));
     uint64_t G = 0, Ga = 0, htot = 0, gcap = 0;
     Scratch gw(s);
-    PM4G_MAX_SMEM(k_vgroup<ACT>);
+    const bool small = n_items < (uint64_t)num_sms() * 8 * 128;   // fewer 128-case tasks than warps
+    const bool fine = small;   // gids one by one (no empty ones: the table may take k_small_variants)
+    const int ipt = small ? 1 : 4;
+    auto kern = small ? k_vgroup<ACT, 1, 1> : k_vgroup<ACT, 4, 8>;
+    PM4G_MAX_SMEM((k_vgroup<ACT, 1, 1>));
+    PM4G_MAX_SMEM((k_vgroup<ACT, 4, 8>));
     static int per_sm = -1;
     if (per_sm < 0)
-        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgroup<ACT>, VG_THREADS, VG_SMEM));
-    const uint64_t tasks = (n_items + VG_TASK - 1) / VG_TASK;
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgroup<ACT, 4, 8>, VG_THREADS, VG_SMEM));
+    const uint64_t tasks = (n_items + 32 * ipt - 1) / (32 * ipt);
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((tasks + VG_THREADS / 32 - 1) / (VG_THREADS / 32),
                                                                     (uint64_t)std::max(per_sm, 1) * num_sms()));
-    const uint64_t slack = (uint64_t)grid * (VG_THREADS / 32) * 2 * VG_GBLOCK;   // unused reserved gids
+    const uint64_t slack = (uint64_t)grid * (VG_THREADS / 32) * 2 * (fine ? 1 : 8);   // unused reserved gids
     for (int attempt = 0;; ++attempt) {
         // groups never exceed the items; the table's claims stop near 3/4 load
         // (reserved gids past gcap abandon the table)
@@ -1082,7 +1267,7 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         PM4G_LAUNCH("k_variant_init", cap * 32.0 + gcap * 8.0, s,
                     (k_vinit<<<gsz(std::max(cap, gcap)), 256, 0, s>>>(tab.as<VSlot>(), cap, g_w, g_rep, gcap)));
         PM4G_LAUNCH("k_variant_group", n_items * 36.0, s,
-                    (k_vgroup<ACT><<<grid, VG_THREADS, VG_SMEM, s>>>(n_items, d_n, k1, k2, off, acts, tab.as<VSlot>(),
+                    (kern<<<grid, VG_THREADS, VG_SMEM, s>>>(n_items, d_n, k1, k2, off, acts, tab.as<VSlot>(),
                                                                      cap - 1, (uint32_t)gcap, g_w, g_rep,
                                                                      g.item_group, ctl, d_tot, d_task)));
         // one host round trip: overflow, gids, collisions, groups, total length (+ the case count)
@@ -1115,18 +1300,27 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         break;
     }
     g.G = G;
+    g.Ga = Ga;
     g.total_len = htot;
     const uint64_t Ga1 = std::max<uint64_t>(Ga, 1);
     if ((st = dalloc_t(&g.weight, Ga1, s))) return bail(st);
     if ((st = dalloc_t(&g.rep_item, Ga1, s))) return bail(st);
     if ((st = dalloc_t(&g.order, Ga1, s))) return bail(st);
-    if ((st = dalloc_t(&g.sorted, Ga1, s))) return bail(st);
     if ((st = dalloc_t(&g.inv, Ga1, s))) return bail(st);
     const int wbits = std::max(1, bit_width_u64(n_items));
+    const uint32_t* g_w = gw.as<uint32_t>();
+    if (Ga <= (uint64_t)SV_MAX) {   // small table: k_small_variants orders and emits it in one launch
+        if (Ga)
+            PM4G_LAUNCH("k_variant_sortkeys", Ga * 20.0, s,
+                        (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight,
+                                                          g.rep_item, g.order, nullptr, nullptr)));
+        *out = g;
+        return PM4G_OK;
+    }
+    if ((st = dalloc_t(&g.sorted, Ga1, s))) return bail(st);
     Scratch sk(s);   // keys [Ga] u64 | group ids [Ga] u32 (the radix payload)
     if ((st = sk.alloc(Ga * 12 + 16))) return bail(st);
     uint32_t* sk_val = (uint32_t*)(sk.as<uint64_t>() + Ga);
-    const uint32_t* g_w = gw.as<uint32_t>();
     if (Ga) {
         PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
                     (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight, g.rep_item,
@@ -1139,6 +1333,28 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         PM4G_LAUNCH("k_variant_inv", Ga * 8.0, s, (k_inv<<<gsz(Ga), 256, 0, s>>>(g.sorted, Ga, g.inv)));
     }
     *out = g;
+    return PM4G_OK;
+}
+
+// the per-case variant index (output position of each item's group), then the
+// groups' scratch is released and the table handed out
+static pm4g_status case_variant_index(const Groups& g, pm4g_variant_table* v, uint64_t n_items, cudaStream_t s) {
+    PM4G_TRY(dalloc_t(&v->case_variant, std::max<uint64_t>(n_items, 1), s));
+    if (n_items)
+        PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
+                    (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items, v->case_variant)));
+    return PM4G_OK;
+}
+
+static pm4g_status finish_variants(Groups& g, pm4g_variant_table* v, uint64_t n_items, bool with_case_variant,
+                                   cudaStream_t s, pm4g_variant_table** out) {
+    const pm4g_status st = with_case_variant ? case_variant_index(g, v, n_items, s) : PM4G_OK;
+    g.free(s);
+    if (st) {
+        free_variants(v);
+        return st;
+    }
+    *out = v;
     return PM4G_OK;
 }
 
@@ -1184,30 +1400,31 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
     if ((st = dalloc_t(&v->seq_off, V1 + 1, s))) return bail(st);
     if ((st = dalloc_t(&v->k1, V1, s))) return bail(st);
     if ((st = dalloc_t(&v->k2, V1, s))) return bail(st);
+    const uint64_t total = g.total_len;   // summed with the grouping, read with its counters
+    v->total_len = total;
+    if ((st = dalloc_t(&v->seq_act, std::max<uint64_t>(total, 1), s))) return bail(st);
+    if constexpr (sizeof(OFF) == 4) {
+        if (!g.sorted) {   // a small one-pass table: ordered and emitted by one CTA
+            PM4G_MAX_SMEM(k_small_variants<ACT>);
+            PM4G_LAUNCH("k_variant_small", g.Ga * 24.0 + g.G * 40.0 + total * 5.0, s,
+                        (k_small_variants<ACT><<<1, SV_THREADS, SV_SMEM, s>>>(
+                            g.weight, g.rep_item, (uint32_t)g.Ga, (uint32_t)g.G, (const uint32_t*)off, acts, rep_code,
+                            k1, k2, v->count, v->len, v->rep_case, v->seq_off, v->seq_act, v->k1, v->k2, g.inv)));
+            return finish_variants(g, v, n_items, with_case_variant, s, out);
+        }
+    }
     if (g.G) {
         PM4G_LAUNCH("k_variant_emit", g.G * 40.0, s,
                     (k_emit<OFF><<<gsz(g.G), 256, 0, s>>>(g, off, rep_code, k1, k2, v->count, v->len,
                                                           v->rep_case, v->k1, v->k2)));
     }
     if ((st = excl_scan_u32_to_u64(v->len, v->seq_off, (int64_t)g.G, s))) return bail(st);
-    const uint64_t total = g.total_len;   // summed by k_compact, read with the round counters
-    v->total_len = total;
-    if ((st = dalloc_t(&v->seq_act, std::max<uint64_t>(total, 1), s))) return bail(st);
     if (g.G) {
         int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>((g.G * 32 + 255) / 256, (uint64_t)num_sms() * 8));
         PM4G_LAUNCH("k_variant_seq", (double)total * 8.0, s,
                     (k_seq_gather<OFF, ACT><<<gs, 256, 0, s>>>(g, off, acts, v->seq_off, v->seq_act)));
     }
-    if (with_case_variant) {
-        if ((st = dalloc_t(&v->case_variant, std::max<uint64_t>(n_items, 1), s))) return bail(st);
-        if (n_items)
-            PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
-                        (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items,
-                                                                    v->case_variant)));
-    }
-    g.free(s);
-    *out = v;
-    return PM4G_OK;
+    return finish_variants(g, v, n_items, with_case_variant, s, out);
 }
 
 pm4g_status variants_from_keys(const pm4g_log* L, const uint64_t* k1, const uint64_t* k2,
