@@ -755,7 +755,15 @@ void free_variants(pm4g_variant_table* v) {
 // a warp's task: 32 * IPT consecutive cases (IPT = 4; IPT = 1 for small logs, so their few
 // tasks spread over more warps and CTAs instead of one CTA's latency chain)
 constexpr int VG_THREADS = 256;
-constexpr int VG_CACHE = 2048, VG_FILL = VG_CACHE / 2, VG_PROBES = 8;
+// per-CTA key cache entries and minimum CTAs per SM (sweep at 100M: 1024 entries
+// with 4 CTAs per SM 0.50 ms; 2048 / 3 CTAs 0.57; 1024 / 5 0.53; 512 / 6 0.59)
+#ifndef PM4G_VG_CACHE
+#define PM4G_VG_CACHE 1024
+#endif
+#ifndef PM4G_VG_MINB
+#define PM4G_VG_MINB 4
+#endif
+constexpr int VG_CACHE = PM4G_VG_CACHE, VG_FILL = VG_CACHE / 2, VG_PROBES = 8;
 constexpr size_t VG_SMEM = (size_t)VG_CACHE * (8 + 8 + 4 + 4 + 4 + 4 + 4);
 constexpr unsigned long long VG_NOMETA = ~0ull;
 
@@ -819,7 +827,7 @@ __device__ __forceinline__ bool seq_same(const ACT* acts, uint32_t f, uint32_t r
 
 // ctl: [0] overflow, [1] gids reserved (the warps' blocks), [2] collisions, [3] groups claimed
 template <class ACT, int VG_IPT, int VG_GBLOCK>
-__global__ __launch_bounds__(VG_THREADS) void k_vgroup(
+__global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
     uint64_t n_items, const uint64_t* __restrict__ d_n, const uint64_t* __restrict__ k1,
     const uint64_t* __restrict__ k2, const uint32_t* __restrict__ off, const ACT* __restrict__ acts,
     VSlot* table, uint64_t mask, uint32_t gcap, uint32_t* __restrict__ g_w, uint32_t* __restrict__ g_rep,
