@@ -22,6 +22,7 @@
 // weight = count, order = representative case code) for the multi-GPU path.
 // Output order: count desc, then representative case code asc (R11), via the
 // library's radix sort on ((~count) << 32 | order).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1220,6 +1221,242 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
     }
 }
 
+// ------------------------------------------------------------------ medium variant tables, one launch
+// Up to VO_MAX groups: ONE cooperative kernel (grid-wide barriers instead of
+// kernel boundaries) orders the groups by (count desc, rep asc) with an LSD
+// radix sort in the reduce-then-scan form -- every CTA owns a contiguous chunk
+// of <= 4096 groups; per pass it histograms its chunk, reads every chunk's
+// histogram to place its digits (no look-back chain), and scatters stably with
+// the ballot ranking -- then emits count / len / rep_case / keys, the sequence
+// offsets (chunk totals + in-chunk scan) and the representatives' sequences,
+// and finally every case's variant index.  Replaces ~14 launches (sort keys,
+// histogram, scan, 5-6 radix passes, inverse, emit, scan, gather, case index)
+// whose latency dominated at these sizes.
+constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = 8, VO_CHUNK = VO_THREADS * VO_IPT;
+constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs
+
+struct VoArgs {
+    const uint64_t* weight;
+    const uint32_t* rep;
+    uint32_t Ga, G, chunk;
+    const uint32_t* off;
+    const uint32_t* rep_code;
+    const uint64_t* k1;
+    const uint64_t* k2;
+    const uint32_t* item_group;
+    uint64_t n_items;
+    uint64_t* count;
+    uint32_t* len;
+    uint32_t* rep_case;
+    uint64_t* seq_off;
+    uint32_t* seq_act;
+    uint64_t* ok1;
+    uint64_t* ok2;
+    uint32_t* inv;
+    uint32_t* case_variant;    // nullptr: not requested
+    uint64_t* key[2];          // [Ga] each
+    uint32_t* val[2];          // [Ga] each
+    uint32_t* hist;            // [gridDim.x][256]
+    uint32_t* tot;             // [max(gridDim.x, 256)]: digit totals, then chunk length totals
+    unsigned long long* mx;    // [2]: max weight, max rep (zeroed)
+};
+
+template <class ACT>
+__global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __restrict__ acts) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t s_whist[VO_WARPS][256];
+    __shared__ uint32_t s_run[256], s_hist[256];
+    __shared__ uint32_t s_scan[VO_WARPS + 1];
+    extern __shared__ __align__(16) uint32_t vo_dyn[];   // [VO_CHUNK] first rows | [VO_CHUNK] prefixes
+    uint32_t* s_f = vo_dyn;
+    uint32_t* s_ex = vo_dyn + VO_CHUNK;
+    __shared__ unsigned long long s_pre;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t c = blockIdx.x, nc = gridDim.x;
+    const uint32_t lo = min(a.Ga, c * a.chunk), hi = min(a.Ga, lo + a.chunk), cn = hi - lo;
+    const uint32_t lt = lanemask_lt();
+    // 1. key bits from the largest weight and representative
+    {
+        unsigned long long mw = 0, mr = 0;
+        for (uint32_t g = lo + tid; g < hi; g += VO_THREADS)
+            if (a.weight[g]) {
+                mw = max(mw, (unsigned long long)a.weight[g]);
+                mr = max(mr, (unsigned long long)a.rep[g]);
+            }
+        for (int o = 16; o; o >>= 1) {
+            mw = max(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+            mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+        }
+        if (lane == 0) {
+            if (mw) atomicMax(&a.mx[0], mw);
+            if (mr) atomicMax(&a.mx[1], mr);
+        }
+    }
+    grid.sync();
+    const unsigned long long maxw = ld_volatile(&a.mx[0]), maxr = ld_volatile(&a.mx[1]);
+    const int rbits = max(1, bit_width_u64(maxr)), bits = rbits + max(1, bit_width_u64(maxw));
+    for (uint32_t g = lo + tid; g < hi; g += VO_THREADS) {
+        const uint64_t w = a.weight[g];
+        // an empty (reserved, unused) gid sorts after every group
+        a.key[0][g] = w ? ((maxw - w) << rbits) | a.rep[g] : low_mask(bits);
+        a.val[0][g] = g;
+    }
+    grid.sync();
+    // 2. LSD passes, 8 bits each
+    int cur = 0;
+    for (int shift = 0; shift < bits; shift += 8) {
+        const uint64_t* ik = a.key[cur];
+        const uint32_t* iv = a.val[cur];
+        uint64_t* okey = a.key[cur ^ 1];
+        uint32_t* oval = a.val[cur ^ 1];
+        uint64_t kk[VO_IPT];
+        uint32_t vv[VO_IPT], dp[VO_IPT];
+        for (int i = tid; i < VO_WARPS * 256; i += VO_THREADS) (&s_whist[0][0])[i] = 0;
+        __syncthreads();
+        // the chunk's items, striped (warp, j, lane) = position order; stable ranks per warp
+#pragma unroll
+        for (int j = 0; j < VO_IPT; ++j) {
+            const uint32_t li = warp * (32 * VO_IPT) + j * 32 + lane;
+            uint32_t d = 255;
+            kk[j] = ~0ull;
+            vv[j] = 0;
+            if (li < cn) {
+                kk[j] = ik[lo + li];
+                vv[j] = iv[lo + li];
+                d = (uint32_t)(kk[j] >> shift) & 255u;
+            }
+            uint32_t peers = 0xffffffffu;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bal : ~bal;
+            }
+            const int leader = __ffs(peers) - 1;
+            uint32_t bse = 0;
+            if (lane == leader) {
+                bse = s_whist[warp][d];
+                s_whist[warp][d] = bse + __popc(peers);
+            }
+            bse = __shfl_sync(0xffffffffu, bse, leader);
+            dp[j] = (d << 16) | (bse + __popc(peers & lt));
+            __syncwarp();
+        }
+        __syncthreads();
+        // the chunk's digit counts (padding ranks last under digit 255, not counted)
+        if (tid < 256) {
+            uint32_t t = 0;
+            for (int w = 0; w < VO_WARPS; ++w) {
+                const uint32_t x = s_whist[w][tid];
+                s_whist[w][tid] = t;   // warp-exclusive prefix inside the chunk
+                t += x;
+            }
+            if (tid == 255) t -= VO_CHUNK - cn;
+            a.hist[(size_t)c * 256 + tid] = t;
+        }
+        uint32_t tot = 0, pre = 0;
+        grid.sync();
+        // digit base: every chunk's counts of smaller digits, plus earlier chunks' of
+        // this digit.  Each CTA reads the whole [nc][256] matrix (rows coalesced;
+        // thread t sums digit t & 255 over half t >> 8 of the chunks), so no
+        // separate scan phase and barrier is needed.
+        {
+            const uint32_t d = tid & 255, half = tid >> 8;
+            const uint32_t q0 = half ? (nc + 1) / 2 : 0u, q1 = half ? nc : (nc + 1) / 2;
+            uint32_t t = 0, pr = 0;
+#pragma unroll 8
+            for (uint32_t q = q0; q < q1; ++q) {
+                const uint32_t h = a.hist[(size_t)q * 256 + d];
+                t += h;
+                pr += q < c ? h : 0u;
+            }
+            if (half) {
+                s_hist[d] = t;
+                s_run[d] = pr;
+            }
+            __syncthreads();
+            if (!half) {
+                t += s_hist[d];
+                pr += s_run[d];
+            }
+            __syncthreads();
+            tot = half ? 0u : t;
+            pre = half ? 0u : pr;
+        }
+        const uint32_t base = block_excl_scan<VO_THREADS>(tot, s_scan, nullptr);
+        if (tid < 256) s_run[tid] = base + pre;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < VO_IPT; ++j) {
+            const uint32_t li = warp * (32 * VO_IPT) + j * 32 + lane;
+            if (li >= cn) continue;
+            const uint32_t d = dp[j] >> 16;
+            const uint32_t pos = s_run[d] + s_whist[warp][d] + (dp[j] & 0xffffu);
+            okey[pos] = kk[j];
+            oval[pos] = vv[j];
+        }
+        grid.sync();
+        cur ^= 1;
+    }
+    // 3. emission of this chunk's output positions [lo, hi)
+    const uint32_t* ord = a.val[cur];
+    uint32_t myL[VO_IPT], sum = 0;
+#pragma unroll
+    for (int j = 0; j < VO_IPT; ++j) {   // thread tid owns positions lo + tid * VO_IPT + j (consecutive)
+        const uint32_t li = tid * VO_IPT + j, p = lo + li;
+        myL[j] = 0;
+        if (li >= cn) continue;
+        const uint32_t g = ord[p];
+        a.inv[g] = p;
+        if (p < a.G) {
+            const uint32_t it = a.rep[g], f = a.off[it];
+            myL[j] = a.off[it + 1] - f;
+            a.count[p] = a.weight[g];
+            a.len[p] = myL[j];
+            a.rep_case[p] = a.rep_code[it];
+            a.ok1[p] = a.k1[it];
+            a.ok2[p] = a.k2[it];
+            s_f[li] = f;
+        }
+        sum += myL[j];
+    }
+    uint32_t ctot = 0;
+    uint32_t ex = block_excl_scan<VO_THREADS>(sum, s_scan, &ctot);
+#pragma unroll
+    for (int j = 0; j < VO_IPT; ++j) {
+        s_ex[tid * VO_IPT + j] = ex;
+        ex += myL[j];
+    }
+    if (tid == 0) a.tot[c] = ctot;
+    grid.sync();
+    if (tid == 0) {
+        unsigned long long pr = 0;
+        for (uint32_t q = 0; q < c; ++q) pr += a.tot[q];
+        s_pre = pr;
+    }
+    __syncthreads();
+    const unsigned long long pre = s_pre;
+    const uint32_t creal = a.G > lo ? min(cn, a.G - lo) : 0u;   // real groups in this chunk
+    for (uint32_t li = tid; li < creal; li += VO_THREADS) a.seq_off[lo + li] = pre + s_ex[li];
+    if (creal && lo + creal == a.G && tid == 0) a.seq_off[a.G] = pre + ctot;
+    if (a.G == 0 && c == 0 && tid == 0) a.seq_off[0] = 0;
+    // the chunk's sequences, flattened (binary search over the in-chunk prefix)
+    for (uint32_t i = tid; i < ctot; i += VO_THREADS) {
+        uint32_t l = 0, h = creal;
+        while (h - l > 1) {
+            const uint32_t m = (l + h) >> 1;
+            if (s_ex[m] <= i) l = m; else h = m;
+        }
+        a.seq_act[pre + i] = (uint32_t)acts[s_f[l] + (i - s_ex[l])];
+    }
+    // 4. every case's variant index (inv complete after the barrier)
+    if (a.case_variant) {
+        grid.sync();
+        for (uint64_t q = (uint64_t)c * VO_THREADS + tid; q < a.n_items; q += (uint64_t)nc * VO_THREADS)
+            a.case_variant[q] = a.inv[a.item_group[q]];
+    }
+}
+
 // The one-pass grouping of a log's cases.  *fallback = true when the general
 // engine must run instead (a hash collision); otherwise *out holds the groups
 // in output order (sorted, inv) exactly as group_items leaves them.
@@ -1317,7 +1554,7 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     if ((st = dalloc_t(&g.inv, Ga1, s))) return bail(st);
     const int wbits = std::max(1, bit_width_u64(n_items));
     const uint32_t* g_w = gw.as<uint32_t>();
-    if (Ga <= (uint64_t)SV_MAX) {   // small table: k_small_variants orders and emits it in one launch
+    if (Ga <= VO_MAX_GROUPS) {   // ordered and emitted in one launch (k_small_variants / k_vorder)
         if (Ga)
             PM4G_LAUNCH("k_variant_sortkeys", Ga * 20.0, s,
                         (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight,
@@ -1341,6 +1578,67 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         PM4G_LAUNCH("k_variant_inv", Ga * 8.0, s, (k_inv<<<gsz(Ga), 256, 0, s>>>(g.sorted, Ga, g.inv)));
     }
     *out = g;
+    return PM4G_OK;
+}
+
+// k_vorder: the medium one-pass table ordered, emitted and indexed in one cooperative launch
+template <class ACT>
+static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t* off, const ACT* acts,
+                                const uint32_t* rep_code, const uint64_t* k1, const uint64_t* k2, uint64_t n_items,
+                                bool with_case_variant, cudaStream_t s) {
+    constexpr size_t dyn = 2 * VO_CHUNK * 4;
+    PM4G_MAX_SMEM(k_vorder<ACT>);
+    static int per_sm = -1;
+    if (per_sm < 0)
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vorder<ACT>, VO_THREADS, dyn));
+    const uint64_t Ga = g.Ga;
+    const uint64_t maxc = (uint64_t)std::max(per_sm, 1) * num_sms();
+    uint64_t nc = std::min<uint64_t>(maxc, std::max<uint64_t>((Ga + 255) / 256, 1));
+    nc = std::max<uint64_t>(nc, (Ga + VO_CHUNK - 1) / VO_CHUNK);
+    nc = std::min<uint64_t>(nc, 2 * VO_THREADS);
+    if (nc > maxc || nc * VO_CHUNK < Ga) return fail(PM4G_ECUDA, "variant table too large for the cooperative ordering");
+    Scratch sc(s);
+    const size_t kb = ((Ga * 8 + 15) & ~(size_t)15), vb = ((Ga * 4 + 15) & ~(size_t)15);
+    PM4G_TRY(sc.alloc(2 * kb + 2 * vb + nc * 256 * 4 + std::max<uint64_t>(nc, 256) * 4 + 64));
+    char* b = (char*)sc.p;
+    VoArgs a{};
+    a.weight = g.weight;
+    a.rep = g.rep_item;
+    a.Ga = (uint32_t)Ga;
+    a.G = (uint32_t)g.G;
+    a.chunk = (uint32_t)((Ga + nc - 1) / nc);
+    a.off = off;
+    a.rep_code = rep_code;
+    a.k1 = k1;
+    a.k2 = k2;
+    a.item_group = g.item_group;
+    a.n_items = n_items;
+    a.count = v->count;
+    a.len = v->len;
+    a.rep_case = v->rep_case;
+    a.seq_off = v->seq_off;
+    a.seq_act = v->seq_act;
+    a.ok1 = v->k1;
+    a.ok2 = v->k2;
+    a.inv = g.inv;
+    a.key[0] = (uint64_t*)b;
+    a.key[1] = (uint64_t*)(b + kb);
+    a.val[0] = (uint32_t*)(b + 2 * kb);
+    a.val[1] = (uint32_t*)(b + 2 * kb + vb);
+    a.hist = (uint32_t*)(b + 2 * kb + 2 * vb);
+    a.tot = a.hist + nc * 256;
+    a.mx = (unsigned long long*)(((uintptr_t)(a.tot + std::max<uint64_t>(nc, 256)) + 15) & ~(uintptr_t)15);
+    // the per-case index in the same launch for small logs; a wide grid gathers it faster otherwise
+    const bool cv_inside = with_case_variant && n_items <= (1ull << 20);
+    if (with_case_variant) PM4G_TRY(dalloc_t(&v->case_variant, std::max<uint64_t>(n_items, 1), s));
+    if (cv_inside) a.case_variant = v->case_variant;
+    PM4G_CK(cudaMemsetAsync(a.mx, 0, 16, s));
+    void* args[] = {(void*)&a, (void*)&acts};
+    PM4G_LAUNCH("k_variant_order", Ga * 60.0 + g.total_len * 5.0 + (with_case_variant ? n_items * 8.0 : 0.0), s,
+                (cudaLaunchCooperativeKernel((const void*)k_vorder<ACT>, dim3((unsigned)nc), dim3(VO_THREADS), args, dyn, s)));
+    if (with_case_variant && !cv_inside && n_items)
+        PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
+                    (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items, v->case_variant)));
     return PM4G_OK;
 }
 
@@ -1412,6 +1710,14 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
     v->total_len = total;
     if ((st = dalloc_t(&v->seq_act, std::max<uint64_t>(total, 1), s))) return bail(st);
     if constexpr (sizeof(OFF) == 4) {
+        if (!g.sorted && g.Ga > (uint64_t)SV_MAX) {   // a medium one-pass table: one cooperative launch
+            const pm4g_status vs = order_medium<ACT>(g, v, (const uint32_t*)off, acts, rep_code, k1, k2, n_items,
+                                                     with_case_variant, s);
+            if (vs) return bail(vs);
+            g.free(s);
+            *out = v;
+            return PM4G_OK;
+        }
         if (!g.sorted) {   // a small one-pass table: ordered and emitted by one CTA
             PM4G_MAX_SMEM(k_small_variants<ACT>);
             PM4G_LAUNCH("k_variant_small", g.Ga * 24.0 + g.G * 40.0 + total * 5.0, s,
