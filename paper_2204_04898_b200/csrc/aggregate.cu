@@ -178,7 +178,24 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     const uint64_t tiles = (C + cpt - 1) / cpt;
 
     if (warp == 0) {
-        // ---------------- producer warp: stream tiles into the ring with TMA
+        // ---------------- producer warp: stream tiles into the ring with TMA.
+        // The case offsets of the NEXT tile are loaded into registers right after
+        // this tile's rows are requested, so their latency hides behind the wait
+        // for a free stage instead of delaying the row transfer.
+        constexpr int OPL = (AGG_CASES + 1 + 31) / 32;   // offsets per lane
+        uint32_t ro[OPL];
+        auto load_off = [&](uint64_t t) {
+            const uint64_t c0 = t * cpt;
+            const uint32_t nc = t < tiles ? (uint32_t)min((uint64_t)cpt, C - c0) : 0u;
+#pragma unroll
+            for (int q = 0; q < OPL; ++q) {
+                const uint32_t j = lane + 32 * q;
+                ro[q] = (t < tiles && j <= nc) ? off[c0 + j] : 0u;
+            }
+        };
+#ifndef PM4G_AGG_NOPF
+        load_off(blockIdx.x);
+#endif
         uint32_t i = 0;
         for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
             const int s = i % AGG_STAGES;
@@ -186,7 +203,15 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
             Stage& st = stage[s];
             const uint64_t c0 = t * cpt;
             const uint32_t nc = (uint32_t)min((uint64_t)cpt, C - c0);
+#ifdef PM4G_AGG_NOPF
             for (uint32_t j = lane; j <= nc; j += 32) st.off[j] = off[c0 + j];
+#else
+#pragma unroll
+            for (int q = 0; q < OPL; ++q) {
+                const uint32_t j = lane + 32 * q;
+                if (j <= nc) st.off[j] = ro[q];
+            }
+#endif
             __syncwarp();
             if (lane == 0) {
                 const uint32_t e0 = st.off[0], e1 = st.off[nc];
@@ -208,6 +233,9 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
                 }
             }
             __syncwarp();
+#ifndef PM4G_AGG_NOPF
+            load_off(t + gridDim.x);
+#endif
         }
     } else {
         // ---------------- consumer warps
