@@ -5,7 +5,8 @@
 
 One step = one pass of the hot path over one batch (the config's log shard):
   A0 pm4g_log_create (validate + metadata, columns borrowed in HBM)
-  [A1 events-mode time filter, only with --filter]
+  [A1 events-mode time filter, only with --filter: pm4g_log_create_filtered
+   validates and filters in one pass; the sort's first radix pass drops the rows]
   A2-A4 pm4g_sort (composite key, onesweep LSD radix sort, case segments)
   A5-A9 pm4g_analyze (fused DFG + start/end + case durations + variant keys,
         then the variant group-count / verify / order)
@@ -130,20 +131,23 @@ def make_shard(cfg: str, rank: int, world: int, device, strong: bool = False):
     return case.contiguous(), act.contiguous(), ts, meta, spec
 
 
-def ingest(pm4g, case, act, ts, meta, host=False, stream=None):
-    """pm4g_log_create: columns (device, borrowed; or pinned host, copied H2D) -> validated log."""
+def ingest(pm4g, case, act, ts, meta, host=False, stream=None, filt=None):
+    """pm4g_log_create: columns (device, borrowed; or pinned host, copied H2D) -> validated log.
+    With filt = (t1, t2): pm4g_log_create_filtered -- the same validation pass also applies the
+    events-mode time filter (A1) to the log's metadata; the sort's first pass drops the rows."""
     return pm4g.pm4g_log_create(case, act, ts, meta["A"], n_case_codes=meta["n_case_codes"],
                                 case_lo=meta["case_lo"], case_hi=meta["case_hi"], borrow=not host,
-                                stream=stream)
+                                stream=stream, time_filter=filt)
 
 
 def run_step(pm4g, case, act, ts, meta, comm, out, filt=None, host=False, trace=None, info=None, log=None):
     tick = (lambda nm: trace.append((nm, time.perf_counter()))) if trace is not None else (lambda nm: None)
     tick("start")
+    fused = log is None and filt is not None   # validation + filter in one pass
     if log is None:
-        log = ingest(pm4g, case, act, ts, meta, host)
+        log = ingest(pm4g, case, act, ts, meta, host, filt=filt)
     tick("log_create")
-    if filt is not None:
+    if filt is not None and not fused:
         f = log.filter_time(filt[0], filt[1], pm4g.PM4G_TIME_EVENTS)
         log.close()
         log = f
@@ -420,12 +424,12 @@ def main():
                         ing_stream.wait_event(wait)
                     for d, h in zip(dcols[slot], (hc, ha, ht)):
                         d.copy_(h, non_blocking=True)
-                    return slot, ingest(pm4g, *dcols[slot], meta, False, ing_stream)
+                    return slot, ingest(pm4g, *dcols[slot], meta, False, ing_stream, filt=filt)
             if pipelined:
                 pending.append(pool.submit(work))
             else:   # small steps: pm4g_log_create copies the pinned host columns itself
                 f = concurrent.futures.Future()
-                f.set_result((slot, ingest(pm4g, hc, ha, ht, meta, True)))
+                f.set_result((slot, ingest(pm4g, hc, ha, ht, meta, True, filt=filt)))
                 pending.append(f)
 
         def e2e_step(prefetch):
@@ -433,7 +437,7 @@ def main():
             slot, log = pending.pop(0).result()
             if prefetch:
                 ingest_async()
-            res, v = run_step(pm4g, None, None, None, meta, comm, out, filt, log=log)
+            res, v = run_step(pm4g, None, None, None, meta, comm, out, None, log=log)   # (filtered at ingest)
             drained[slot] = torch.cuda.Event()
             drained[slot].record(stream)
             tabs = v.get()

@@ -100,6 +100,15 @@ typedef struct pm4g_log_desc {
  * build needs (ts_min, ts_max, key bit widths).  Synchronises `stream` once.
  * *out receives a new log in the "ingested" state. */
 pm4g_status pm4g_log_create(const pm4g_log_desc* desc, pm4g_stream_t stream, pm4g_log** out);
+/* pm4g_log_create followed by pm4g_filter_time(.., PM4G_TIME_EVENTS) (P:126,
+ * keep rows with t1 <= ts <= t2, inclusive) in ONE pass over the
+ * columns: every row is validated as pm4g_log_create does (same errors), while
+ * the metadata and the radix histograms cover the kept rows only, and the
+ * returned log is the lazily filtered one (pm4g_sort's first radix pass keeps
+ * the rows in range; see pm4g_filter_time).  With extra columns it is exactly
+ * the two calls.  EINVAL if t1 > t2.  Synchronises `stream` once. */
+pm4g_status pm4g_log_create_filtered(const pm4g_log_desc* desc, int64_t t1, int64_t t2, pm4g_stream_t stream,
+                                     pm4g_log** out);
 pm4g_status pm4g_log_destroy(pm4g_log* log);
 
 typedef struct pm4g_log_info {

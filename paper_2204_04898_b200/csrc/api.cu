@@ -218,6 +218,7 @@ struct Meta {
     long long ts_min, ts_max;
     unsigned int case_min, case_max;
     unsigned long long bad_case, bad_act, bad_extra;
+    unsigned long long kept;   // rows with t1 <= ts <= t2 (pm4g_log_create_filtered)
 };
 
 // One pass over the ingested columns: metadata (ts / case ranges), the first
@@ -225,11 +226,14 @@ struct Meta {
 // histograms of the case digits the sort's LSD passes will use (digit p of
 // case - case_lo, `bits` per digit, layout derived from [case_lo, case_hi)).
 // Vectorised: 4 rows per thread per iteration (16-byte loads of case and ts).
+// With tf, every row is still validated but the metadata, the kept count and
+// the histograms cover only the rows with t1 <= ts <= t2 (the events-mode
+// time filter of pm4g_log_create_filtered, fused into this pass).
 template <class P>
 __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ cs, const P* __restrict__ act,
                                                   const int64_t* __restrict__ ts, int64_t n, uint32_t lo,
                                                   uint32_t hi, uint32_t A, Meta* m, int hpasses, int hbits,
-                                                  uint32_t* __restrict__ hist) {
+                                                  uint32_t* __restrict__ hist, int tf, int64_t t1, int64_t t2) {
     // per-warp digit histograms (same-address atomics only within a warp)
     __shared__ uint32_t shw[8][4][256];
     for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&shw[0][0][0])[i] = 0;
@@ -238,14 +242,17 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
     long long tmin = LLONG_MAX, tmax = LLONG_MIN;
     unsigned cmin = 0xffffffffu, cmax = 0;
     unsigned long long bc = ~0ull, ba = ~0ull;
+    unsigned kept = 0;
     const uint32_t hmask = (1u << hbits) - 1;
     auto row = [&](int64_t i, uint32_t c, long long t, uint32_t a) {
+        if ((c < lo || c >= hi) && (unsigned long long)i < bc) bc = i;
+        if (a >= A && (unsigned long long)i < ba) ba = i;
+        if (tf && (t < t1 || t > t2)) return;
+        ++kept;
         tmin = min(tmin, t);
         tmax = max(tmax, t);
         cmin = min(cmin, c);
         cmax = max(cmax, c);
-        if ((c < lo || c >= hi) && (unsigned long long)i < bc) bc = i;
-        if (a >= A && (unsigned long long)i < ba) ba = i;
         const uint32_t f = c - lo;
         for (int p = 0; p < hpasses; ++p) atomicAdd(&sh[p][(f >> (p * hbits)) & hmask], 1u);
     };
@@ -269,8 +276,10 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
         cmax = max(cmax, __shfl_xor_sync(~0u, cmax, o));
         bc = min(bc, __shfl_xor_sync(~0u, bc, o));
         ba = min(ba, __shfl_xor_sync(~0u, ba, o));
+        kept += __shfl_xor_sync(~0u, kept, o);
     }
     if ((threadIdx.x & 31) == 0) {
+        if (kept) atomicAdd(&m->kept, (unsigned long long)kept);
         atomicMin(&m->ts_min, tmin);
         atomicMax(&m->ts_max, tmax);
         atomicMin(&m->case_min, cmin);
@@ -344,8 +353,10 @@ void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, 
     }
 }
 
-pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
-    Meta h{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u, ~0ull, ~0ull, ~0ull};
+pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s, const int64_t* tfilt) {
+    Meta h{LLONG_MAX, LLONG_MIN, 0xffffffffu, 0u, ~0ull, ~0ull, ~0ull, 0ull};
+    const int tf = tfilt ? 1 : 0;
+    const int64_t t1 = tfilt ? tfilt[0] : 0, t2 = tfilt ? tfilt[1] : 0;
     Scratch md(s);
     PM4G_TRY(md.alloc(sizeof(Meta)));
     Meta* dm = md.as<Meta>();
@@ -365,9 +376,9 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
         int g = grid_for((n + 3) / 4, 256);
         double bytes = (double)n * (12 + L->act_bytes);
         switch (L->act_bytes) {
-            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
-            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
-            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist)); break;
+            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
+            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
+            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
         }
         for (auto& c : L->extra)
             if (c.kind == PM4G_KIND_CODES)
@@ -382,6 +393,12 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s) {
         return fail(PM4G_EDATA, "activity code out of range (>= n_activities) at row " + std::to_string(h.bad_act));
     if (h.bad_extra != ~0ull)
         return fail(PM4G_EDATA, "extra-column code out of range at row " + std::to_string(h.bad_extra));
+    if (tf) {   // the log is the lazily time-filtered one (A1 fused into the sort's first pass)
+        L->tf_n = L->n;
+        L->tf_t1 = t1;
+        L->tf_t2 = t2;
+        L->n = (int64_t)h.kept;
+    }
     apply_meta(L, h.ts_min, h.ts_max, h.case_min, h.case_max, hpasses, hbits);
     return PM4G_OK;
 }
@@ -514,10 +531,42 @@ pm4g_status pm4g_prof_record(int32_t i, const char** name, double* start_ms, dou
     return PM4G_OK;
 }
 
+static pm4g_status log_create_impl(const pm4g_log_desc* d, cudaStream_t s, pm4g_log** out, const int64_t* tfilt);
+
 pm4g_status pm4g_log_create(const pm4g_log_desc* d, pm4g_stream_t stream, pm4g_log** out) {
+    return log_create_impl(d, (cudaStream_t)stream, out, nullptr);
+}
+
+pm4g_status pm4g_log_create_filtered(const pm4g_log_desc* d, int64_t t1, int64_t t2, pm4g_stream_t stream,
+                                     pm4g_log** out) {
     if (!d || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
+    if (t1 > t2) return fail(PM4G_EINVAL, "t1 > t2 (S:414)");
     cudaStream_t s = (cudaStream_t)stream;
+    if (d->n_extra > 0 || getenv("PM4G_NO_LAZY_FILTER")) {   // create, then the compacting filter
+        pm4g_log* P = nullptr;
+        PM4G_TRY(log_create_impl(d, s, &P, nullptr));
+        const pm4g_status st = pm4g_filter_time(P, t1, t2, PM4G_TIME_EVENTS, (pm4g_stream_t)s, out);
+        pm4g_log_destroy(P);
+        return st;
+    }
+    const int64_t tf[2] = {t1, t2};
+    pm4g_log* L = nullptr;
+    PM4G_TRY(log_create_impl(d, s, &L, tf));
+    if (L->n == 0 || L->wide) {   // only the narrow first pass of a non-empty log keeps rows on the fly
+        const pm4g_status st = materialize(L, s);
+        if (st) {
+            pm4g_log_destroy(L);
+            return st;
+        }
+    }
+    *out = L;
+    return PM4G_OK;
+}
+
+static pm4g_status log_create_impl(const pm4g_log_desc* d, cudaStream_t s, pm4g_log** out, const int64_t* tfilt) {
+    if (!d || !out) return fail(PM4G_EINVAL, "null argument");
+    *out = nullptr;
     if (d->n_events < 0) return fail(PM4G_EINVAL, "n_events < 0");
     if (d->n_events > MAX_SHARD_EVENTS)
         return fail(PM4G_EINVAL, "n_events exceeds 2^31-2 per shard; shard the log across ranks");
@@ -598,7 +647,7 @@ pm4g_status pm4g_log_create(const pm4g_log_desc* d, pm4g_stream_t stream, pm4g_l
         L->extra.push_back(x);
     }
     if ((st = dalloc((void**)&L->d_n_cases, 8, s)) != PM4G_OK) return bail(st);
-    if ((st = validate_and_meta(L, s)) != PM4G_OK) return bail(st);
+    if ((st = validate_and_meta(L, s, tfilt)) != PM4G_OK) return bail(st);
     *out = L;
     return PM4G_OK;
 }

@@ -29,6 +29,17 @@ typedef void* NcclComm;
 typedef int NcclResult;  // ncclSuccess = 0
 enum { NCCL_UINT64 = 5, NCCL_UINT8 = 1 };  // ncclDataType_t: ncclUint8 = 1, ncclUint64 = 5
 enum { NCCL_SUM = 0 };
+// NCCL is dlopen'ed (no link-time dependency); where its header is present the
+// ABI constants used here are checked against it at compile time.
+#if __has_include(<nccl.h>)
+}  // namespace pm4g
+#include <nccl.h>
+namespace pm4g {
+static_assert(NCCL_UINT64 == (int)ncclUint64 && NCCL_UINT8 == (int)ncclUint8, "ncclDataType_t values");
+static_assert(NCCL_SUM == (int)ncclSum && COMM_SUM == (int)ncclSum && COMM_MIN == (int)ncclMin &&
+                  COMM_MAX == (int)ncclMax, "ncclRedOp_t values");
+static_assert(sizeof(NcclUid) == sizeof(ncclUniqueId), "ncclUniqueId size");
+#endif
 
 struct NcclApi {
     void* h = nullptr;

@@ -343,7 +343,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp
 
 // ------------------------------------------------------------------ entry points
 // (implemented across the .cu files)
-pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s);   // K1
+// K1; tfilt = {t1, t2}: the log becomes the lazily events-filtered one (pm4g_log_create_filtered)
+pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s, const int64_t* tfilt = nullptr);
 void hist_layout(const pm4g_log* L, int* hpasses, int* hbits);
 void apply_meta(pm4g_log* L, int64_t ts_min, int64_t ts_max, uint32_t case_min, uint32_t case_max,
                 int hpasses, int hbits);

@@ -75,6 +75,7 @@ class pm4g_outputs(ctypes.Structure):
 
 _SIGS = {
     "pm4g_log_create": ([ctypes.POINTER(pm4g_log_desc), P, ctypes.POINTER(P)], I32),
+    "pm4g_log_create_filtered": ([ctypes.POINTER(pm4g_log_desc), I64, I64, P, ctypes.POINTER(P)], I32),
     "pm4g_log_destroy": ([P], I32),
     "pm4g_log_info_get": ([P, ctypes.POINTER(pm4g_log_info)], I32),
     "pm4g_sort": ([P, P], I32),
@@ -176,9 +177,11 @@ class Extra:
 
 def pm4g_log_create(case: torch.Tensor, act: torch.Tensor, ts: torch.Tensor, n_activities: int,
                     n_case_codes: int | None = None, case_lo: int = 0, case_hi: int = 0,
-                    extra: list[Extra] | None = None, borrow: bool = False, stream=None) -> "Log":
+                    extra: list[Extra] | None = None, borrow: bool = False, stream=None,
+                    time_filter: tuple[int, int] | None = None) -> "Log":
     """Columns are CUDA tensors (device input) or CPU tensors (PM4G_HOST_INPUT: copied H2D
-    inside the call).  case: 4-byte codes; act: 1/2/4-byte codes; ts: int64."""
+    inside the call).  case: 4-byte codes; act: 1/2/4-byte codes; ts: int64.
+    time_filter=(t1, t2): pm4g_log_create_filtered (create + events-mode time filter, one pass)."""
     n = int(case.numel())
     host = not case.is_cuda
     for t in (case, act, ts):
@@ -194,7 +197,11 @@ def pm4g_log_create(case: torch.Tensor, act: torch.Tensor, ts: torch.Tensor, n_a
                       case_lo, case_hi, n_activities, len(ex), cols,
                       (PM4G_HOST_INPUT if host else 0) | (PM4G_BORROW if borrow else 0))
     out = ctypes.c_void_p()
-    _check(lib().pm4g_log_create(ctypes.byref(d), _stream(stream), ctypes.byref(out)))
+    if time_filter is None:
+        _check(lib().pm4g_log_create(ctypes.byref(d), _stream(stream), ctypes.byref(out)))
+    else:
+        _check(lib().pm4g_log_create_filtered(ctypes.byref(d), int(time_filter[0]), int(time_filter[1]),
+                                              _stream(stream), ctypes.byref(out)))
     keep = (case, act, ts, ex) if borrow else None
     return Log(out, n_activities, act.element_size(), keep)
 

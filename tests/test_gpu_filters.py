@@ -256,3 +256,27 @@ def test_lazy_filter_then_partition_and_sort_analyze():
     for r, p in enumerate(parts):
         m = keep & (case >= bounds[r]) & (case < bounds[r + 1])
         _check(p, oracle.run(case[m], act[m], ts[m], A))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_create_filtered_equals_create_then_filter(seed):
+    """pm4g_log_create_filtered validates every row and builds the kept rows'
+    metadata in one pass: the result equals the oracle on the kept rows (P:126,
+    S:413), for ranges keeping some, none and all rows; invalid rows outside
+    the range are still rejected."""
+    case, act, ts = _lazy_case(10 + seed, n=200_000)
+    A, nc = 12, int(case.max()) + 1
+    for t1, t2 in ((-4 * 10**8, 6 * 10**8), (10**9 + 1, 10**9 + 9), (-10**9, 10**9)):
+        c, a, t = to_device_cols(case, act, ts, A)
+        f = pm4g.pm4g_log_create(c, a, t, A, n_case_codes=nc, time_filter=(t1, t2))
+        keep = oracle.filter_time(case, ts, t1, t2, 0)
+        assert f.n == int(keep.sum())
+        _check(f, _expect(case, act, ts, A, keep))
+    bad = act.copy()
+    bad[7] = A + 3
+    ts2 = ts.copy()
+    ts2[7] = 10**9   # outside the range, still validated
+    c, a, t = to_device_cols(case, bad, ts2, A + 4)
+    with pytest.raises(pm4g.Pm4gError) as e:
+        pm4g.pm4g_log_create(c, a, t, A, n_case_codes=nc, time_filter=(-10**8, 10**8))
+    assert e.value.status == pm4g.PM4G_EDATA
