@@ -753,16 +753,21 @@ void free_variants(pm4g_variant_table* v) {
 //     reruns the general round-based engine (group_items) from scratch.
 // Result: item_group[c] = dense gid, per-group count / min case / total length,
 // i.e. the Groups of group_items without a compaction or item pass.
-// a warp's task: 32 * IPT consecutive cases (IPT = 4; IPT = 1 for small logs, so their few
-// tasks spread over more warps and CTAs instead of one CTA's latency chain)
+// a warp's task: 32 * IPT consecutive cases (IPT = PM4G_VG_IPT; IPT = 1 for small logs,
+// so their few tasks spread over more warps and CTAs instead of one CTA's latency chain)
 constexpr int VG_THREADS = 256;
-// per-CTA key cache entries and minimum CTAs per SM (sweep at 100M: 1024 entries
-// with 4 CTAs per SM 0.50 ms; 2048 / 3 CTAs 0.57; 1024 / 5 0.53; 512 / 6 0.59)
+// per-CTA key cache entries, minimum CTAs per SM and cases per lane per task
+// (sweep, 100M / 1B-8 shard: 2 cases per lane, 1024 entries, 4 CTAs per SM
+// 0.36 / 0.36 ms; 4 per lane 0.50 / 0.55; 1 per lane 0.43 / 0.40; 8 per lane
+// 0.62 / 0.97; 2048 entries with 3 CTAs 0.60 / 0.45)
 #ifndef PM4G_VG_CACHE
 #define PM4G_VG_CACHE 1024
 #endif
 #ifndef PM4G_VG_MINB
 #define PM4G_VG_MINB 4
+#endif
+#ifndef PM4G_VG_IPT
+#define PM4G_VG_IPT 2   // cases per lane per task (large logs)
 #endif
 constexpr int VG_CACHE = PM4G_VG_CACHE, VG_FILL = VG_CACHE / 2, VG_PROBES = 8;
 constexpr size_t VG_SMEM = (size_t)VG_CACHE * (8 + 8 + 4 + 4 + 4 + 4 + 4);
@@ -1485,13 +1490,13 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     Scratch gw(s);
     const bool small = n_items < (uint64_t)num_sms() * 8 * 128;   // fewer 128-case tasks than warps
     const bool fine = small;   // gids one by one (no empty ones: the table may take k_small_variants)
-    const int ipt = small ? 1 : 4;
-    auto kern = small ? k_vgroup<ACT, 1, 1> : k_vgroup<ACT, 4, 8>;
+    const int ipt = small ? 1 : PM4G_VG_IPT;
+    auto kern = small ? k_vgroup<ACT, 1, 1> : k_vgroup<ACT, PM4G_VG_IPT, 8>;
     PM4G_MAX_SMEM((k_vgroup<ACT, 1, 1>));
-    PM4G_MAX_SMEM((k_vgroup<ACT, 4, 8>));
+    PM4G_MAX_SMEM((k_vgroup<ACT, PM4G_VG_IPT, 8>));
     static int per_sm = -1;
     if (per_sm < 0)
-        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgroup<ACT, 4, 8>, VG_THREADS, VG_SMEM));
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vgroup<ACT, PM4G_VG_IPT, 8>, VG_THREADS, VG_SMEM));
     const uint64_t tasks = (n_items + 32 * ipt - 1) / (32 * ipt);
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((tasks + VG_THREADS / 32 - 1) / (VG_THREADS / 32),
                                                                     (uint64_t)std::max(per_sm, 1) * num_sms()));
@@ -1554,7 +1559,8 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     if ((st = dalloc_t(&g.inv, Ga1, s))) return bail(st);
     const int wbits = std::max(1, bit_width_u64(n_items));
     const uint32_t* g_w = gw.as<uint32_t>();
-    if (Ga <= VO_MAX_GROUPS) {   // ordered and emitted in one launch (k_small_variants / k_vorder)
+    static const uint64_t vo_max = getenv("PM4G_VO_MAX") ? strtoull(getenv("PM4G_VO_MAX"), nullptr, 10) : VO_MAX_GROUPS;
+    if (Ga <= std::min(vo_max, VO_MAX_GROUPS)) {   // ordered and emitted in one launch (k_small_variants / k_vorder)
         if (Ga)
             PM4G_LAUNCH("k_variant_sortkeys", Ga * 20.0, s,
                         (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight,
