@@ -229,11 +229,11 @@ struct Meta {
 // With tf, every row is still validated but the metadata, the kept count and
 // the histograms cover only the rows with t1 <= ts <= t2 (the events-mode
 // time filter of pm4g_log_create_filtered, fused into this pass).
-template <class P>
+template <class P, bool TF>
 __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ cs, const P* __restrict__ act,
                                                   const int64_t* __restrict__ ts, int64_t n, uint32_t lo,
                                                   uint32_t hi, uint32_t A, Meta* m, int hpasses, int hbits,
-                                                  uint32_t* __restrict__ hist, int tf, int64_t t1, int64_t t2) {
+                                                  uint32_t* __restrict__ hist, int64_t t1, int64_t t2) {
     // per-warp digit histograms (same-address atomics only within a warp)
     __shared__ uint32_t shw[8][4][256];
     for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&shw[0][0][0])[i] = 0;
@@ -247,8 +247,10 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
     auto row = [&](int64_t i, uint32_t c, long long t, uint32_t a) {
         if ((c < lo || c >= hi) && (unsigned long long)i < bc) bc = i;
         if (a >= A && (unsigned long long)i < ba) ba = i;
-        if (tf && (t < t1 || t > t2)) return;
-        ++kept;
+        if (TF) {
+            if (t < t1 || t > t2) return;
+            ++kept;
+        }
         tmin = min(tmin, t);
         tmax = max(tmax, t);
         cmin = min(cmin, c);
@@ -256,16 +258,34 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
         const uint32_t f = c - lo;
         for (int p = 0; p < hpasses; ++p) atomicAdd(&sh[p][(f >> (p * hbits)) & hmask], 1u);
     };
-    const bool vec = (((uintptr_t)cs | (uintptr_t)ts) & 15) == 0;
+    const bool vec = (((uintptr_t)cs | (uintptr_t)ts) & 15) == 0 && ((uintptr_t)act & (4 * sizeof(P) - 1)) == 0;
     const int64_t nq = vec ? n / 4 : 0;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
         const uint4 c4 = ((const uint4*)cs)[q];
         const longlong2 t01 = ((const longlong2*)ts)[2 * q], t23 = ((const longlong2*)ts)[2 * q + 1];
         const int64_t i = 4 * q;
-        row(i, c4.x, t01.x, (uint32_t)act[i]);
-        row(i + 1, c4.y, t01.y, (uint32_t)act[i + 1]);
-        row(i + 2, c4.z, t23.x, (uint32_t)act[i + 2]);
-        row(i + 3, c4.w, t23.y, (uint32_t)act[i + 3]);
+        uint32_t a[4];
+        if constexpr (sizeof(P) == 1) {   // the four activities in one 4-byte load
+            const uint32_t w = ((const uint32_t*)act)[q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) a[k] = (w >> (8 * k)) & 0xffu;
+        } else if constexpr (sizeof(P) == 2) {
+            const uint2 w = ((const uint2*)act)[q];
+            a[0] = w.x & 0xffffu;
+            a[1] = w.x >> 16;
+            a[2] = w.y & 0xffffu;
+            a[3] = w.y >> 16;
+        } else {
+            const uint4 w = ((const uint4*)act)[q];
+            a[0] = w.x;
+            a[1] = w.y;
+            a[2] = w.z;
+            a[3] = w.w;
+        }
+        row(i, c4.x, t01.x, a[0]);
+        row(i + 1, c4.y, t01.y, a[1]);
+        row(i + 2, c4.z, t23.x, a[2]);
+        row(i + 3, c4.w, t23.y, a[3]);
     }
     for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         row(i, cs[i], ts[i], (uint32_t)act[i]);
@@ -276,10 +296,10 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
         cmax = max(cmax, __shfl_xor_sync(~0u, cmax, o));
         bc = min(bc, __shfl_xor_sync(~0u, bc, o));
         ba = min(ba, __shfl_xor_sync(~0u, ba, o));
-        kept += __shfl_xor_sync(~0u, kept, o);
+        if (TF) kept += __shfl_xor_sync(~0u, kept, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        if (kept) atomicAdd(&m->kept, (unsigned long long)kept);
+        if (TF && kept) atomicAdd(&m->kept, (unsigned long long)kept);
         atomicMin(&m->ts_min, tmin);
         atomicMax(&m->ts_max, tmax);
         atomicMin(&m->case_min, cmin);
@@ -376,9 +396,9 @@ pm4g_status validate_and_meta(pm4g_log* L, cudaStream_t s, const int64_t* tfilt)
         int g = grid_for((n + 3) / 4, 256);
         double bytes = (double)n * (12 + L->act_bytes);
         switch (L->act_bytes) {
-            case 1: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint8_t><<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
-            case 2: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint16_t><<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
-            default: PM4G_LAUNCH("k_validate", bytes, s, k_validate<uint32_t><<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, tf, t1, t2)); break;
+            case 1: PM4G_LAUNCH("k_validate", bytes, s, (tf ? k_validate<uint8_t, true> : k_validate<uint8_t, false>)<<<g, 256, 0, s>>>(L->case_, (const uint8_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, t1, t2)); break;
+            case 2: PM4G_LAUNCH("k_validate", bytes, s, (tf ? k_validate<uint16_t, true> : k_validate<uint16_t, false>)<<<g, 256, 0, s>>>(L->case_, (const uint16_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, t1, t2)); break;
+            default: PM4G_LAUNCH("k_validate", bytes, s, (tf ? k_validate<uint32_t, true> : k_validate<uint32_t, false>)<<<g, 256, 0, s>>>(L->case_, (const uint32_t*)L->act, L->ts, n, L->case_lo, hi, L->A, dm, hpasses, hbits, L->hist, t1, t2)); break;
         }
         for (auto& c : L->extra)
             if (c.kind == PM4G_KIND_CODES)

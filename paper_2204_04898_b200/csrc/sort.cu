@@ -37,9 +37,24 @@
 namespace pm4g {
 
 constexpr int RADIX = 256;
-constexpr int SORT_THREADS = 512;
+#ifndef PM4G_SORT_THREADS   // sweep knobs (PM4G_NVCC_EXTRA): radix-pass CTA geometry
+#define PM4G_SORT_THREADS 512
+#endif
+#ifndef PM4G_SORT_IPT
+#define PM4G_SORT_IPT 8
+#endif
+#ifndef PM4G_SORT_MINB
+#define PM4G_SORT_MINB 2
+#endif
+#ifndef PM4G_FMT_THREADS       // format-kernel CTA geometry
+#define PM4G_FMT_THREADS 512
+#endif
+#ifndef PM4G_FMT_IPT
+#define PM4G_FMT_IPT 8
+#endif
+constexpr int SORT_THREADS = PM4G_SORT_THREADS;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_IPT = 8;
+constexpr int SORT_IPT = PM4G_SORT_IPT;
 constexpr int SORT_TILE = SORT_THREADS * SORT_IPT;  // 4096
 constexpr int MAX_PASSES = 8;
 
@@ -321,7 +336,7 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
 // HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
 // the digits sit above ts_bits >= 32), extracted with one 32-bit shift
 template <class P, bool FROM_COLS, bool WITH_IDX, bool HI, bool WIDE = false, bool TF = false>
-__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
+__global__ __launch_bounds__(SORT_THREADS, PM4G_SORT_MINB) void k_onesweep(PassArgs<P, FROM_COLS, WITH_IDX> a) {
     using Lay = OsLayout<P, FROM_COLS, WITH_IDX, WIDE>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* u_key = (uint64_t*)(smem + Lay::o_in);
@@ -402,7 +417,7 @@ struct OsPfLayout {
 };
 
 template <class P, bool HI>
-__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf(PassArgs<P, false, false> a, uint32_t n_tiles) {
+__global__ __launch_bounds__(SORT_THREADS, PM4G_SORT_MINB) void k_onesweep_pf(PassArgs<P, false, false> a, uint32_t n_tiles) {
     using Lay = OsPfLayout<P>;
     extern __shared__ __align__(128) unsigned char smem[];
     P* v_act = (P*)(smem + Lay::o_vact);
@@ -480,7 +495,7 @@ struct Os0Layout {
 };
 
 template <class P, bool HI, bool TF>
-__global__ __launch_bounds__(SORT_THREADS, 2) void k_onesweep_pf0(PassArgs<P, true, false> a, uint32_t n_tiles) {
+__global__ __launch_bounds__(SORT_THREADS, PM4G_SORT_MINB) void k_onesweep_pf0(PassArgs<P, true, false> a, uint32_t n_tiles) {
     using Lay = Os0Layout<P>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t* u_case = (uint32_t*)(smem + Lay::o_case);
@@ -721,7 +736,7 @@ static pm4g_status lsd_sort(const uint32_t* in_case, const int64_t* in_ts, const
 // case offsets; each case owned by this tile (head inside it) is sorted by key
 // in shared memory.  A case may run up to FMT_EXT positions past the tile end;
 // longer ones (and cases over FMT_WARP_MAX rows) go to the exact fallback.
-constexpr int FMT_THREADS = 512, FMT_IPT = 8, FMT_TILE = FMT_THREADS * FMT_IPT;
+constexpr int FMT_THREADS = PM4G_FMT_THREADS, FMT_IPT = PM4G_FMT_IPT, FMT_TILE = FMT_THREADS * FMT_IPT;
 constexpr int FMT_EXT = 512, FMT_BUF = FMT_TILE + FMT_EXT;
 constexpr int FMT_WARP_MAX = 1024;  // longer cases: exact fallback (stable radix sort)
 constexpr int FMT_TIES = 512;       // tie groups listed per tile (more: laid out in place)
