@@ -1239,6 +1239,9 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
 // whose latency dominated at these sizes.
 constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = 8, VO_CHUNK = VO_THREADS * VO_IPT;
 constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs
+#ifndef PM4G_VO_TARGET
+#define PM4G_VO_TARGET 256   // groups per chunk aimed at (more CTAs, but each reads every chunk's histogram)
+#endif
 
 struct VoArgs {
     const uint64_t* weight;
@@ -1599,7 +1602,7 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
         PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vorder<ACT>, VO_THREADS, dyn));
     const uint64_t Ga = g.Ga;
     const uint64_t maxc = (uint64_t)std::max(per_sm, 1) * num_sms();
-    uint64_t nc = std::min<uint64_t>(maxc, std::max<uint64_t>((Ga + 255) / 256, 1));
+    uint64_t nc = std::min<uint64_t>(maxc, std::max<uint64_t>((Ga + PM4G_VO_TARGET - 1) / PM4G_VO_TARGET, 1));
     nc = std::max<uint64_t>(nc, (Ga + VO_CHUNK - 1) / VO_CHUNK);
     nc = std::min<uint64_t>(nc, 2 * VO_THREADS);
     if (nc > maxc || nc * VO_CHUNK < Ga) return fail(PM4G_ECUDA, "variant table too large for the cooperative ordering");
