@@ -652,6 +652,10 @@ pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* 
         o.k2 = o.k1 + std::max<uint64_t>(cap, 1);
     }
     PM4G_TRY(aggregate(L, o, s));
+    if (t_pending_format) {   // pm4g_sort_analyze: the format's fallback count, now past the aggregate
+        PM4G_TRY(sort_defer_copy(t_pending_format, s));
+        t_pending_format = nullptr;
+    }
     if (want_tables || want_mm) {
         if (comm) PM4G_TRY(comm_allreduce_u64(comm, o.packed, packed_len(L->A), s));
         PM4G_TRY(finalize_tables(o.packed, L->A, out->cnt, out->dur_sum, out->mean, out->start,

@@ -738,8 +738,10 @@ pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* c
     FmtDeferred d(s);
     PM4G_TRY(sort_impl(L, s, &d));
     // the analysis synchronises (variant counters); the deferred format check
-    // then costs no extra wait
+    // then costs no extra wait (its count is copied right after the aggregate launch)
+    t_pending_format = &d;
     pm4g_status st = pm4g_analyze(L, out, comm, stream);
+    t_pending_format = nullptr;
     bool fixed = false;
     const pm4g_status fs = sort_finish(&d, s, &fixed);
     if (fs != PM4G_OK) {   // the input columns are gone and the order is provisional

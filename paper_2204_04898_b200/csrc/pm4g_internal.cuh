@@ -360,8 +360,14 @@ struct FmtDeferred {
     bool active = false;
     uint32_t* h_nbig = nullptr;             // pinned: fallback count, copied after k_format
     cudaEvent_t ev = nullptr;               // recorded after that copy
+    const uint32_t* d_nbig = nullptr;       // the device count, until the copy is enqueued
     explicit FmtDeferred(cudaStream_t s) : grp(s), st(s) {}
 };
+// Enqueue the fallback count's copy to pinned memory (+ its event): deferred
+// past the aggregate launch, so no copy sits between k_format and k_aggregate.
+pm4g_status sort_defer_copy(FmtDeferred* d, cudaStream_t s);
+// set by pm4g_sort_analyze for the pm4g_analyze call it makes (this thread)
+extern thread_local FmtDeferred* t_pending_format;
 pm4g_status sort_log(pm4g_log* L, cudaStream_t s, FmtDeferred* d = nullptr);   // A2-A4
 pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed);
 pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4

@@ -1274,10 +1274,9 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     if (!h_nbig) PM4G_CK(cudaHostAlloc((void**)&h_nbig, 4, cudaHostAllocPortable));
     if (!evs[dev]) PM4G_CK(cudaEventCreateWithFlags(&evs[dev], cudaEventDisableTiming));
     cudaEvent_t ev = evs[dev];
-    PM4G_CK(cudaMemcpyAsync(h_nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
-    PM4G_CK(cudaEventRecord(ev, s));
     d->h_nbig = h_nbig;
     d->ev = ev;
+    d->d_nbig = fa.big_count;   // copied by sort_defer_copy (after the aggregate launch)
     d->grp.take(grp);
     static_assert(sizeof(FmtArgs<P>) <= sizeof(d->fa_raw), "type-erased FmtArgs");
     memcpy(d->fa_raw, &fa, sizeof(fa));
@@ -1440,9 +1439,20 @@ static pm4g_status finish_t(FmtDeferred* d, cudaStream_t s, bool* fixed) {
     return format_fallback<P>(fa, nbig, s);
 }
 
+thread_local FmtDeferred* t_pending_format = nullptr;
+
+pm4g_status sort_defer_copy(FmtDeferred* d, cudaStream_t s) {
+    if (!d || !d->d_nbig) return PM4G_OK;
+    PM4G_CK(cudaMemcpyAsync(d->h_nbig, d->d_nbig, 4, cudaMemcpyDeviceToHost, s));
+    PM4G_CK(cudaEventRecord(d->ev, s));
+    d->d_nbig = nullptr;
+    return PM4G_OK;
+}
+
 pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed) {
     *fixed = false;
     if (!d->active) return PM4G_OK;
+    PM4G_TRY(sort_defer_copy(d, s));
     d->active = false;
     switch (d->act_bytes) {
         case 1: return finish_t<uint8_t>(d, s, fixed);
