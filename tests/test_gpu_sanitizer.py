@@ -35,7 +35,7 @@ CSRC = os.path.join(ROOT, "paper_2204_04898_b200", "csrc")
 # (source text of the first access, source text of the second access)
 BENIGN = [
     ("s_perm[s0 + r] = (uint16_t)p;", "s_perm[s0 + r] = (uint16_t)p;"),
-    ("st.off[j] = off[c0 + j];", "st.off["),
+    ("st.off[j] = ", "st.off["),
 ]
 
 
