@@ -119,6 +119,12 @@ CONFIGS: dict[str, LogSpec] = {
                     40, 0.02, 4),
     "1B": LogSpec("1B", 50_000_000, 256, 20.0, 1_000_000_000, 1 << 18, False, 0.0,
                   80, 0.02, 5),
+    # long cases (not a BASELINE.json config): the BPIC2018 shape (Table 1:
+    # bpic2018_2 = 5,028,532 events / 87,618 cases / 28,457 variants / 41 activities;
+    # x1 base = half), mean 57 events per case, fully shuffled rows -- the in-case
+    # ranking's O(m) per row and the exact fallback's long cases at their heaviest
+    "bpic2018": LogSpec("bpic2018", 43_809, 41, 2_514_266 / 43_809, 2_514_266,
+                        28_457, True, 0.0, 400, 0.02, 6),
 }
 
 

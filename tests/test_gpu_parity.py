@@ -41,7 +41,7 @@ def test_random_tiny_logs(seed):
     check_log(case, act, ts, A, n_case_codes=ncodes)
 
 
-@pytest.mark.parametrize("name", ["tiny", "roadtraffic", "bpic2019"])
+@pytest.mark.parametrize("name", ["tiny", "roadtraffic", "bpic2019", "bpic2018"])
 def test_configs_full_size(name):
     L = generate(CONFIGS[name])
     g, r = check_log(L.case.numpy(), L.act.numpy(), L.ts.numpy(), L.n_activities,
@@ -358,8 +358,9 @@ def test_sort_analyze_fallback_cases(shape):
                   oracle.run(case, act, ts, 7))
 
 
-def test_sort_analyze_config_bpic2019():
-    L = generate(CONFIGS["bpic2019"])
+@pytest.mark.parametrize("name", ["bpic2019", "bpic2018"])
+def test_sort_analyze_config(name):
+    L = generate(CONFIGS[name])
     c, a, t = L.case.numpy(), L.act.numpy(), L.ts.numpy()
     assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True),
                   oracle.run(c, a, t, L.n_activities))
@@ -439,3 +440,20 @@ def test_format_tie_groups(ts_range, extras):
     else:
         assert_parity(gpu_run(case, act, ts, 9, n_case_codes=int(case.max()) + 1),
                       oracle.run(case, act, ts, 9))
+
+
+def test_long_cases_up_to_the_rank_limit():
+    """Cases of 300-1024 rows (the in-shared-memory ranking's O(m) per row at its
+    largest; 1024 = FMT_WARP_MAX) mixed with short ones and cases just past the
+    limit (the exact fallback), shuffled, with timestamp ties: the formatted log
+    and every aggregate equal the oracle's."""
+    rng = np.random.default_rng(41)
+    lens = np.concatenate([rng.integers(300, 1025, 300), rng.integers(1, 40, 20_000), [1025, 1030, 2000]])
+    case = np.repeat(rng.permutation(lens.size), lens)
+    n = case.size
+    case = case[rng.permutation(n)]
+    act = rng.integers(0, 30, n)
+    ts = rng.integers(0, 5_000, n) * 7
+    for sa in (False, True):
+        assert_parity(gpu_run(case, act, ts, 30, n_case_codes=int(case.max()) + 1, sort_analyze=sa),
+                      oracle.run(case, act, ts, 30))
