@@ -1034,6 +1034,16 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
     }
 }
 
+// (the radix fallback) the groups' u64 weights and representatives as the u32
+// arrays k_vfinal reads
+__global__ void k_vrekey(const uint64_t* __restrict__ weight, const uint32_t* __restrict__ rep, uint64_t G,
+                         uint32_t* __restrict__ w32, uint32_t* __restrict__ r32) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G; g += (uint64_t)gridDim.x * blockDim.x) {
+        w32[g] = (uint32_t)weight[g];
+        r32[g] = rep[g];
+    }
+}
+
 // dense groups -> Groups arrays (u64 weight, rep item = min case = order) and
 // the sort key ((Wmax - weight) << order_bits) | rep of each group
 __global__ void k_vfinal(const uint32_t* __restrict__ g_w, const uint32_t* __restrict__ g_rep, uint64_t G,
@@ -1239,6 +1249,7 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
 // whose latency dominated at these sizes.
 constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = 8, VO_CHUNK = VO_THREADS * VO_IPT;
 constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs
+constexpr pm4g_status VO_NOT_LAUNCHED = (pm4g_status)100;   // internal: the cooperative grid was refused
 #ifndef PM4G_VO_TARGET
 #define PM4G_VO_TARGET 256   // groups per chunk aimed at (more CTAs, but each reads every chunk's histogram)
 #endif
@@ -1590,6 +1601,30 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     return PM4G_OK;
 }
 
+// The one-pass table's ordering with the library radix sort (the general path;
+// used when the cooperative kernel cannot be launched): g.sorted / g.inv.
+static pm4g_status order_groups_radix(Groups& g, int order_bits, uint64_t n_items, cudaStream_t s) {
+    const uint64_t Ga = g.Ga, Ga1 = std::max<uint64_t>(Ga, 1);
+    const int wbits = std::max(1, bit_width_u64(n_items));
+    PM4G_TRY(dalloc_t(&g.sorted, Ga1, s));
+    Scratch sk(s), gw(s);   // keys [Ga] | vals [Ga]; the u32 weights / reps k_vfinal reads
+    PM4G_TRY(sk.alloc(Ga * 12 + 16));
+    PM4G_TRY(gw.alloc(Ga * 8 + 16));
+    uint64_t* key = sk.as<uint64_t>();
+    uint32_t* val = (uint32_t*)(key + Ga);
+    uint32_t* w32 = gw.as<uint32_t>();
+    uint32_t* r32 = w32 + Ga;
+    if (!Ga) return PM4G_OK;
+    PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
+                (k_vrekey<<<gsz(Ga), 256, 0, s>>>(g.weight, g.rep_item, Ga, w32, r32)));
+    PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
+                (k_vfinal<<<gsz(Ga), 256, 0, s>>>(w32, r32, Ga, wbits, order_bits, g.weight, g.rep_item, g.order,
+                                                  key, val)));
+    PM4G_TRY(radix_sort_u64_to(key, val, g.sorted, (int64_t)Ga, wbits + order_bits, s));
+    PM4G_LAUNCH("k_variant_inv", Ga * 8.0, s, (k_inv<<<gsz(Ga), 256, 0, s>>>(g.sorted, Ga, g.inv)));
+    return PM4G_OK;
+}
+
 // k_vorder: the medium one-pass table ordered, emitted and indexed in one cooperative launch
 template <class ACT>
 static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t* off, const ACT* acts,
@@ -1643,8 +1678,19 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     if (cv_inside) a.case_variant = v->case_variant;
     PM4G_CK(cudaMemsetAsync(a.mx, 0, 16, s));
     void* args[] = {(void*)&a, (void*)&acts};
-    PM4G_LAUNCH("k_variant_order", Ga * 60.0 + g.total_len * 5.0 + (with_case_variant ? n_items * 8.0 : 0.0), s,
-                (cudaLaunchCooperativeKernel((const void*)k_vorder<ACT>, dim3((unsigned)nc), dim3(VO_THREADS), args, dyn, s)));
+    // a cooperative grid can be refused (e.g. too large while other work holds the
+    // device, or under a tool): the caller then orders the table with the radix passes
+    const bool no_coop = getenv("PM4G_DEBUG_NO_COOP") != nullptr;   // test hook: force the fallback
+    if (no_coop) return VO_NOT_LAUNCHED;
+    prof_begin("k_variant_order", Ga * 60.0 + g.total_len * 5.0 + (cv_inside ? n_items * 8.0 : 0.0), s);
+    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k_vorder<ACT>, dim3((unsigned)nc),
+                                                       dim3(VO_THREADS), args, dyn, s);
+    prof_end(s);
+    if (le != cudaSuccess) {
+        cudaGetLastError();
+        return VO_NOT_LAUNCHED;
+    }
+    count_launch();
     if (with_case_variant && !cv_inside && n_items)
         PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
                     (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items, v->case_variant)));
@@ -1722,10 +1768,19 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
         if (!g.sorted && g.Ga > (uint64_t)SV_MAX) {   // a medium one-pass table: one cooperative launch
             const pm4g_status vs = order_medium<ACT>(g, v, (const uint32_t*)off, acts, rep_code, k1, k2, n_items,
                                                      with_case_variant, s);
-            if (vs) return bail(vs);
-            g.free(s);
-            *out = v;
-            return PM4G_OK;
+            if (vs == PM4G_OK) {
+                g.free(s);
+                *out = v;
+                return PM4G_OK;
+            }
+            if (vs != VO_NOT_LAUNCHED) return bail(vs);
+            // not launched: order with the radix passes, then the general emission below
+            if (v->case_variant) {
+                dfree(v->case_variant, s);
+                v->case_variant = nullptr;
+            }
+            const pm4g_status os = order_groups_radix(g, order_bits, n_items, s);
+            if (os) return bail(os);
         }
         if (!g.sorted) {   // a small one-pass table: ordered and emitted by one CTA
             PM4G_MAX_SMEM(k_small_variants<ACT>);

@@ -457,3 +457,15 @@ def test_long_cases_up_to_the_rank_limit():
     for sa in (False, True):
         assert_parity(gpu_run(case, act, ts, 30, n_case_codes=int(case.max()) + 1, sort_analyze=sa),
                       oracle.run(case, act, ts, 30))
+
+
+@pytest.mark.parametrize("name", ["bpic2019", "bpic2018"])
+def test_variant_ordering_radix_fallback(monkeypatch, name):
+    """A table of 2k-1.2M groups is ordered by one cooperative kernel; when the
+    grid cannot be launched (PM4G_DEBUG_NO_COOP forces it) the library radix
+    passes order it instead -- same results (R11: count desc, rep asc)."""
+    monkeypatch.setenv("PM4G_DEBUG_NO_COOP", "1")
+    L = generate(CONFIGS[name])
+    c, a, t = L.case.numpy(), L.act.numpy(), L.ts.numpy()
+    assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True),
+                  oracle.run(c, a, t, L.n_activities))
