@@ -117,34 +117,40 @@ pm4g_status comm_allreduce_u64_op(pm4g_comm* c, uint64_t* buf, size_t count, int
 }
 
 __global__ void k_pack_entries(const pm4g_variant_table v, uint64_t* out) {
-    // per entry: k1, k2, count, (rep_case | len << 32)
+    // per entry: k1, k2, count, (rep_case | sequence offset << 32)
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < v.V;
          i += (uint64_t)gridDim.x * blockDim.x) {
         out[4 * i + 0] = v.k1[i];
         out[4 * i + 1] = v.k2[i];
         out[4 * i + 2] = v.count[i];
-        out[4 * i + 3] = (uint64_t)v.rep_case[i] | ((uint64_t)v.len[i] << 32);
+        out[4 * i + 3] = (uint64_t)v.rep_case[i] | (v.seq_off[i] << 32);
     }
 }
 
-__global__ void k_unpack_entries(const uint64_t* in, uint64_t V, const uint32_t* acts_in,
-                                 uint64_t T, pm4g_variant_table v) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V;
+// every rank's packed entries (rank-major, contiguous) -> the merge's flat
+// items; the sequences stay where they were received.  sz: [R][2] (V_r, T_r).
+__global__ void k_unpack_entries(const uint64_t* __restrict__ in, const uint64_t* __restrict__ sz, int R,
+                                 MergeItems m) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m.V;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        v.k1[i] = in[4 * i + 0];
-        v.k2[i] = in[4 * i + 1];
-        v.count[i] = in[4 * i + 2];
-        v.rep_case[i] = (uint32_t)in[4 * i + 3];
-        v.len[i] = (uint32_t)(in[4 * i + 3] >> 32);
+        uint64_t vb = 0, tb = 0;
+        for (int r = 0; r < R; ++r) {   // the entry's rank (R is small)
+            if (i < vb + sz[2 * r]) break;
+            vb += sz[2 * r];
+            tb += sz[2 * r + 1];
+        }
+        m.k1[i] = in[4 * i + 0];
+        m.k2[i] = in[4 * i + 1];
+        m.w[i] = in[4 * i + 2];
+        m.ord[i] = (uint32_t)in[4 * i + 3];
+        m.so[i] = (uint32_t)(tb + (in[4 * i + 3] >> 32));
     }
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < T;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        v.seq_act[i] = acts_in[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) m.so[m.V] = (uint32_t)m.T;
 }
 
 pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* local, cudaStream_t s,
                                           pm4g_variant_table** out) {
-    const int R = c->nranks;
+    const int R = c->nranks, me = c->rank;
     if (R == 1) {
         const pm4g_variant_table* parts[1] = {local};
         return merge_variant_tables(parts, 1, s, out, 0);
@@ -160,63 +166,45 @@ pm4g_status comm_variants_allgather_merge(pm4g_comm* c, pm4g_variant_table* loca
     std::vector<uint64_t> sizes(2 * R);
     PM4G_CK(cudaMemcpyAsync(sizes.data(), d_sz, 16 * R, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
-    uint64_t Vmax = 1, Tmax = 1;
+    std::vector<uint64_t> vb(R + 1, 0), tb(R + 1, 0);
     for (int i = 0; i < R; ++i) {
-        Vmax = std::max(Vmax, sizes[2 * i]);
-        Tmax = std::max(Tmax, sizes[2 * i + 1]);
+        vb[i + 1] = vb[i] + sizes[2 * i];
+        tb[i + 1] = tb[i] + sizes[2 * i + 1];
     }
-    Scratch send(s), recv(s);
-    PM4G_TRY(send.alloc(Vmax * 32 + Tmax * 4));
-    PM4G_TRY(recv.alloc((size_t)R * (Vmax * 32 + Tmax * 4)));
-    uint64_t* se = send.as<uint64_t>();
-    uint32_t* sa = (uint32_t*)(se + 4 * Vmax);
+    const uint64_t V = vb[R], T = tb[R];
+    if (V > 0xfffffffeull || T > (uint64_t)MAX_SHARD_EVENTS)
+        return fail(PM4G_EINVAL, "merged variant tables exceed 2^31 - 2 activities");
+    // an all-gather with per-rank sizes (grouped sends / receives): every rank's
+    // entries and sequences land contiguously, in rank order, where the merge
+    // reads them -- this rank's own are written in place
+    Scratch ent(s), acts(s), items(s);
+    PM4G_TRY(ent.alloc(V * 32 + 16));
+    PM4G_TRY(acts.alloc(T * 4 + 16));
+    uint64_t* re = ent.as<uint64_t>();
+    uint32_t* ra = acts.as<uint32_t>();
     if (local->V) {
         int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((local->V + 255) / 256, 1024));
-        PM4G_LAUNCH("k_pack_entries", local->V * 64.0, s, k_pack_entries<<<g, 256, 0, s>>>(*local, se));
-        PM4G_CK(cudaMemcpyAsync(sa, local->seq_act, local->total_len * 4, cudaMemcpyDeviceToDevice, s));
+        PM4G_LAUNCH("k_pack_entries", local->V * 64.0, s, k_pack_entries<<<g, 256, 0, s>>>(*local, re + 4 * vb[me]));
+        PM4G_CK(cudaMemcpyAsync(ra + tb[me], local->seq_act, local->total_len * 4, cudaMemcpyDeviceToDevice, s));
     }
-    uint64_t* re = recv.as<uint64_t>();
-    uint32_t* ra = (uint32_t*)(re + 4 * Vmax * R);
-    r = g_nccl.allGather(se, re, 4 * Vmax, NCCL_UINT64, c->comm, s);
-    if (r) return nccl_fail(r, "ncclAllGather(entries)");
-    r = g_nccl.allGather(sa, ra, Tmax * 4, NCCL_UINT8, c->comm, s);
-    if (r) return nccl_fail(r, "ncclAllGather(sequences)");
-    // unpack into R temporary tables (this rank's own table is used as is, so
-    // its per-case index survives) and merge
-    std::vector<pm4g_variant_table*> parts(R, nullptr);
-    pm4g_status st = PM4G_OK;
-    for (int i = 0; i < R && st == PM4G_OK; ++i) {
-        if (i == c->rank) continue;
-        pm4g_variant_table* v = new pm4g_variant_table();
-        v->stream = s;
-        v->V = sizes[2 * i];
-        v->total_len = sizes[2 * i + 1];
-        parts[i] = v;
-        uint64_t V1 = std::max<uint64_t>(v->V, 1);
-        if ((st = dalloc_t(&v->k1, V1, s)) || (st = dalloc_t(&v->k2, V1, s)) ||
-            (st = dalloc_t(&v->count, V1, s)) || (st = dalloc_t(&v->rep_case, V1, s)) ||
-            (st = dalloc_t(&v->len, V1, s)) ||
-            (st = dalloc_t(&v->seq_act, std::max<uint64_t>(v->total_len, 1), s)))
-            break;
-        uint64_t n = std::max(v->V, v->total_len);
-        if (n) {
-            int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 1024));
-            prof_begin("k_unpack_entries", v->V * 64.0, s);
-            k_unpack_entries<<<g, 256, 0, s>>>(re + 4 * Vmax * i, v->V, ra + Tmax * i, v->total_len, *v);
-            cudaError_t e = cudaGetLastError();
-            prof_end(s);
-            count_launch();
-            if (e != cudaSuccess) st = cuda_fail(e, "k_unpack_entries");
-        }
+    if ((r = g_nccl.groupStart())) return nccl_fail(r, "ncclGroupStart");
+    for (int p = 0; p < R && !r; ++p) {
+        if (p == me) continue;
+        if (local->V) r = g_nccl.send(re + 4 * vb[me], local->V * 32, NCCL_UINT8, p, c->comm, s);
+        if (!r && local->total_len) r = g_nccl.send(ra + tb[me], local->total_len * 4, NCCL_UINT8, p, c->comm, s);
+        if (!r && sizes[2 * p]) r = g_nccl.recv(re + 4 * vb[p], sizes[2 * p] * 32, NCCL_UINT8, p, c->comm, s);
+        if (!r && sizes[2 * p + 1]) r = g_nccl.recv(ra + tb[p], sizes[2 * p + 1] * 4, NCCL_UINT8, p, c->comm, s);
     }
-    if (st == PM4G_OK) {
-        std::vector<const pm4g_variant_table*> cparts(parts.begin(), parts.end());
-        cparts[c->rank] = local;
-        st = merge_variant_tables(cparts.data(), R, s, out, c->rank);
-    }
-    for (int i = 0; i < R; ++i)
-        if (i != c->rank) free_variants(parts[i]);
-    return st;
+    const NcclResult re_end = g_nccl.groupEnd();
+    if (r) return nccl_fail(r, "ncclSend/ncclRecv(variants)");
+    if (re_end) return nccl_fail(re_end, "ncclGroupEnd");
+    MergeItems m;
+    PM4G_TRY(merge_items_alloc(V, 0, items, &m));
+    m.T = T;
+    m.sa = ra;
+    const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>((V + 255) / 256, (uint64_t)num_sms() * 8));
+    PM4G_LAUNCH("k_unpack_entries", V * 64.0, s, (k_unpack_entries<<<g, 256, 0, s>>>(re, d_sz, R, m)));
+    return merge_flat(m, local, vb[me], s, out);
 }
 
 __global__ void k_sum_parts(const uint64_t* parts, int R, uint64_t len, uint64_t* out) {

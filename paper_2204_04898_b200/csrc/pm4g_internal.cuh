@@ -458,6 +458,19 @@ pm4g_status make_ingested_log(const pm4g_log* like, int64_t n, uint32_t case_lo,
 
 pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
                                  pm4g_variant_table** out, int local_part);
+// the merge's items, flat (entries of every part, part-major; see merge_flat)
+struct MergeItems {
+    uint64_t V = 0, T = 0;
+    uint64_t* k1 = nullptr;
+    uint64_t* k2 = nullptr;
+    uint64_t* w = nullptr;     // [V] entry counts
+    uint32_t* ord = nullptr;   // [V] entry representative cases
+    uint32_t* so = nullptr;    // [V + 1] sequence offsets into sa
+    uint32_t* sa = nullptr;    // [T]
+};
+pm4g_status merge_items_alloc(uint64_t V, uint64_t T, Scratch& buf, MergeItems* m);
+pm4g_status merge_flat(const MergeItems& in, const pm4g_variant_table* lp, uint64_t lp_first, cudaStream_t s,
+                       pm4g_variant_table** out);
 void free_variants(pm4g_variant_table* v);
 
 }  // namespace pm4g

@@ -634,8 +634,9 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
 // ------------------------------------------------------------------ exclusive scan
 constexpr int SCAN_THREADS = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_THREADS * SCAN_IPT;
 
+template <class OUT>
 __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __restrict__ in,
-                                                            uint64_t* __restrict__ out, int64_t n,
+                                                            OUT* __restrict__ out, int64_t n,
                                                             st_t* status, uint32_t* counter) {
     __shared__ uint32_t s_tile, s_scan[SCAN_THREADS / 32 + 1], s_prefix;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
@@ -655,19 +656,20 @@ __global__ __launch_bounds__(SCAN_THREADS) void k_excl_scan(const uint32_t* __re
         if (threadIdx.x == 0) s_prefix = pf;
     }
     __syncthreads();
-    uint64_t r = (uint64_t)s_prefix + ex;
+    OUT r = (OUT)s_prefix + ex;
 #pragma unroll
     for (int j = 0; j < SCAN_IPT; ++j) {
         if (b + j < n) out[b + j] = r;
         r += v[j];
     }
-    if (threadIdx.x == 0 && (int64_t)(tile + 1) * SCAN_TILE >= n) out[n] = (uint64_t)s_prefix + total;
+    if (threadIdx.x == 0 && (int64_t)(tile + 1) * SCAN_TILE >= n) out[n] = (OUT)s_prefix + total;
 }
 
 // out[0..n] = exclusive prefix sums of in[0..n), out[n] = total (< 2^31)
-pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
+template <class OUT>
+static pm4g_status excl_scan_u32(const uint32_t* in, OUT* out, int64_t n, cudaStream_t s) {
     if (n == 0) {
-        PM4G_CK(cudaMemsetAsync(out, 0, 8, s));
+        PM4G_CK(cudaMemsetAsync(out, 0, sizeof(OUT), s));
         return PM4G_OK;
     }
     const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -675,9 +677,13 @@ pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, c
     PM4G_TRY(st.alloc((tiles + 1) * sizeof(st_t)));
     PM4G_CK(cudaMemsetAsync(st.p, 0, (tiles + 1) * sizeof(st_t), s));
     PM4G_LAUNCH("k_excl_scan", n * 12.0, s,
-                (k_excl_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, st.as<st_t>() + 1,
-                                                                     st.as<uint32_t>())));
+                (k_excl_scan<OUT><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, st.as<st_t>() + 1,
+                                                                          st.as<uint32_t>())));
     return PM4G_OK;
+}
+
+pm4g_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, cudaStream_t s) {
+    return excl_scan_u32<uint64_t>(in, out, n, s);
 }
 
 // ------------------------------------------------------------------ emission
@@ -702,15 +708,18 @@ __global__ void k_emit(const Groups g, const OFF* __restrict__ off, const uint32
 }
 
 // one warp per variant: copy the representative's sequence
+constexpr int SEQ_LANES = 8;
 template <class OFF, class ACT>
 __global__ void k_seq_gather(const Groups g, const OFF* __restrict__ off, const ACT* __restrict__ acts,
                              const uint64_t* __restrict__ seq_off, uint32_t* __restrict__ seq_act) {
-    const uint64_t warps = (uint64_t)gridDim.x * blockDim.x / 32;
-    for (uint64_t p = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; p < g.G; p += warps) {
+    // SEQ_LANES lanes per variant (sequences are short: more of them in flight)
+    const uint64_t teams = (uint64_t)gridDim.x * blockDim.x / SEQ_LANES;
+    const uint32_t ln = threadIdx.x & (SEQ_LANES - 1);
+    for (uint64_t p = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / SEQ_LANES; p < g.G; p += teams) {
         const uint32_t it = g.rep_item[g.sorted[p]];
         const OFF f = off[it];
         const uint64_t o = seq_off[p], L = seq_off[p + 1] - o;
-        for (uint64_t i = threadIdx.x & 31; i < L; i += 32) seq_act[o + i] = (uint32_t)acts[f + i];
+        for (uint64_t i = ln; i < L; i += SEQ_LANES) seq_act[o + i] = (uint32_t)acts[f + i];
     }
 }
 
@@ -832,10 +841,23 @@ __device__ __forceinline__ bool seq_same(const ACT* acts, uint32_t f, uint32_t r
 }
 
 // ctl: [0] overflow, [1] gids reserved (the warps' blocks), [2] collisions, [3] groups claimed
+// weight / order (nullptr: 1 / the item index): the merge of shard tables groups
+// their entries (weight = count, order = representative case code).  Weighted
+// counts stay u32: a weight or a sum past 2^32 - 1 counts as a collision (the
+// general engine then groups with u64 weights).
+__device__ __forceinline__ void vg_add_w(uint32_t* p, uint32_t w, bool checked, uint32_t* ctl) {
+    if (!checked) {
+        atomicAdd(p, w);
+    } else if (atomicAdd(p, w) > 0xffffffffu - w) {
+        atomicAdd(&ctl[2], 1u);
+    }
+}
+
 template <class ACT, int VG_IPT, int VG_GBLOCK>
 __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
     uint64_t n_items, const uint64_t* __restrict__ d_n, const uint64_t* __restrict__ k1,
     const uint64_t* __restrict__ k2, const uint32_t* __restrict__ off, const ACT* __restrict__ acts,
+    const uint64_t* __restrict__ weight, const uint32_t* __restrict__ order,
     VSlot* table, uint64_t mask, uint32_t gcap, uint32_t* __restrict__ g_w, uint32_t* __restrict__ g_rep,
     uint32_t* __restrict__ item_gid, uint32_t* ctl, unsigned long long* total_len, uint32_t* task_counter) {
     extern __shared__ __align__(16) unsigned char vg_sm[];
@@ -874,7 +896,7 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
         if (lane == 0) task = atomicAdd((unsigned long long*)task_counter, 1ull);
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task * VG_TASK >= n_items) break;
-        uint32_t f[VG_IPT], l[VG_IPT], gid[VG_IPT], cof[VG_IPT], cln[VG_IPT];
+        uint32_t f[VG_IPT], l[VG_IPT], gid[VG_IPT], cof[VG_IPT], cln[VG_IPT], wt[VG_IPT], od[VG_IPT];
         uint64_t ka[VG_IPT], kb[VG_IPT];
         int hit[VG_IPT];   // cache entry, -1: miss, -2: none (past the end / abandoned / collision)
 #pragma unroll
@@ -887,6 +909,13 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
             kb[u] = k2[t];
             f[u] = off[t];
             l[u] = off[t + 1];
+            wt[u] = 1u;
+            if (weight) {
+                const uint64_t w = weight[t];
+                wt[u] = (uint32_t)w;
+                if ((w >> 32) || !w) atomicAdd(&ctl[2], 1u);
+            }
+            od[u] = order ? order[t] : (uint32_t)t;
         }
         // A: the CTA's cache (an entry is used once its k2 is written)
 #pragma unroll
@@ -932,6 +961,7 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
                     if (probes >= mask || ((probes & 31) == 31 && ld_volatile(&ctl[0]))) {
                         atomicExch(&ctl[0], 1u);
                         sp = nullptr;
+                        m = K128{VG_NOMETA, 0};   // (m held the last probed slot's: not this key's)
                         break;
                     }
                     h = (h + 1) & mask;
@@ -989,8 +1019,8 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
             }
             item_gid[t] = gid[u];
             if (hit[u] >= 0) {
-                atomicAdd(&c_cnt[hit[u]], 1u);
-                atomicMin(&c_rep[hit[u]], t);
+                vg_add_w(&c_cnt[hit[u]], wt[u], weight != nullptr, ctl);
+                atomicMin(&c_rep[hit[u]], od[u]);
                 continue;
             }
             bool cached = false;
@@ -1002,8 +1032,8 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
                         c_gid[h] = gid[u];
                         c_off[h] = cof[u];
                         c_len[h] = cln[u];
-                        atomicAdd(&c_cnt[h], 1u);
-                        atomicMin(&c_rep[h], t);
+                        vg_add_w(&c_cnt[h], wt[u], weight != nullptr, ctl);
+                        atomicMin(&c_rep[h], od[u]);
                         __threadfence_block();
                         st_volatile(&c_k2[h], (unsigned long long)kb[u]);
                         cached = true;
@@ -1013,8 +1043,8 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
                 }
             }
             if (!cached) {
-                atomicAdd(&g_w[gid[u]], 1u);
-                atomicMin(&g_rep[gid[u]], t);
+                vg_add_w(&g_w[gid[u]], wt[u], weight != nullptr, ctl);
+                atomicMin(&g_rep[gid[u]], od[u]);
             }
         }
     }
@@ -1024,7 +1054,7 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
     // flush the cache's counts and minimum cases into the dense group arrays
     for (int i = threadIdx.x; i < VG_CACHE; i += VG_THREADS) {
         if (c_cnt[i]) {
-            atomicAdd(&g_w[c_gid[i]], c_cnt[i]);
+            vg_add_w(&g_w[c_gid[i]], c_cnt[i], weight != nullptr, ctl);
             atomicMin(&g_rep[c_gid[i]], c_rep[i]);
         }
     }
@@ -1034,13 +1064,23 @@ __global__ __launch_bounds__(VG_THREADS, PM4G_VG_MINB) void k_vgroup(
     }
 }
 
-// (the radix fallback) the groups' u64 weights and representatives as the u32
+// (the radix fallback) the groups' u64 weights and order keys as the u32
 // arrays k_vfinal reads
 __global__ void k_vrekey(const uint64_t* __restrict__ weight, const uint32_t* __restrict__ rep, uint64_t G,
                          uint32_t* __restrict__ w32, uint32_t* __restrict__ r32) {
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < G; g += (uint64_t)gridDim.x * blockDim.x) {
         w32[g] = (uint32_t)weight[g];
         r32[g] = rep[g];
+    }
+}
+
+// (weighted merge) the representative item of each group: the one holding the
+// group's minimum order (orders are unique per item)
+__global__ void k_vrepitem(const uint32_t* __restrict__ order, const uint32_t* __restrict__ item_gid,
+                           const uint32_t* __restrict__ g_rep, uint64_t n_items, uint32_t* __restrict__ rep_item) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_items; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = item_gid[t];
+        if (order[t] == g_rep[g]) rep_item[g] = (uint32_t)t;
     }
 }
 
@@ -1054,7 +1094,7 @@ __global__ void k_vfinal(const uint32_t* __restrict__ g_w, const uint32_t* __res
         const uint64_t w = g_w[g];
         const uint32_t r = g_rep[g];
         weight[g] = w;
-        rep_item[g] = r;
+        if (rep_item) rep_item[g] = r;   // nullptr: already set
         order[g] = r;
         if (!key) continue;   // small tables: ordered by k_small_variants
         // an empty (reserved, unused) gid sorts after every group
@@ -1077,8 +1117,8 @@ constexpr size_t SV_SMEM = (size_t)SV_MAX * 8 + 2 * (size_t)SV_MAX * 2 + (size_t
 
 template <class ACT>
 __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
-    const uint64_t* __restrict__ weight, const uint32_t* __restrict__ rep, uint32_t Ga, uint32_t G,
-    const uint32_t* __restrict__ off, const ACT* __restrict__ acts, const uint32_t* __restrict__ rep_code,
+    const uint64_t* __restrict__ weight, const uint32_t* __restrict__ order, const uint32_t* __restrict__ rep,
+    uint32_t Ga, uint32_t G, const uint32_t* __restrict__ off, const ACT* __restrict__ acts, const uint32_t* __restrict__ rep_code,
     const uint64_t* __restrict__ k1, const uint64_t* __restrict__ k2, uint64_t* __restrict__ count,
     uint32_t* __restrict__ len, uint32_t* __restrict__ rep_case, uint64_t* __restrict__ seq_off,
     uint32_t* __restrict__ seq_act, uint64_t* __restrict__ ok1, uint64_t* __restrict__ ok2,
@@ -1101,7 +1141,7 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
     for (uint32_t g = tid; g < Ga; g += SV_THREADS)
         if (weight[g]) {
             mw = max(mw, (unsigned long long)weight[g]);
-            mr = max(mr, rep[g]);
+            mr = max(mr, order[g]);
         }
     for (int o = 16; o; o >>= 1) {
         mw = max(mw, __shfl_xor_sync(0xffffffffu, mw, o));
@@ -1116,7 +1156,7 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
     for (uint32_t g = tid; g < Ga; g += SV_THREADS) {
         const uint64_t w = weight[g];
         // an empty (reserved, unused) gid sorts after every group
-        s_key[g] = w ? ((s_maxw - w) << rbits) | rep[g] : low_mask(bits);
+        s_key[g] = w ? ((s_maxw - w) << rbits) | order[g] : low_mask(bits);
         s_idx[g] = (uint16_t)g;
     }
     __syncthreads();
@@ -1256,7 +1296,8 @@ constexpr pm4g_status VO_NOT_LAUNCHED = (pm4g_status)100;   // internal: the coo
 
 struct VoArgs {
     const uint64_t* weight;
-    const uint32_t* rep;
+    const uint32_t* order;     // the groups' order keys (min order of their items)
+    const uint32_t* rep;       // the groups' representative items
     uint32_t Ga, G, chunk;
     const uint32_t* off;
     const uint32_t* rep_code;
@@ -1301,7 +1342,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
         for (uint32_t g = lo + tid; g < hi; g += VO_THREADS)
             if (a.weight[g]) {
                 mw = max(mw, (unsigned long long)a.weight[g]);
-                mr = max(mr, (unsigned long long)a.rep[g]);
+                mr = max(mr, (unsigned long long)a.order[g]);
             }
         for (int o = 16; o; o >>= 1) {
             mw = max(mw, __shfl_xor_sync(0xffffffffu, mw, o));
@@ -1318,7 +1359,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
     for (uint32_t g = lo + tid; g < hi; g += VO_THREADS) {
         const uint64_t w = a.weight[g];
         // an empty (reserved, unused) gid sorts after every group
-        a.key[0][g] = w ? ((maxw - w) << rbits) | a.rep[g] : low_mask(bits);
+        a.key[0][g] = w ? ((maxw - w) << rbits) | a.order[g] : low_mask(bits);
         a.val[0][g] = g;
     }
     grid.sync();
@@ -1481,7 +1522,8 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
 // in output order (sorted, inv) exactly as group_items leaves them.
 template <class ACT>
 static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const uint64_t* k2, const uint32_t* off,
-                                    const ACT* acts, int order_bits, cudaStream_t s, Groups* out,
+                                    const ACT* acts, const uint64_t* weight, const uint32_t* order, int order_bits,
+                                    cudaStream_t s, Groups* out,
                                     const uint64_t* d_n, uint64_t* n_true, bool* fallback) {
     *fallback = false;
     if (n_true) *n_true = n_items;
@@ -1498,7 +1540,10 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         return PM4G_OK;
     }
     const uint64_t full = pow2_at_least(std::max<uint64_t>(1024, 2 * n_items));
-    uint64_t cap = std::min<uint64_t>(full, std::max<uint64_t>(1ull << 19, pow2_at_least(n_items / 8)));
+    // a log's cases hold few distinct sequences; the merge's items (the shards'
+    // variants) are mostly distinct: a table that never trips its load limit
+    uint64_t cap = std::min<uint64_t>(full, weight ? pow2_at_least(n_items)
+                                                   : std::max<uint64_t>(1ull << 19, pow2_at_least(n_items / 8)));
     if (const uint64_t dc = debug_variant_cap()) cap = std::min<uint64_t>(full, pow2_at_least(std::max<uint64_t>(dc, 64)));
     uint64_t G = 0, Ga = 0, htot = 0, gcap = 0;
     Scratch gw(s);
@@ -1531,7 +1576,7 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         PM4G_LAUNCH("k_variant_init", cap * 32.0 + gcap * 8.0, s,
                     (k_vinit<<<gsz(std::max(cap, gcap)), 256, 0, s>>>(tab.as<VSlot>(), cap, g_w, g_rep, gcap)));
         PM4G_LAUNCH("k_variant_group", n_items * 36.0, s,
-                    (kern<<<grid, VG_THREADS, VG_SMEM, s>>>(n_items, d_n, k1, k2, off, acts, tab.as<VSlot>(),
+                    (kern<<<grid, VG_THREADS, VG_SMEM, s>>>(n_items, d_n, k1, k2, off, acts, weight, order, tab.as<VSlot>(),
                                                                      cap - 1, (uint32_t)gcap, g_w, g_rep,
                                                                      g.item_group, ctl, d_tot, d_task)));
         // one host round trip: overflow, gids, collisions, groups, total length (+ the case count)
@@ -1571,14 +1616,22 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
     if ((st = dalloc_t(&g.rep_item, Ga1, s))) return bail(st);
     if ((st = dalloc_t(&g.order, Ga1, s))) return bail(st);
     if ((st = dalloc_t(&g.inv, Ga1, s))) return bail(st);
-    const int wbits = std::max(1, bit_width_u64(n_items));
+    const int wbits = weight ? 32 : std::max(1, bit_width_u64(n_items));   // u32 counts
     const uint32_t* g_w = gw.as<uint32_t>();
+    // the weighted merge: the item holding each group's minimum order represents it
+    auto rep_items = [&]() -> pm4g_status {
+        if (order && Ga)
+            PM4G_LAUNCH("k_variant_rep", n_items * 12.0, s,
+                        (k_vrepitem<<<gsz(n_items), 256, 0, s>>>(order, g.item_group, g_w + gcap, n_items, g.rep_item)));
+        return PM4G_OK;
+    };
     static const uint64_t vo_max = getenv("PM4G_VO_MAX") ? strtoull(getenv("PM4G_VO_MAX"), nullptr, 10) : VO_MAX_GROUPS;
     if (Ga <= std::min(vo_max, VO_MAX_GROUPS)) {   // ordered and emitted in one launch (k_small_variants / k_vorder)
         if (Ga)
             PM4G_LAUNCH("k_variant_sortkeys", Ga * 20.0, s,
                         (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight,
                                                           g.rep_item, g.order, nullptr, nullptr)));
+        if ((st = rep_items())) return bail(st);
         *out = g;
         return PM4G_OK;
     }
@@ -1590,6 +1643,7 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
                     (k_vfinal<<<gsz(Ga), 256, 0, s>>>(g_w, g_w + gcap, Ga, wbits, order_bits, g.weight, g.rep_item,
                                                       g.order, sk.as<uint64_t>(), sk_val)));
+        if ((st = rep_items())) return bail(st);
         if (Ga <= RANK_SORT_MAX)
             PM4G_LAUNCH("k_rank_sort", Ga * 12.0, s,
                         (k_rank_sort<<<(unsigned)((Ga + 255) / 256), 256, 0, s>>>(sk.as<uint64_t>(), (uint32_t)Ga, g.sorted)));
@@ -1603,9 +1657,9 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
 
 // The one-pass table's ordering with the library radix sort (the general path;
 // used when the cooperative kernel cannot be launched): g.sorted / g.inv.
-static pm4g_status order_groups_radix(Groups& g, int order_bits, uint64_t n_items, cudaStream_t s) {
+static pm4g_status order_groups_radix(Groups& g, int order_bits, uint64_t n_items, bool weighted, cudaStream_t s) {
     const uint64_t Ga = g.Ga, Ga1 = std::max<uint64_t>(Ga, 1);
-    const int wbits = std::max(1, bit_width_u64(n_items));
+    const int wbits = weighted ? 32 : std::max(1, bit_width_u64(n_items));
     PM4G_TRY(dalloc_t(&g.sorted, Ga1, s));
     Scratch sk(s), gw(s);   // keys [Ga] | vals [Ga]; the u32 weights / reps k_vfinal reads
     PM4G_TRY(sk.alloc(Ga * 12 + 16));
@@ -1616,9 +1670,9 @@ static pm4g_status order_groups_radix(Groups& g, int order_bits, uint64_t n_item
     uint32_t* r32 = w32 + Ga;
     if (!Ga) return PM4G_OK;
     PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
-                (k_vrekey<<<gsz(Ga), 256, 0, s>>>(g.weight, g.rep_item, Ga, w32, r32)));
+                (k_vrekey<<<gsz(Ga), 256, 0, s>>>(g.weight, g.order, Ga, w32, r32)));
     PM4G_LAUNCH("k_variant_sortkeys", Ga * 28.0, s,
-                (k_vfinal<<<gsz(Ga), 256, 0, s>>>(w32, r32, Ga, wbits, order_bits, g.weight, g.rep_item, g.order,
+                (k_vfinal<<<gsz(Ga), 256, 0, s>>>(w32, r32, Ga, wbits, order_bits, g.weight, nullptr, g.order,
                                                   key, val)));
     PM4G_TRY(radix_sort_u64_to(key, val, g.sorted, (int64_t)Ga, wbits + order_bits, s));
     PM4G_LAUNCH("k_variant_inv", Ga * 8.0, s, (k_inv<<<gsz(Ga), 256, 0, s>>>(g.sorted, Ga, g.inv)));
@@ -1647,6 +1701,7 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     char* b = (char*)sc.p;
     VoArgs a{};
     a.weight = g.weight;
+    a.order = g.order;
     a.rep = g.rep_item;
     a.Ga = (uint32_t)Ga;
     a.G = (uint32_t)g.G;
@@ -1730,9 +1785,10 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
     bool general = true;
     const uint64_t* dn = d_n;
     if constexpr (sizeof(OFF) == 4) {   // a log's cases: the one-pass grouping unless it meets a collision
-        if (!weight && !order) {   // (weak debug keys collide: they exercise the fallback)
-            PM4G_TRY((group_cases_fast<ACT>(n_items, k1, k2, (const uint32_t*)off, acts, order_bits, s, &g, d_n, &nt,
-                                            &general)));
+        // (weak debug keys collide: they exercise the fallback)
+        if (!weight == !order) {
+            PM4G_TRY((group_cases_fast<ACT>(n_items, k1, k2, (const uint32_t*)off, acts, weight, order, order_bits, s,
+                                            &g, d_n, &nt, &general)));
             if (general) {   // the case count is known now
                 n_items = nt;
                 dn = nullptr;
@@ -1779,14 +1835,14 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
                 dfree(v->case_variant, s);
                 v->case_variant = nullptr;
             }
-            const pm4g_status os = order_groups_radix(g, order_bits, n_items, s);
+            const pm4g_status os = order_groups_radix(g, order_bits, n_items, weight != nullptr, s);
             if (os) return bail(os);
         }
         if (!g.sorted) {   // a small one-pass table: ordered and emitted by one CTA
             PM4G_MAX_SMEM(k_small_variants<ACT>);
             PM4G_LAUNCH("k_variant_small", g.Ga * 24.0 + g.G * 40.0 + total * 5.0, s,
                         (k_small_variants<ACT><<<1, SV_THREADS, SV_SMEM, s>>>(
-                            g.weight, g.rep_item, (uint32_t)g.Ga, (uint32_t)g.G, (const uint32_t*)off, acts, rep_code,
+                            g.weight, g.order, g.rep_item, (uint32_t)g.Ga, (uint32_t)g.G, (const uint32_t*)off, acts, rep_code,
                             k1, k2, v->count, v->len, v->rep_case, v->seq_off, v->seq_act, v->k1, v->k2, g.inv)));
             return finish_variants(g, v, n_items, with_case_variant, s, out);
         }
@@ -1798,7 +1854,7 @@ static pm4g_status build_variants(uint64_t n_items, const uint64_t* k1, const ui
     }
     if ((st = excl_scan_u32_to_u64(v->len, v->seq_off, (int64_t)g.G, s))) return bail(st);
     if (g.G) {
-        int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>((g.G * 32 + 255) / 256, (uint64_t)num_sms() * 8));
+        int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>((g.G * SEQ_LANES + 255) / 256, (uint64_t)num_sms() * 64));
         PM4G_LAUNCH("k_variant_seq", (double)total * 8.0, s,
                     (k_seq_gather<OFF, ACT><<<gs, 256, 0, s>>>(g, off, acts, v->seq_off, v->seq_act)));
     }
@@ -1837,44 +1893,20 @@ __global__ void k_compose_case_variant(const uint32_t* __restrict__ local_cv, ui
         out[c] = item_out[offset + local_cv[c]];
 }
 
-pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
-                                 pm4g_variant_table** out, int local_part) {
-    uint64_t V = 0, T = 0;
-    for (int r = 0; r < n_parts; ++r) {
-        V += parts[r]->V;
-        T += parts[r]->total_len;
-    }
-    Scratch buf(s);
-    // k1 k2 weight (u64) | order len (u32) | seq_off (u64, V+1) | seq_act (u32, T)
-    PM4G_TRY(buf.alloc((V + 1) * 8 * 4 + (V + 1) * 4 * 2 + (T + 1) * 4));
-    uint64_t* k1 = buf.as<uint64_t>();
-    uint64_t* k2 = k1 + V + 1;
-    uint64_t* w = k2 + V + 1;
-    uint64_t* so = w + V + 1;
-    uint32_t* ord = (uint32_t*)(so + V + 1);
-    uint32_t* ln = ord + V + 1;
-    uint32_t* sa = ln + V + 1;
-    uint64_t vo = 0, to = 0;
-    for (int r = 0; r < n_parts; ++r) {
-        const pm4g_variant_table* p = parts[r];
-        if (!p->V) continue;
-        PM4G_CK(cudaMemcpyAsync(k1 + vo, p->k1, p->V * 8, cudaMemcpyDeviceToDevice, s));
-        PM4G_CK(cudaMemcpyAsync(k2 + vo, p->k2, p->V * 8, cudaMemcpyDeviceToDevice, s));
-        PM4G_CK(cudaMemcpyAsync(w + vo, p->count, p->V * 8, cudaMemcpyDeviceToDevice, s));
-        PM4G_CK(cudaMemcpyAsync(ord + vo, p->rep_case, p->V * 4, cudaMemcpyDeviceToDevice, s));
-        PM4G_CK(cudaMemcpyAsync(ln + vo, p->len, p->V * 4, cudaMemcpyDeviceToDevice, s));
-        PM4G_CK(cudaMemcpyAsync(sa + to, p->seq_act, p->total_len * 4, cudaMemcpyDeviceToDevice, s));
-        vo += p->V;
-        to += p->total_len;
-    }
-    PM4G_TRY(excl_scan_u32_to_u64(ln, so, (int64_t)V, s));
-    const pm4g_variant_table* lp = local_part >= 0 ? parts[local_part] : nullptr;
+// The merge's items, flat: entry i (of every part, part-major) has keys k1/k2,
+// weight w (its count), order ord (its representative case) and sequence
+// sa[so[i], so[i + 1]).  lp (optional) is the part whose per-case index the
+// merged table carries; its entries start at item lp_first.
+pm4g_status merge_flat(const MergeItems& in, const pm4g_variant_table* lp, uint64_t lp_first, cudaStream_t s,
+                       pm4g_variant_table** out) {
+    // the entries' sequences are addressed with u32 offsets
+    if (in.V > 0xfffffffeull || in.T > (uint64_t)MAX_SHARD_EVENTS)
+        return fail(PM4G_EINVAL, "merged variant tables exceed 2^31 - 2 activities");
     const bool compose = lp && lp->case_variant && lp->n_cases;
     pm4g_variant_table* v = nullptr;
-    PM4G_TRY((build_variants<uint64_t, uint32_t>(V, k1, k2, so, sa, w, ord, 32, ord, compose, s, &v)));
+    PM4G_TRY((build_variants<uint32_t, uint32_t>(in.V, in.k1, in.k2, in.so, in.sa, in.w, in.ord, 32, in.ord, compose,
+                                                 s, &v)));
     if (compose) {   // v->case_variant holds item -> output for the V merged entries
-        uint64_t offset = 0;
-        for (int r = 0; r < local_part; ++r) offset += parts[r]->V;
         uint32_t* cv = nullptr;
         pm4g_status st = dalloc_t(&cv, std::max<uint64_t>(lp->n_cases, 1), s);
         if (st) {
@@ -1883,13 +1915,70 @@ pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_p
         }
         PM4G_LAUNCH("k_compose_case_variant", lp->n_cases * 12.0, s,
                     (k_compose_case_variant<<<gsz(lp->n_cases), 256, 0, s>>>(lp->case_variant, lp->n_cases,
-                                                                             v->case_variant, offset, cv)));
+                                                                             v->case_variant, lp_first, cv)));
         dfree(v->case_variant, s);
         v->case_variant = cv;
         v->n_cases = lp->n_cases;
     }
     *out = v;
     return PM4G_OK;
+}
+
+// one part's entries into the flat items (its sequences start at tbase)
+__global__ void k_flat_part(const pm4g_variant_table p, uint64_t tbase, MergeItems m, uint64_t vbase) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.V; i += (uint64_t)gridDim.x * blockDim.x) {
+        m.k1[vbase + i] = p.k1[i];
+        m.k2[vbase + i] = p.k2[i];
+        m.w[vbase + i] = p.count[i];
+        m.ord[vbase + i] = p.rep_case[i];
+        m.so[vbase + i] = (uint32_t)(tbase + p.seq_off[i]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && vbase + p.V == m.V) m.so[m.V] = (uint32_t)m.T;
+}
+
+pm4g_status merge_items_alloc(uint64_t V, uint64_t T, Scratch& buf, MergeItems* m) {
+    // k1 k2 w (u64, V) | so (u32, V + 1) | ord (u32, V) | sa (u32, T)
+    PM4G_TRY(buf.alloc(V * 24 + 16 + (V + 1) * 4 + V * 4 + 16 + (T + 1) * 4));
+    m->V = V;
+    m->T = T;
+    m->k1 = buf.as<uint64_t>();
+    m->k2 = m->k1 + V;
+    m->w = m->k2 + V;
+    m->so = (uint32_t*)(m->w + V);
+    m->ord = m->so + V + 1;
+    m->sa = (uint32_t*)(((uintptr_t)(m->ord + V) + 15) & ~(uintptr_t)15);
+    return PM4G_OK;
+}
+
+// Merge R per-shard tables (disjoint case ranges): items = entries.  With
+// local_part >= 0, the merged table also carries the case -> variant index of
+// that part's cases: its local index composed with the merged position of the
+// part's entries (the merge groups entries, so entry i of part r lands at
+// item_out[offset_r + i]).
+pm4g_status merge_variant_tables(const pm4g_variant_table* const* parts, int n_parts, cudaStream_t s,
+                                 pm4g_variant_table** out, int local_part) {
+    uint64_t V = 0, T = 0;
+    for (int r = 0; r < n_parts; ++r) {
+        V += parts[r]->V;
+        T += parts[r]->total_len;
+    }
+    if (V > 0xfffffffeull || T > (uint64_t)MAX_SHARD_EVENTS)
+        return fail(PM4G_EINVAL, "merged variant tables exceed 2^31 - 2 activities");
+    Scratch buf(s);
+    MergeItems m;
+    PM4G_TRY(merge_items_alloc(V, T, buf, &m));
+    uint64_t vo = 0, to = 0, lp_first = 0;
+    for (int r = 0; r < n_parts; ++r) {
+        const pm4g_variant_table* p = parts[r];
+        if (r == local_part) lp_first = vo;
+        if (!p->V) continue;
+        PM4G_LAUNCH("k_merge_flat", p->V * 64.0, s, (k_flat_part<<<gsz(p->V), 256, 0, s>>>(*p, to, m, vo)));
+        PM4G_CK(cudaMemcpyAsync(m.sa + to, p->seq_act, p->total_len * 4, cudaMemcpyDeviceToDevice, s));
+        vo += p->V;
+        to += p->total_len;
+    }
+    if (!V) PM4G_CK(cudaMemsetAsync(m.so, 0, 4, s));   // (else the last part's k_flat_part writes so[V] = T)
+    return merge_flat(m, local_part >= 0 ? parts[local_part] : nullptr, lp_first, s, out);
 }
 
 }  // namespace pm4g

@@ -77,6 +77,25 @@ def test_weak_hash_cross_shard_merge(monkeypatch):
     assert merged.as_dict() == full.variants()
 
 
+@pytest.mark.parametrize("env", [("PM4G_DEBUG_NO_COOP", "1"), ("PM4G_DEBUG_VARIANT_CAP", "64")])
+def test_merge_one_pass_fallbacks(monkeypatch, env):
+    """The merge's one-pass grouping (weighted items, order = representative case)
+    through its other exits: the radix ordering when the cooperative grid is
+    refused, and the table regrowth after an overflow."""
+    monkeypatch.setenv(*env)
+    spec = CONFIGS["bpic2019"]
+    L = generate(spec)
+    full = oracle.run(L.case.numpy(), L.act.numpy(), L.ts.numpy(), spec.n_activities)
+    logs = [_shard_log(spec, lo, hi) for lo, hi in shard_ranges(spec.n_cases, 3)]
+    parts = [lg.variants() for lg in logs]
+    assert pm4g.pm4g_variants_merge(parts).as_dict() == full.variants()
+    mr = pm4g.pm4g_variants_merge(parts, local_part=1)
+    lo, hi = shard_ranges(spec.n_cases, 3)[1]
+    cv = mr.case_index(logs[1].info().n_cases).cpu().numpy()
+    sel = (full.case_code >= lo) & (full.case_code < hi)
+    assert np.array_equal(cv, full.case_variant[sel])
+
+
 def test_world_one_communicator_path():
     """comm != NULL with nranks = 1 runs the comm code path (no NCCL) and agrees."""
     spec = CONFIGS["tiny"]
