@@ -26,7 +26,14 @@ import sys
 
 import pytest
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pytestmark = [
+    pytest.mark.gpu, pytest.mark.slow,
+    # opt-in: the GPU pool this repo is tested on has closed compute-sanitizer
+    # (runs under it left GPUs needing a reset), so the default GPU suite skips
+    # these; PM4G_SANITIZER=1 runs them where the tool is allowed
+    pytest.mark.skipif(os.environ.get("PM4G_SANITIZER") != "1",
+                       reason="compute-sanitizer runs are opt-in (PM4G_SANITIZER=1)"),
+]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
@@ -45,6 +52,8 @@ def _run(tool, extra):
     env = dict(os.environ, PYTORCH_NO_CUDA_MEMORY_CACHING="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, env=env, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "sanitize_run ok" in out, out[-6000:]
     return out
 
