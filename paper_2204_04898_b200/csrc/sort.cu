@@ -43,6 +43,9 @@ constexpr int RADIX = 256;
 #ifndef PM4G_SORT_IPT
 #define PM4G_SORT_IPT 8
 #endif
+#ifndef PM4G_RANK_OR   // radix ranking peers: 1 = shared-memory atomicOr masks, 0 = 8 ballots
+#define PM4G_RANK_OR 1
+#endif
 #ifndef PM4G_SORT_MINB
 #define PM4G_SORT_MINB 2
 #endif
@@ -193,14 +196,14 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
     };
 
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
-    // Peers (lanes holding the same digit) from one ballot per digit bit.
     // dp[j] = digit << 16 | rank of the key among its warp's keys of that digit.
     uint64_t k[SORT_IPT];
-    uint32_t dp[SORT_IPT];   // 0xffffffff: a row dropped by the time filter (tf)
+    uint32_t dp[SORT_IPT];   // the digit, then digit << 16 | rank; 0xffffffff: a row dropped by the time filter (tf)
     const uint32_t lt = lanemask_lt();
     constexpr bool tf = FROM_COLS && TF;   // a time-filtered pass 0 (a separate instantiation)
+    uint32_t okm = 0;                      // bit j: row j is kept (tf)
 #pragma unroll
-    for (int j = 0; j < SORT_IPT; ++j) {
+    for (int j = 0; j < SORT_IPT; ++j) {   // the warp's rows -> registers
         const uint32_t li = warp * (32 * SORT_IPT) + j * 32 + lane;
         uint32_t d = dmask;
         k[j] = ~0ull;
@@ -223,10 +226,39 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
                 d = digit(k[j]);
             }
         }
+        dp[j] = d;
+        if (!tf || ok) okm |= 1u << j;
+    }
+#if PM4G_RANK_OR
+    // Peers (lanes holding the same digit) from one shared-memory atomicOr of
+    // the lane's bit into its digit's word of a warp-private mask table, read
+    // back after the warp's ORs; the group's leader clears the word for the
+    // next key.  The table (RADIX words) overlays the warp's own key rows
+    // (2 KB), whose values are in registers now and which are next written by
+    // the permutation after the block barrier.  (8 ballots per key cost ~30
+    // more instructions; MATCH.ANY is slower still, tools/mbench_peers.cu.)
+    static_assert(SORT_IPT * 32 * 8 >= RADIX * 4, "the mask table must fit the warp's key rows");
+    uint32_t* wmask = (uint32_t*)(u_key + warp * (32 * SORT_IPT));
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < RADIX / 128; ++q) ((uint4*)wmask)[lane + 32 * q] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+#endif
+#pragma unroll
+    for (int j = 0; j < SORT_IPT; ++j) {
+        const uint32_t d = dp[j];
+        const bool ok = (okm >> j) & 1u;
+        uint32_t peers;
+#if PM4G_RANK_OR
+        if (ok) atomicOr(&wmask[d], 1u << lane);
+        __syncwarp();
+        peers = ok ? wmask[d] : 0u;
+        __syncwarp();
+#else
         // peers = AND over digit bits of (ballot of lanes with the bit == my bit):
         // the bit tested against a constant mask is the ballot predicate, and
         // its sign-extended copy (0 or ~0) folds the choice into one 3-input op
-        uint32_t peers = 0xffffffffu;
+        peers = 0xffffffffu;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {   // bits above a.bits are 0 in every lane: no-ops
             uint32_t bal, m;   // ballot of the bit, and the bit as 0 / ~0, from one predicate
@@ -237,14 +269,18 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
             peers &= ~(bal ^ m);
         }
         if (tf) peers &= __ballot_sync(0xffffffffu, ok);   // dropped rows are nobody's peers
-        const int leader = tf ? ((__ffs(peers) - 1) & 31) : __ffs(peers) - 1;   // (a dropped lane may have no peers)
+#endif
+        const int leader = (__ffs(peers) - 1) & 31;   // (a dropped lane has no peers)
         uint32_t bse = 0;
-        if (lane == leader && (!tf || ok)) {
+        if (lane == leader && ok) {
             bse = s_whist[warp][d];
             s_whist[warp][d] = bse + __popc(peers);
+#if PM4G_RANK_OR
+            wmask[d] = 0u;
+#endif
         }
         bse = __shfl_sync(0xffffffffu, bse, leader);
-        dp[j] = (tf && !ok) ? 0xffffffffu : (d << 16) | (bse + __popc(peers & lt));
+        dp[j] = !ok ? 0xffffffffu : (d << 16) | (bse + __popc(peers & lt));
         __syncwarp();
     }
     __syncthreads();   // every key is in registers: u_key may be overwritten
