@@ -42,7 +42,15 @@ constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
-constexpr int AGG_CONSUMERS = 256;     // 8 consumer warps; + 1 producer warp
+#ifndef PM4G_AGG_CONS
+#define PM4G_AGG_CONS 512
+#endif
+// 16 consumer warps + 1 producer warp: the kernel is latency-bound at two
+// CTAs per SM (smem), so more warps per CTA hide more of it (sweep, one B200:
+// 8 / 12 / 16 / 24 consumer warps -> 100M 0.516 / 0.498 / 0.498 / 0.572 ms,
+// 1B/8 shard TAB_HASH 0.796 / 0.734 / 0.667 / 0.687 ms)
+constexpr int AGG_CONSUMERS = PM4G_AGG_CONS;
+static_assert(AGG_CONSUMERS >= AGG_CASES, "one consumer thread per case of a tile");
 constexpr int AGG_BLOCK = AGG_CONSUMERS + 32;
 
 enum { TAB_FULL = 1, TAB_HASH = 2 };

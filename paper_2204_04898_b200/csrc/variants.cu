@@ -1319,7 +1319,13 @@ struct VoArgs {
     uint32_t* hist;            // [gridDim.x][256]
     uint32_t* tot;             // [max(gridDim.x, 256)]: digit totals, then chunk length totals
     unsigned long long* mx;    // [2]: max weight, max rep (zeroed)
+    unsigned long long* trace; // debug (PM4G_VO_TRACE): CTA 0's %globaltimer at each phase
 };
+__device__ __forceinline__ unsigned long long vo_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <class ACT>
 __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __restrict__ acts) {
@@ -1336,6 +1342,9 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
     const uint32_t c = blockIdx.x, nc = gridDim.x;
     const uint32_t lo = min(a.Ga, c * a.chunk), hi = min(a.Ga, lo + a.chunk), cn = hi - lo;
     const uint32_t lt = lanemask_lt();
+    int ntr = 0;
+    auto mark = [&]() { if (a.trace && c == 0 && tid == 0) a.trace[ntr++] = vo_now(); };
+    mark();
     // 1. key bits from the largest weight and representative
     {
         unsigned long long mw = 0, mr = 0;
@@ -1354,6 +1363,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
         }
     }
     grid.sync();
+    mark();
     const unsigned long long maxw = ld_volatile(&a.mx[0]), maxr = ld_volatile(&a.mx[1]);
     const int rbits = max(1, bit_width_u64(maxr)), bits = rbits + max(1, bit_width_u64(maxw));
     for (uint32_t g = lo + tid; g < hi; g += VO_THREADS) {
@@ -1363,6 +1373,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
         a.val[0][g] = g;
     }
     grid.sync();
+    mark();
     // 2. LSD passes, 8 bits each
     int cur = 0;
     for (int shift = 0; shift < bits; shift += 8) {
@@ -1416,6 +1427,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
         }
         uint32_t tot = 0, pre = 0;
         grid.sync();
+        mark();
         // digit base: every chunk's counts of smaller digits, plus earlier chunks' of
         // this digit.  Each CTA reads the whole [nc][256] matrix (rows coalesced;
         // thread t sums digit t & 255 over half t >> 8 of the chunks), so no
@@ -1456,6 +1468,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
             oval[pos] = vv[j];
         }
         grid.sync();
+        mark();
         cur ^= 1;
     }
     // 3. emission of this chunk's output positions [lo, hi)
@@ -1489,6 +1502,7 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
     }
     if (tid == 0) a.tot[c] = ctot;
     grid.sync();
+    mark();
     if (tid == 0) {
         unsigned long long pr = 0;
         for (uint32_t q = 0; q < c; ++q) pr += a.tot[q];
@@ -1515,6 +1529,9 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
         for (uint64_t q = (uint64_t)c * VO_THREADS + tid; q < a.n_items; q += (uint64_t)nc * VO_THREADS)
             a.case_variant[q] = a.inv[a.item_group[q]];
     }
+    __syncthreads();
+    mark();
+    if (a.trace && c == 0 && tid == 0) a.trace[63] = ntr;
 }
 
 // The one-pass grouping of a log's cases.  *fallback = true when the general
@@ -1694,7 +1711,7 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     uint64_t nc = std::min<uint64_t>(maxc, std::max<uint64_t>((Ga + PM4G_VO_TARGET - 1) / PM4G_VO_TARGET, 1));
     nc = std::max<uint64_t>(nc, (Ga + VO_CHUNK - 1) / VO_CHUNK);
     nc = std::min<uint64_t>(nc, 2 * VO_THREADS);
-    if (nc > maxc || nc * VO_CHUNK < Ga) return fail(PM4G_ECUDA, "variant table too large for the cooperative ordering");
+    if (nc > maxc || nc * VO_CHUNK < Ga) return VO_NOT_LAUNCHED;   // more groups than co-resident chunks hold: radix passes
     Scratch sc(s);
     const size_t kb = ((Ga * 8 + 15) & ~(size_t)15), vb = ((Ga * 4 + 15) & ~(size_t)15);
     PM4G_TRY(sc.alloc(2 * kb + 2 * vb + nc * 256 * 4 + std::max<uint64_t>(nc, 256) * 4 + 64));
@@ -1732,6 +1749,10 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     if (with_case_variant) PM4G_TRY(dalloc_t(&v->case_variant, std::max<uint64_t>(n_items, 1), s));
     if (cv_inside) a.case_variant = v->case_variant;
     PM4G_CK(cudaMemsetAsync(a.mx, 0, 16, s));
+    static const bool trace = getenv("PM4G_VO_TRACE") != nullptr;
+    static unsigned long long* d_trace = nullptr;
+    if (trace && !d_trace) PM4G_CK(cudaMalloc(&d_trace, 64 * 8));
+    a.trace = trace ? d_trace : nullptr;
     void* args[] = {(void*)&a, (void*)&acts};
     // a cooperative grid can be refused (e.g. too large while other work holds the
     // device, or under a tool): the caller then orders the table with the radix passes
@@ -1746,6 +1767,14 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
         return VO_NOT_LAUNCHED;
     }
     count_launch();
+    if (trace) {
+        unsigned long long h[64];
+        PM4G_CK(cudaMemcpyAsync(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost, s));
+        PM4G_CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "k_vorder G=%llu Ga=%llu nc=%llu chunk=%u phases(us):", (unsigned long long)g.G, (unsigned long long)Ga, (unsigned long long)nc, a.chunk);
+        for (unsigned i = 1; i < h[63] && i < 63; ++i) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1e3);
+        fprintf(stderr, "\n");
+    }
     if (with_case_variant && !cv_inside && n_items)
         PM4G_LAUNCH("k_case_variant", n_items * 8.0, s,
                     (k_case_variant<<<gsz(n_items), 256, 0, s>>>(g.item_group, g.inv, n_items, v->case_variant)));
