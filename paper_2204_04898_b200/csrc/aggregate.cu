@@ -42,33 +42,32 @@ constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
-#ifndef PM4G_AGG_CONS
-#define PM4G_AGG_CONS 512
+#ifndef PM4G_AGG_FCONS
+#define PM4G_AGG_FCONS 512
 #endif
-// 16 consumer warps + 1 producer warp: the kernel is latency-bound at two
-// CTAs per SM (smem), so more warps per CTA hide more of it (sweep, one B200:
-// 8 / 12 / 16 / 24 consumer warps -> 100M 0.516 / 0.498 / 0.498 / 0.572 ms,
-// 1B/8 shard TAB_HASH 0.796 / 0.734 / 0.667 / 0.687 ms)
-constexpr int AGG_CONSUMERS = PM4G_AGG_CONS;
-static_assert(AGG_CONSUMERS >= AGG_CASES, "one consumer thread per case of a tile");
-constexpr int AGG_BLOCK = AGG_CONSUMERS + 32;
+#ifndef PM4G_AGG_HCONS
+#define PM4G_AGG_HCONS 992
+#endif
 
 enum { TAB_FULL = 1, TAB_HASH = 2 };
 
-// Stage geometry per table mode (measured): the dense table leaves room for a
-// second CTA per SM with 3 stages of 2048 rows (0.68 -> 0.53 ms at 100M); the
-// hash table takes 4096 slots and 2 stages of 2048 rows, so two CTAs share an
-// SM too (1B/8 shard, A = 256, ~1,000 distinct edges: 8192 slots + 2 x 4096
-// rows, one CTA per SM, 0.97 ms -> 0.80 ms; 2048 slots 0.86, 1024 rows x 4
-// stages 1.12).  The PM4G_AGG_H* macros are the sweep's knobs.
+// Geometry per table mode (measured on one B200; the kernel is latency-bound,
+// so the number of warps in flight decides).  TAB_FULL: 16 consumer warps,
+// 3 stages of 2048 rows, two CTAs per SM (100M, A = 64: 8 / 12 / 16 / 24
+// consumer warps 0.516 / 0.498 / 0.498 / 0.572 ms; 4 stages 0.73, 2 x 4096
+// 0.51).  TAB_HASH: 31 consumer warps, 8192 slots, 2 stages of 4096 rows, one
+// CTA per SM (1B/8 shard, A = 256, ~1,000 distinct edges: 0.597 ms; the same
+// with 23 warps 0.603; 16 warps + 4096 slots + 2 x 2048 rows at two CTAs per
+// SM 0.667, with 8 warps 0.796; 3 stages or 1024-row stages slower).  The
+// PM4G_AGG_* macros are the sweep's knobs.
 #ifndef PM4G_AGG_HROWS
-#define PM4G_AGG_HROWS 2048
+#define PM4G_AGG_HROWS 4096
 #endif
 #ifndef PM4G_AGG_HSTAGES
 #define PM4G_AGG_HSTAGES 2
 #endif
 #ifndef PM4G_AGG_HSLOTS
-#define PM4G_AGG_HSLOTS 4096
+#define PM4G_AGG_HSLOTS 8192
 #endif
 #ifndef PM4G_AGG_FROWS
 #define PM4G_AGG_FROWS 2048
@@ -80,6 +79,9 @@ template <int MODE>
 struct AggGeom {
     static constexpr uint32_t ROWS = MODE == TAB_FULL ? PM4G_AGG_FROWS : PM4G_AGG_HROWS;   // rows of a staged case tile
     static constexpr int STAGES = MODE == TAB_FULL ? PM4G_AGG_FSTAGES : PM4G_AGG_HSTAGES;
+    static constexpr int CONS = MODE == TAB_FULL ? PM4G_AGG_FCONS : PM4G_AGG_HCONS;       // consumer threads
+    static constexpr int BLOCK = CONS + 32;                                                 // + 1 producer warp
+    static_assert(CONS >= AGG_CASES, "one consumer thread per case of a tile");
 };
 
 // One pipeline stage: the tile's case offsets and its rows (keys, activities).
@@ -137,7 +139,7 @@ __device__ __forceinline__ void smem_acc(uint32_t* cnt, uint32_t* lo, uint32_t* 
 
 // WIDE: the log's key is ts - ts_min alone; a row's case is rcase[row]
 template <class P, int MODE, bool MM, bool WIDE = false>
-__global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
+__global__ __launch_bounds__(AggGeom<MODE>::BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
     uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
@@ -145,6 +147,7 @@ __global__ __launch_bounds__(AGG_BLOCK) void k_aggregate(
     uint32_t* __restrict__ cco, uint32_t case_min, const uint32_t* __restrict__ rcase) {
     constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
     constexpr int AGG_STAGES = AggGeom<MODE>::STAGES;
+    constexpr int AGG_CONSUMERS = AggGeom<MODE>::CONS, AGG_BLOCK = AggGeom<MODE>::BLOCK;
     using Stage = AggStage<P, AGG_STAGE>;
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
@@ -376,13 +379,18 @@ static pm4g_status launch_agg_w(const pm4g_log* L, const AggOut& o, cudaStream_t
     const double mean_len = (double)L->n / (double)std::max<uint64_t>(cap, 1);
     const uint32_t cpt = (uint32_t)std::max(32.0, std::min((double)AGG_CASES, 0.7 * AGG_STAGE / std::max(mean_len, 1.0)));
     const uint64_t tiles = std::max<uint64_t>(1, (cap + cpt - 1) / cpt);
-    const int per_sm = std::max(1, (int)std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
+    static int per_sm_c[2] = {-1, -1};   // smem depends only on whether tables are requested
+    int& per_sm = per_sm_c[o.tables ? 1 : 0];
+    if (per_sm < 0)
+        PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aggregate<P, MODE, MM, WIDE>,
+                                                              AggGeom<MODE>::BLOCK, smem));
+    per_sm = std::max(per_sm, 1);
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
     const double bytes = (double)L->n * (8 + sizeof(P) + (WIDE ? 4 : 0)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
                          (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0) + (o.case_code ? cap * 4.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, MODE, MM, WIDE><<<(unsigned)grid, AGG_BLOCK, smem, s>>>(
+                (k_aggregate<P, MODE, MM, WIDE><<<(unsigned)grid, AggGeom<MODE>::BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
                     o.tables ? o.packed : nullptr, o.mm, o.n_events, o.dur, o.k1, o.k2,
                     debug_weak_hash() ? 1 : 0, o.case_code, L->case_min, L->rcase)));

@@ -469,3 +469,22 @@ def test_variant_ordering_radix_fallback(monkeypatch, name):
     c, a, t = L.case.numpy(), L.act.numpy(), L.ts.numpy()
     assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True),
                   oracle.run(c, a, t, L.n_activities))
+
+
+def test_variant_table_past_cooperative_capacity():
+    """A table with more groups than the cooperative ordering's co-resident
+    chunks hold (one CTA per SM x 4096 groups) takes the radix ordering instead
+    of failing: 800k cases of 4-6 random activities out of 64, nearly all
+    distinct variants (R11 order, every output vs the oracle)."""
+    rng = np.random.default_rng(7)
+    C = 800_000
+    m = rng.integers(4, 7, size=C)
+    case = np.repeat(np.arange(C, dtype=np.int64), m)
+    n = case.size
+    act = rng.integers(0, 64, size=n)
+    ts = rng.integers(0, 1 << 40, size=n)
+    perm = rng.permutation(n)
+    case, act, ts = case[perm], act[perm], ts[perm]
+    r = oracle.run(case, act, ts, 64)
+    assert len(r.v_count) > 148 * 4096   # past a one-CTA-per-SM cooperative grid
+    assert_parity(gpu_run(case, act, ts, 64, n_case_codes=C, sort_analyze=True), r)
