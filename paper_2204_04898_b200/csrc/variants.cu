@@ -1288,7 +1288,7 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
 // histogram, scan, 5-6 radix passes, inverse, emit, scan, gather, case index)
 // whose latency dominated at these sizes.
 constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = 8, VO_CHUNK = VO_THREADS * VO_IPT;
-constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs
+constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs (order_medium checks the real occupancy)
 constexpr pm4g_status VO_NOT_LAUNCHED = (pm4g_status)100;   // internal: the cooperative grid was refused
 #ifndef PM4G_VO_TARGET
 #define PM4G_VO_TARGET 256   // groups per chunk aimed at (more CTAs, but each reads every chunk's histogram)
@@ -1514,14 +1514,31 @@ __global__ __launch_bounds__(VO_THREADS) void k_vorder(VoArgs a, const ACT* __re
     for (uint32_t li = tid; li < creal; li += VO_THREADS) a.seq_off[lo + li] = pre + s_ex[li];
     if (creal && lo + creal == a.G && tid == 0) a.seq_off[a.G] = pre + ctot;
     if (a.G == 0 && c == 0 && tid == 0) a.seq_off[0] = 0;
-    // the chunk's sequences, flattened (binary search over the in-chunk prefix)
-    for (uint32_t i = tid; i < ctot; i += VO_THREADS) {
-        uint32_t l = 0, h = creal;
-        while (h - l > 1) {
-            const uint32_t m = (l + h) >> 1;
-            if (s_ex[m] <= i) l = m; else h = m;
+    // the chunk's sequences, flattened: thread t writes output elements
+    // [t E, (t + 1) E) of the chunk -- one binary search for its first element's
+    // variant, then a walk across the variant boundaries (work balanced whatever
+    // the lengths; a search per element cost 2x at 100M)
+    {
+        const uint32_t E = (ctot + VO_THREADS - 1) / VO_THREADS;
+        const uint32_t i0 = min(ctot, tid * E), i1 = min(ctot, i0 + E);
+        if (i0 < i1) {
+            uint32_t l = 0, h = creal;
+            while (h - l > 1) {
+                const uint32_t m = (l + h) >> 1;
+                if (s_ex[m] <= i0) l = m; else h = m;
+            }
+            uint32_t nxt = l + 1 < creal ? s_ex[l + 1] : ctot;
+            uint32_t src = s_f[l] + (i0 - s_ex[l]);
+            uint32_t* dst = a.seq_act + pre;
+            for (uint32_t i = i0; i < i1; ++i) {
+                while (i == nxt) {   // next variant (every length >= 1)
+                    ++l;
+                    src = s_f[l];
+                    nxt = l + 1 < creal ? s_ex[l + 1] : ctot;
+                }
+                dst[i] = (uint32_t)acts[src++];
+            }
         }
-        a.seq_act[pre + i] = (uint32_t)acts[s_f[l] + (i - s_ex[l])];
     }
     // 4. every case's variant index (inv complete after the barrier)
     if (a.case_variant) {
@@ -1708,10 +1725,15 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
         PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vorder<ACT>, VO_THREADS, dyn));
     const uint64_t Ga = g.Ga;
     const uint64_t maxc = (uint64_t)std::max(per_sm, 1) * num_sms();
-    uint64_t nc = std::min<uint64_t>(maxc, std::max<uint64_t>((Ga + PM4G_VO_TARGET - 1) / PM4G_VO_TARGET, 1));
+    // one chunk per SM at most, unless the table needs more (every CTA reads every
+    // chunk's histogram per pass: 296 chunks of a 300k table cost 15 us more than 148)
+    uint64_t nc = std::min<uint64_t>((uint64_t)num_sms(), std::max<uint64_t>((Ga + PM4G_VO_TARGET - 1) / PM4G_VO_TARGET, 1));
     nc = std::max<uint64_t>(nc, (Ga + VO_CHUNK - 1) / VO_CHUNK);
     nc = std::min<uint64_t>(nc, 2 * VO_THREADS);
-    if (nc > maxc || nc * VO_CHUNK < Ga) return VO_NOT_LAUNCHED;   // more groups than co-resident chunks hold: radix passes
+    if (nc > maxc || nc * VO_CHUNK < Ga) {   // more groups than co-resident chunks hold: radix passes
+        if (getenv("PM4G_VO_TRACE")) fprintf(stderr, "k_vorder: Ga=%llu past capacity\n", (unsigned long long)Ga);
+        return VO_NOT_LAUNCHED;
+    }
     Scratch sc(s);
     const size_t kb = ((Ga * 8 + 15) & ~(size_t)15), vb = ((Ga * 4 + 15) & ~(size_t)15);
     PM4G_TRY(sc.alloc(2 * kb + 2 * vb + nc * 256 * 4 + std::max<uint64_t>(nc, 256) * 4 + 64));
@@ -1764,6 +1786,9 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     prof_end(s);
     if (le != cudaSuccess) {
         cudaGetLastError();
+        if (trace)
+            fprintf(stderr, "k_vorder not launched (%s): G=%llu Ga=%llu nc=%llu per_sm=%d\n", cudaGetErrorString(le),
+                    (unsigned long long)g.G, (unsigned long long)Ga, (unsigned long long)nc, per_sm);
         return VO_NOT_LAUNCHED;
     }
     count_launch();
