@@ -818,7 +818,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     uint32_t* s_idx = (uint32_t*)(((uintptr_t)(s_act + FMT_BUF) + 15) & ~(uintptr_t)15);  // WI only
     uint32_t* s_c = s_idx + FMT_BUF;                                                      // WIDE: case of each row
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
-    __shared__ uint32_t s_prefix, s_nbig, s_bigh[16], s_ntie;
+    __shared__ uint32_t s_prefix, s_nbig, s_bigh[16], s_ntie, s_anywide;
     __shared__ uint16_t s_tie[FMT_TIES];   // slots starting a group of equal keys
     __shared__ int s_ext, s_wlast[FMT_THREADS / 32];
     __shared__ __align__(8) uint64_t s_bar;
@@ -921,12 +921,19 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             const uint32_t b = ball[j];
             const uint32_t incl = r + __popc(b & (lt | (1u << lane)));   // heads at positions <= li
             if (b & (1u << lane)) s_head[incl - 1] = (uint16_t)li;
-            if (li < tn) s_ci[li] = incl ? (uint16_t)(incl - 1) : (uint16_t)0xffff;  // 0xffff: previous tile's case
+            if (li < tn) {
+                s_ci[li] = incl ? (uint16_t)(incl - 1) : (uint16_t)0xffff;  // 0xffff: previous tile's case
+                s_perm[li] = (uint16_t)0xffff;                                // slots start empty
+            }
             r += __popc(b);
         }
     }
     if (tid < 16) s_bigh[tid] = 0;
-    if (tid == 0) s_nbig = 0;
+    if (tid == 0) {
+        s_nbig = 0;
+        s_anywide = 0;
+        s_ntie = 0;
+    }
     for (uint32_t h = tid; h < H; h += FMT_THREADS) s_wide[h] = 0;
     __syncthreads();
 
@@ -975,61 +982,73 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
             if (WI) s_idx[p] = a.gidx[i];
             if (WIDE) s_c[p] = a.case_col[s_idx[p]] - a.case_min;
             s_ci[p] = (uint16_t)(H - 1);
+            s_perm[p] = (uint16_t)0xffff;
         }
         wsync();
 
-        // ---- 4a. narrow cases: every key within +-2^30 of the case's first key,
-        // so any two keys of the case differ by < 2^31 and a comparison is the
-        // sign of their 32-bit low-word difference (exact, modular).  Slots
-        // (= output positions, the case's own row range) start empty (0xffff);
-        // rows of a fallback case mark theirs 0xfffe.
-        for (int p = h0 + wt; p < oend; p += NW) {
-            const uint32_t h = s_ci[p];
-            const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
-            const bool big = e0 - s0 > FMT_WARP_MAX;   // long case: exact fallback
-            s_perm[p] = big ? (uint16_t)0xfffe : (uint16_t)0xffff;
-            if (big && p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
-            const int64_t d = (int64_t)(s_key[p] - s_key[s0]);
-            if (d < -(1ll << 30) || d >= (1ll << 30)) s_wide[h] = 1;
-        }
-        if (wt == 0) s_ntie = 0;
-        wsync();
-
-        // ---- 4. rank each row inside its case and claim slot s0 + rank.
-        // Narrow cases: rank = #(key_j < key_p), one 32-bit subtract + sign per
+        // ---- 4. rank each row inside its case and claim slot s0 + rank (slots
+        // = output positions, the case's own row range; they start empty).
+        // Narrow cases (every key within +-2^30 of the case's first key, so any
+        // two keys differ by < 2^31): rank = #(key_j < key_p), the sign of the
+        // 32-bit low-word difference (exact, modular), one subtract + sign per
         // element; rows with equal keys (ties) claim the same slot, leaving
         // empty slots behind it, and phase 5 lays the tied rows out in ingest
-        // order.  Wide cases: the exact stable rank #(key_j < key_p) + #(j < p
-        // with key_j == key_p) (unique slots).  Event-parallel with one loop per
-        // case (a warp mostly reads one case -> broadcast smem reads).
+        // order.  Every case is ranked narrow first while each row checks its
+        // own key against the case's first; a case found wide (rare: a case
+        // spanning > 2^30 key units) is re-ranked below with the exact stable
+        // rank.  Rows of a fallback case (> FMT_WARP_MAX rows) mark their own
+        // slot 0xfffe.  Event-parallel with one loop per case (a warp mostly
+        // reads one case -> broadcast smem reads).
         for (int p = h0 + wt; p < oend; p += NW) {
             const uint32_t h = s_ci[p];
             const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
-            if (e0 - s0 > FMT_WARP_MAX) continue;
-            int r = 0;
-            const uint64_t ki = s_key[p], ki1 = ki + 1;
-            if (!s_wide[h]) {
-                const uint32_t* lo = (const uint32_t*)(s_key + s0);   // low word of key s0 + j at lo[2 j]
-                const uint32_t ti = (uint32_t)ki;
-                const int m = e0 - s0;
-                // four elements per trip, the < 4 left over predicated (no
-                // remainder loops: lanes of one warp have different m)
-                int j = 0;
-#pragma unroll 1
-                for (; j + 4 <= m; j += 4)
-                    r += (int)(((lo[2 * j] - ti) >> 31) + ((lo[2 * j + 2] - ti) >> 31) +
-                               ((lo[2 * j + 4] - ti) >> 31) + ((lo[2 * j + 6] - ti) >> 31));
-                if (j < m) r += (int)((lo[2 * j] - ti) >> 31);
-                if (j + 1 < m) r += (int)((lo[2 * j + 2] - ti) >> 31);
-                if (j + 2 < m) r += (int)((lo[2 * j + 4] - ti) >> 31);
-            } else if (ki1 != 0) {   // the all-ones key (key_bits = 64) has no successor
-                for (int j = s0; j < e0; ++j) r += s_key[j] < (j < p ? ki1 : ki);
-            } else {
-                for (int j = s0; j < e0; ++j) r += (s_key[j] < ki) | ((s_key[j] == ki) & (j < p));
+            if (e0 - s0 > FMT_WARP_MAX) {   // long case: exact fallback
+                s_perm[p] = (uint16_t)0xfffe;
+                if (p == s0) s_bigh[atomicAdd(&s_nbig, 1u) & 15] = h;
+                continue;
             }
-            s_perm[s0 + r] = (uint16_t)p;
+            int r = 0;
+            const uint64_t ki = s_key[p];
+            const int64_t d = (int64_t)(ki - s_key[s0]);
+            if (d < -(1ll << 30) || d >= (1ll << 30)) {
+                s_wide[h] = 1;
+                s_anywide = 1;
+            }
+            const uint32_t* lo = (const uint32_t*)(s_key + s0);   // low word of key s0 + j at lo[2 j]
+            const uint32_t ti = (uint32_t)ki;
+            const int m = e0 - s0;
+            // four elements per trip, the < 4 left over predicated (no
+            // remainder loops: lanes of one warp have different m)
+            int j = 0;
+#pragma unroll 1
+            for (; j + 4 <= m; j += 4)
+                r += (int)(((lo[2 * j] - ti) >> 31) + ((lo[2 * j + 2] - ti) >> 31) +
+                           ((lo[2 * j + 4] - ti) >> 31) + ((lo[2 * j + 6] - ti) >> 31));
+            if (j < m) r += (int)((lo[2 * j] - ti) >> 31);
+            if (j + 1 < m) r += (int)((lo[2 * j + 2] - ti) >> 31);
+            if (j + 2 < m) r += (int)((lo[2 * j + 4] - ti) >> 31);
+            s_perm[s0 + r] = (uint16_t)p;   // (a wide case's claims stay inside its own slots)
         }
         wsync();
+        if (s_anywide) {   // wide cases: clear their slots, then the exact stable rank (unique slots)
+            for (int p = h0 + wt; p < oend; p += NW)
+                if (s_wide[s_ci[p]]) s_perm[p] = (uint16_t)0xffff;
+            wsync();
+            for (int p = h0 + wt; p < oend; p += NW) {
+                const uint32_t h = s_ci[p];
+                if (!s_wide[h]) continue;
+                const int s0 = s_head[h], e0 = ((int)h + 1 < Hown) ? s_head[h + 1] : oend;
+                const uint64_t ki = s_key[p], ki1 = ki + 1;
+                int r = 0;
+                if (ki1 != 0) {   // the all-ones key (key_bits = 64) has no successor
+                    for (int j = s0; j < e0; ++j) r += s_key[j] < (j < p ? ki1 : ki);
+                } else {
+                    for (int j = s0; j < e0; ++j) r += (s_key[j] < ki) | ((s_key[j] == ki) & (j < p));
+                }
+                s_perm[s0 + r] = (uint16_t)p;
+            }
+            wsync();
+        }
 
         // ---- 5. write the formatted rows of the owned range, slot by slot
         // (consecutive threads, consecutive output rows).  A slot followed by
