@@ -764,7 +764,10 @@ void free_variants(pm4g_variant_table* v) {
 // i.e. the Groups of group_items without a compaction or item pass.
 // a warp's task: 32 * IPT consecutive cases (IPT = PM4G_VG_IPT; IPT = 1 for small logs,
 // so their few tasks spread over more warps and CTAs instead of one CTA's latency chain)
-constexpr int VG_THREADS = 256;
+#ifndef PM4G_VG_THREADS
+#define PM4G_VG_THREADS 256
+#endif
+constexpr int VG_THREADS = PM4G_VG_THREADS;
 // per-CTA key cache entries, minimum CTAs per SM and cases per lane per task
 // (sweep, 100M / 1B-8 shard: 2 cases per lane, 1024 entries, 4 CTAs per SM
 // 0.36 / 0.36 ms; 4 per lane 0.50 / 0.55; 1 per lane 0.43 / 0.40; 8 per lane

@@ -488,3 +488,25 @@ def test_variant_table_past_cooperative_capacity():
     r = oracle.run(case, act, ts, 64)
     assert len(r.v_count) > 148 * 4096   # past a one-CTA-per-SM cooperative grid
     assert_parity(gpu_run(case, act, ts, 64, n_case_codes=C, sort_analyze=True), r)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_format_mixed_narrow_and_wide_cases(seed):
+    """k_format ranks every case narrow first (32-bit key differences) and
+    re-ranks a case found wide (a key > 2^30 units from its first) exactly:
+    tiles mixing narrow and wide cases, ties inside both, cases crossing tile
+    ends -- every output vs the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    C = 6000
+    m = rng.integers(1, 40, size=C)
+    case = np.repeat(np.arange(C, dtype=np.int64), m)
+    n = case.size
+    wide = rng.random(C) < 0.1                        # ~10% of the cases span > 2^30
+    span = np.where(wide[case], 1 << 34, 1 << 20)
+    ts = (rng.random(n) * span).astype(np.int64)
+    tie = rng.random(n) < 0.2                         # equal timestamps inside a case
+    ts[tie] = (case[tie] * 7) % 1000
+    act = rng.integers(0, 12, size=n)
+    p = rng.permutation(n)
+    case, act, ts = case[p], act[p], ts[p]
+    assert_parity(gpu_run(case, act, ts, 12, n_case_codes=C, sort_analyze=True), oracle.run(case, act, ts, 12))
