@@ -43,7 +43,7 @@ constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
 #ifndef PM4G_AGG_FCONS
-#define PM4G_AGG_FCONS 512
+#define PM4G_AGG_FCONS 992
 #endif
 #ifndef PM4G_AGG_HCONS
 #define PM4G_AGG_HCONS 992
@@ -52,10 +52,11 @@ constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 enum { TAB_FULL = 1, TAB_HASH = 2 };
 
 // Geometry per table mode (measured on one B200; the kernel is latency-bound,
-// so the number of warps in flight decides).  TAB_FULL: 16 consumer warps,
-// 3 stages of 2048 rows, two CTAs per SM (100M, A = 64: 8 / 12 / 16 / 24
-// consumer warps 0.516 / 0.498 / 0.498 / 0.572 ms; 4 stages 0.73, 2 x 4096
-// 0.51).  TAB_HASH: 31 consumer warps, 8192 slots, 2 stages of 4096 rows, one
+// so the number of warps in flight decides).  TAB_FULL: 31 consumer warps,
+// 3 stages of 4096 rows, one CTA per SM (100M, A = 64: 0.478 ms; two CTAs per
+// SM of 3 x 2048-row stages with 8 / 12 / 16 / 24 consumer warps 0.516 /
+// 0.498 / 0.498 / 0.572 ms; 31 warps with 2048-row stages 0.73, 2 x 4096
+// 0.487).  TAB_HASH: 31 consumer warps, 8192 slots, 2 stages of 4096 rows, one
 // CTA per SM (1B/8 shard, A = 256, ~1,000 distinct edges: 0.597 ms; the same
 // with 23 warps 0.603; 16 warps + 4096 slots + 2 x 2048 rows at two CTAs per
 // SM 0.667, with 8 warps 0.796; 3 stages or 1024-row stages slower).  The
@@ -70,14 +71,17 @@ enum { TAB_FULL = 1, TAB_HASH = 2 };
 #define PM4G_AGG_HSLOTS 8192
 #endif
 #ifndef PM4G_AGG_FROWS
-#define PM4G_AGG_FROWS 2048
+#define PM4G_AGG_FROWS 4096
 #endif
 #ifndef PM4G_AGG_FSTAGES
 #define PM4G_AGG_FSTAGES 3
 #endif
-template <int MODE>
+template <class P, int MODE>
 struct AggGeom {
-    static constexpr uint32_t ROWS = MODE == TAB_FULL ? PM4G_AGG_FROWS : PM4G_AGG_HROWS;   // rows of a staged case tile
+    // rows of a staged case tile (wider activity codes: half the TAB_FULL stage, so
+    // a 100 KB dense table and three stages still fit one CTA's shared memory)
+    static constexpr uint32_t ROWS = MODE == TAB_FULL ? (sizeof(P) == 1 ? PM4G_AGG_FROWS : PM4G_AGG_FROWS / 2)
+                                                      : PM4G_AGG_HROWS;
     static constexpr int STAGES = MODE == TAB_FULL ? PM4G_AGG_FSTAGES : PM4G_AGG_HSTAGES;
     static constexpr int CONS = MODE == TAB_FULL ? PM4G_AGG_FCONS : PM4G_AGG_HCONS;       // consumer threads
     static constexpr int BLOCK = CONS + 32;                                                 // + 1 producer warp
@@ -139,15 +143,15 @@ __device__ __forceinline__ void smem_acc(uint32_t* cnt, uint32_t* lo, uint32_t* 
 
 // WIDE: the log's key is ts - ts_min alone; a row's case is rcase[row]
 template <class P, int MODE, bool MM, bool WIDE = false>
-__global__ __launch_bounds__(AggGeom<MODE>::BLOCK) void k_aggregate(
+__global__ __launch_bounds__(AggGeom<P, MODE>::BLOCK) void k_aggregate(
     const uint64_t* __restrict__ key, const P* __restrict__ act, const uint32_t* __restrict__ off,
     const uint64_t* __restrict__ d_n_cases, int ts_bits, uint32_t A, uint32_t cpt,
     uint64_t* __restrict__ packed, uint64_t* __restrict__ mm, uint32_t* __restrict__ n_events,
     int64_t* __restrict__ dur, uint64_t* __restrict__ k1o, uint64_t* __restrict__ k2o, int weak,
     uint32_t* __restrict__ cco, uint32_t case_min, const uint32_t* __restrict__ rcase) {
-    constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
-    constexpr int AGG_STAGES = AggGeom<MODE>::STAGES;
-    constexpr int AGG_CONSUMERS = AggGeom<MODE>::CONS, AGG_BLOCK = AggGeom<MODE>::BLOCK;
+    constexpr uint32_t AGG_STAGE = AggGeom<P, MODE>::ROWS;
+    constexpr int AGG_STAGES = AggGeom<P, MODE>::STAGES;
+    constexpr int AGG_CONSUMERS = AggGeom<P, MODE>::CONS, AGG_BLOCK = AggGeom<P, MODE>::BLOCK;
     using Stage = AggStage<P, AGG_STAGE>;
     extern __shared__ __align__(128) unsigned char agg_sm[];
     __shared__ __align__(8) uint64_t s_full[AGG_STAGES], s_empty[AGG_STAGES];
@@ -369,8 +373,8 @@ template <class P, int MODE, bool MM, bool WIDE>
 static pm4g_status launch_agg_w(const pm4g_log* L, const AggOut& o, cudaStream_t s) {
     const uint32_t A = L->A;
     const size_t tab = o.tables ? (size_t)tab_words_for<P, MM>(MODE, A) * 4 : 0;
-    constexpr uint32_t AGG_STAGE = AggGeom<MODE>::ROWS;
-    const size_t smem = tab + AggGeom<MODE>::STAGES * sizeof(AggStage<P, AGG_STAGE>);
+    constexpr uint32_t AGG_STAGE = AggGeom<P, MODE>::ROWS;
+    const size_t smem = tab + AggGeom<P, MODE>::STAGES * sizeof(AggStage<P, AGG_STAGE>);
     PM4G_MAX_SMEM(k_aggregate<P, MODE, MM, WIDE>);
     const uint64_t cap = std::min<uint64_t>((uint64_t)L->n, (uint64_t)(L->case_max - L->case_min) + 1);
     // cases per tile: a tile's rows should fit one stage (mean length from the
@@ -383,14 +387,14 @@ static pm4g_status launch_agg_w(const pm4g_log* L, const AggOut& o, cudaStream_t
     int& per_sm = per_sm_c[o.tables ? 1 : 0];
     if (per_sm < 0)
         PM4G_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aggregate<P, MODE, MM, WIDE>,
-                                                              AggGeom<MODE>::BLOCK, smem));
+                                                              AggGeom<P, MODE>::BLOCK, smem));
     per_sm = std::max(per_sm, 1);
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)num_sms() * per_sm);
     // algorithmic bytes: read key + act once per event, + per-case offsets and outputs
     const double bytes = (double)L->n * (8 + sizeof(P) + (WIDE ? 4 : 0)) + (double)cap * 4 + (o.n_events ? cap * 4.0 : 0) +
                          (o.dur ? cap * 8.0 : 0) + (o.k1 ? cap * 16.0 : 0) + (o.case_code ? cap * 4.0 : 0);
     PM4G_LAUNCH("k_aggregate", bytes, s,
-                (k_aggregate<P, MODE, MM, WIDE><<<(unsigned)grid, AggGeom<MODE>::BLOCK, smem, s>>>(
+                (k_aggregate<P, MODE, MM, WIDE><<<(unsigned)grid, AggGeom<P, MODE>::BLOCK, smem, s>>>(
                     L->key, (const P*)L->s_act, L->off, L->d_n_cases, L->ts_bits, A, cpt,
                     o.tables ? o.packed : nullptr, o.mm, o.n_events, o.dur, o.k1, o.k2,
                     debug_weak_hash() ? 1 : 0, o.case_code, L->case_min, L->rcase)));

@@ -510,3 +510,29 @@ def test_format_mixed_narrow_and_wide_cases(seed):
     p = rng.permutation(n)
     case, act, ts = case[p], act[p], ts[p]
     assert_parity(gpu_run(case, act, ts, 12, n_case_codes=C, sort_analyze=True), oracle.run(case, act, ts, 12))
+
+
+@pytest.mark.parametrize("dtype", [torch.int16, torch.int32])
+@pytest.mark.parametrize("A", [7, 60, 91])
+def test_wide_activity_codes_with_dense_table(dtype, A):
+    """2- and 4-byte activity codes with a small alphabet (the caller's choice of
+    width): the dense shared-memory DFG table next to the wider stages, with and
+    without the min / max tables -- every output vs the oracle."""
+    from tests.parity import collect
+    rng = np.random.default_rng(A)
+    n = 60_000
+    case = rng.integers(0, 5_000, n)
+    act = rng.integers(0, A, n)
+    ts = rng.integers(0, 10**9, n)
+    c = torch.as_tensor(case).to(torch.uint32).cuda()
+    a = torch.as_tensor(act).to(dtype).cuda()
+    t = torch.as_tensor(ts).cuda()
+    log = pm4g.pm4g_log_create(c, a, t, A, n_case_codes=5_000)
+    log.sort()
+    assert_parity(collect(log), oracle.run(case, act, ts, A))
+    o = log.analyze(minmax=True)
+    rmn, rmx = oracle.dfg_minmax(case, act, ts, A)
+    assert np.array_equal(o["dur_min"].cpu().numpy().view(np.uint64), rmn.reshape(-1).astype(np.uint64))
+    assert np.array_equal(o["dur_max"].cpu().numpy().view(np.uint64), rmx.reshape(-1).astype(np.uint64))
+    o["variants"].close()
+    log.close()
