@@ -46,6 +46,9 @@ constexpr int RADIX = 256;
 #ifndef PM4G_RANK_OR   // radix ranking peers: 1 = shared-memory atomicOr masks, 0 = 8 ballots
 #define PM4G_RANK_OR 1
 #endif
+#ifndef PM4G_LB            // look-back predecessors per L2 round trip
+#define PM4G_LB 4
+#endif
 #ifndef PM4G_SORT_MINB
 #define PM4G_SORT_MINB 2
 #endif
@@ -164,6 +167,15 @@ struct OsLayout {
     static constexpr size_t bytes = (o_vdig + (WIDE ? T : 0) + 15) / 16 * 16;
 };
 
+#ifdef PM4G_OS_PROF
+__device__ unsigned long long g_osprof[8];
+extern "C" void pm4g_debug_osprof(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_osprof, 8 * 8);
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_osprof, z, 8 * 8);
+}
+#endif
 struct NoHook {
     __device__ void operator()() const {}
 };
@@ -195,6 +207,11 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         return sh_ok ? (uint32_t)(k >> sh) & dmask : 0u;
     };
 
+#ifdef PM4G_OS_PROF
+    const long long pt0 = clock64();
+    long long pt1 = 0, pt2 = 0, pt3 = 0;
+    uint32_t ptrips = 0;
+#endif
     // ---- stable local rank: warp-striped order (warp, j, lane) == index order.
     // dp[j] = digit << 16 | rank of the key among its warp's keys of that digit.
     uint64_t k[SORT_IPT];
@@ -284,6 +301,9 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         __syncwarp();
     }
     __syncthreads();   // every key is in registers: u_key may be overwritten
+#ifdef PM4G_OS_PROF
+    pt1 = clock64();
+#endif
     after_rank();
 
     // ---- per-digit totals; warp bases = tile-exclusive start + warp-exclusive prefix
@@ -329,31 +349,43 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         if (WIDE) v_dig[p] = (uint8_t)(dp[j] >> 16);
     }
 
-    // ---- decoupled look-back for this digit, 4 predecessors per round trip
+#ifdef PM4G_OS_PROF
+    pt2 = clock64();
+#endif
+    // ---- decoupled look-back for this digit, PM4G_LB predecessors per round trip
+    // (4, 8 or 16 per trip, with or without requesting the first batch right
+    // after the publish, measured equal or slower: the wait is for predecessors
+    // still ranking, not the walk -- PM4G_OS_PROF phase counters)
     if (dig) {
         uint32_t prefix = 0;
         if (tile > 0) {
             int64_t p = (int64_t)tile - 1;
             bool done = false;
             while (!done) {
-                st_t w[4];
+                st_t w[PM4G_LB];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < PM4G_LB; ++q)
                     w[q] = (p - q >= 0) ? ld_volatile(a.status + (size_t)(p - q) * RADIX + d) : st_inc(0);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < PM4G_LB; ++q) {
                     if (done) break;
                     while (w[q] == 0) w[q] = ld_volatile(a.status + (size_t)(p - q) * RADIX + d);
                     prefix += st_val(w[q]);
                     if (st_is_inc(w[q])) done = true;
                 }
-                p -= 4;
+                p -= PM4G_LB;
+#ifdef PM4G_OS_PROF
+                ++ptrips;
+#endif
             }
             st_volatile(st, st_inc(prefix + pub));
         }
         s_gbase[d] = (long long)a.bucket_off[d] + prefix - start;
     }
     __syncthreads();
+#ifdef PM4G_OS_PROF
+    pt3 = clock64();
+#endif
 
     // ---- coalesced write-out: consecutive threads, consecutive positions
 #pragma unroll 4
@@ -367,6 +399,17 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
             if (WITH_IDX) a.out_idx[g] = v_idx[sidx];
         }
     }
+#ifdef PM4G_OS_PROF
+    if (tid == 0) {
+        const long long pt4 = clock64();
+        atomicAdd(&g_osprof[0], (unsigned long long)(pt1 - pt0));
+        atomicAdd(&g_osprof[1], (unsigned long long)(pt2 - pt1));
+        atomicAdd(&g_osprof[2], (unsigned long long)(pt3 - pt2));
+        atomicAdd(&g_osprof[3], (unsigned long long)(pt4 - pt3));
+        atomicAdd(&g_osprof[4], (unsigned long long)ptrips);
+        atomicAdd(&g_osprof[5], 1ull);
+    }
+#endif
 }
 
 // HI: the digit lies in the key's high word (32 <= shift < 64, the usual case:
