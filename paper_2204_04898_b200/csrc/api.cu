@@ -260,33 +260,49 @@ __global__ __launch_bounds__(256) void k_validate(const uint32_t* __restrict__ c
     };
     const bool vec = (((uintptr_t)cs | (uintptr_t)ts) & 15) == 0 && ((uintptr_t)act & (4 * sizeof(P) - 1)) == 0;
     const int64_t nq = vec ? n / 4 : 0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        const uint4 c4 = ((const uint4*)cs)[q];
-        const longlong2 t01 = ((const longlong2*)ts)[2 * q], t23 = ((const longlong2*)ts)[2 * q + 1];
+    auto quad = [&](int64_t q, const uint4& c4, const longlong2& t01, const longlong2& t23, const uint4& aw) {
         const int64_t i = 4 * q;
         uint32_t a[4];
         if constexpr (sizeof(P) == 1) {   // the four activities in one 4-byte load
-            const uint32_t w = ((const uint32_t*)act)[q];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) a[k] = (w >> (8 * k)) & 0xffu;
+            for (int k = 0; k < 4; ++k) a[k] = (aw.x >> (8 * k)) & 0xffu;
         } else if constexpr (sizeof(P) == 2) {
-            const uint2 w = ((const uint2*)act)[q];
-            a[0] = w.x & 0xffffu;
-            a[1] = w.x >> 16;
-            a[2] = w.y & 0xffffu;
-            a[3] = w.y >> 16;
+            a[0] = aw.x & 0xffffu;
+            a[1] = aw.x >> 16;
+            a[2] = aw.y & 0xffffu;
+            a[3] = aw.y >> 16;
         } else {
-            const uint4 w = ((const uint4*)act)[q];
-            a[0] = w.x;
-            a[1] = w.y;
-            a[2] = w.z;
-            a[3] = w.w;
+            a[0] = aw.x;
+            a[1] = aw.y;
+            a[2] = aw.z;
+            a[3] = aw.w;
         }
         row(i, c4.x, t01.x, a[0]);
         row(i + 1, c4.y, t01.y, a[1]);
         row(i + 2, c4.z, t23.x, a[2]);
         row(i + 3, c4.w, t23.y, a[3]);
+    };
+    auto load_act = [&](int64_t q) -> uint4 {
+        if constexpr (sizeof(P) == 1) return make_uint4(((const uint32_t*)act)[q], 0, 0, 0);
+        else if constexpr (sizeof(P) == 2) {
+            const uint2 w = ((const uint2*)act)[q];
+            return make_uint4(w.x, w.y, 0, 0);
+        } else return ((const uint4*)act)[q];
+    };
+    // two quads per thread per trip, every load issued before any row is processed
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; q + stride < nq; q += 2 * stride) {
+        const int64_t r = q + stride;
+        const uint4 c4 = ((const uint4*)cs)[q], d4 = ((const uint4*)cs)[r];
+        const longlong2 t01 = ((const longlong2*)ts)[2 * q], t23 = ((const longlong2*)ts)[2 * q + 1];
+        const longlong2 u01 = ((const longlong2*)ts)[2 * r], u23 = ((const longlong2*)ts)[2 * r + 1];
+        const uint4 aq = load_act(q), ar = load_act(r);
+        quad(q, c4, t01, t23, aq);
+        quad(r, d4, u01, u23, ar);
     }
+    for (; q < nq; q += stride)
+        quad(q, ((const uint4*)cs)[q], ((const longlong2*)ts)[2 * q], ((const longlong2*)ts)[2 * q + 1], load_act(q));
     for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         row(i, cs[i], ts[i], (uint32_t)act[i]);
     for (int o = 16; o; o >>= 1) {
