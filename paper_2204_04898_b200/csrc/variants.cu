@@ -1290,7 +1290,10 @@ __global__ __launch_bounds__(SV_THREADS) void k_small_variants(
 // and finally every case's variant index.  Replaces ~14 launches (sort keys,
 // histogram, scan, 5-6 radix passes, inverse, emit, scan, gather, case index)
 // whose latency dominated at these sizes.
-constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = 8, VO_CHUNK = VO_THREADS * VO_IPT;
+#ifndef PM4G_VO_IPT
+#define PM4G_VO_IPT 8
+#endif
+constexpr int VO_THREADS = 512, VO_WARPS = VO_THREADS / 32, VO_IPT = PM4G_VO_IPT, VO_CHUNK = VO_THREADS * VO_IPT;
 constexpr uint64_t VO_MAX_GROUPS = 296ull * VO_CHUNK;   // chunks of <= 4096 over co-resident CTAs (order_medium checks the real occupancy)
 constexpr pm4g_status VO_NOT_LAUNCHED = (pm4g_status)100;   // internal: the cooperative grid was refused
 #ifndef PM4G_VO_TARGET
