@@ -42,6 +42,9 @@ constexpr int AGG_THREADS = 256;
 constexpr int AGG_CASES = 256;   // cases per tile
 constexpr size_t AGG_SMEM_MAX = 100 * 1024;     // TAB_FULL table budget
 
+#ifndef PM4G_AGG_PMIN   // fewest pair threads left when the case-holding warps skip the pairs
+#define PM4G_AGG_PMIN 512
+#endif
 #ifndef PM4G_AGG_FCONS
 #define PM4G_AGG_FCONS 992
 #endif
@@ -268,7 +271,17 @@ __global__ __launch_bounds__(AggGeom<P, MODE>::BLOCK) void k_aggregate(
             auto A_at = [&](uint32_t r) -> uint32_t { return staged ? (uint32_t)st.act[r - aa] : (uint32_t)act[r]; };
             if (tables) {
                 // directly-follows pairs (r, r+1) of one case
-                for (uint32_t r = e0 + ct; r + 1 < e1; r += AGG_CONSUMERS) {
+                // the warps holding the tile's cases (threads < nc, one serial
+                // per-case loop each, below) take no pairs when enough other
+                // warps remain, so they do not hold the stage's release (ncu:
+                // 39% of the stall samples were consumers waiting for a full
+                // stage, i.e. for the case-holding warps to free one; 1B/8 shard
+                // 0.60 -> 0.46 ms, 100M 0.48 -> 0.41 ms; a team-parallel Horner
+                // hash instead cost 7x the instructions and was 2-3x slower)
+                const uint32_t pw = (nc + 31) & ~31u;
+                const uint32_t p0 = AGG_CONSUMERS - pw >= PM4G_AGG_PMIN ? pw : 0u;
+                const uint32_t r0 = (uint32_t)ct >= p0 ? e0 + (ct - p0) : e1;   // e1: no pairs
+                for (uint32_t r = r0; r + 1 < e1; r += AGG_CONSUMERS - p0) {
                     const uint64_t kk = K_at(r), kn = K_at(r + 1);
                     if (WIDE ? rcase[r] != rcase[r + 1] : !same_case(kk, kn, ts_bits)) continue;
                     const uint32_t e = A_at(r) * A + A_at(r + 1);
