@@ -877,13 +877,18 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
 
     // ---- 1. the tile's rows -> smem (TMA bulk copies for full tiles), head ballots
     const bool bulk = tn == FMT_TILE && a.aligned;
+    // the FMT_EXT rows after the tile come in the same transfer when they exist
+    // (the tile's last case may run into them): the extension scan and rows then
+    // read shared memory instead of waiting on global loads (11% of a tile's time)
+    const bool xbulk = !WIDE && bulk && base + FMT_BUF <= a.n;
     if (bulk) {
         if (tid == 0) {
+            const uint32_t rows = xbulk ? FMT_BUF : FMT_TILE;
             mbar_init(&s_bar, 1);
-            mbar_expect_tx(&s_bar, FMT_TILE * (uint32_t)(8 + sizeof(P) + (WI ? 4 : 0)));
-            tma_load_1d(s_key, a.gkey + base, FMT_TILE * 8, &s_bar);
-            tma_load_1d(s_act, a.gact + base, FMT_TILE * (uint32_t)sizeof(P), &s_bar);
-            if (WI) tma_load_1d(s_idx, a.gidx + base, FMT_TILE * 4, &s_bar);
+            mbar_expect_tx(&s_bar, rows * (uint32_t)(8 + sizeof(P) + (WI ? 4 : 0)));
+            tma_load_1d(s_key, a.gkey + base, rows * 8, &s_bar);
+            tma_load_1d(s_act, a.gact + base, rows * (uint32_t)sizeof(P), &s_bar);
+            if (WI) tma_load_1d(s_idx, a.gidx + base, rows * 4, &s_bar);
         }
     } else {
         for (int p = tid; p < tn; p += FMT_THREADS) {
@@ -997,7 +1002,9 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
                 ext = -1;
                 for (int o = 0; o <= FMT_EXT; o += 32) {
                     const int64_t i = base + tn + o + lane;
-                    const bool stop = i >= a.n || (WIDE ? gcase(i) != lastc : !same_case(a.gkey[i], last, tb));
+                    const bool stop = i >= a.n || (WIDE ? gcase(i) != lastc
+                                                        : !same_case(xbulk && o + lane < FMT_EXT ? s_key[tn + o + lane] : a.gkey[i],
+                                                                     last, tb));
                     const uint32_t bb = __ballot_sync(0xffffffffu, stop);
                     if (bb) {
                         const int e = o + __ffs(bb) - 1;
@@ -1020,9 +1027,11 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         const int oend = Hown == (int)H ? tn + ext : (int)s_head[H - 1];   // owned rows [h0, oend)
         for (int p = tn + wt; p < oend; p += NW) {                          // extension rows
             const int64_t i = base + p;
-            s_key[p] = a.gkey[i];
-            s_act[p] = a.gact[i];
-            if (WI) s_idx[p] = a.gidx[i];
+            if (!xbulk) {
+                s_key[p] = a.gkey[i];
+                s_act[p] = a.gact[i];
+                if (WI) s_idx[p] = a.gidx[i];
+            }
             if (WIDE) s_c[p] = a.case_col[s_idx[p]] - a.case_min;
             s_ci[p] = (uint16_t)(H - 1);
             s_perm[p] = (uint16_t)0xffff;
