@@ -53,8 +53,8 @@ def kernels_md(rep, events):
              "|---|---|---|---|---|---|---|---|---|---|---|"]
     per = defaultdict(list)
     for r in rows:
-        ms = num(r["gpu__time_duration.sum"]) * (1e-3 if u.get("gpu__time_duration.sum") == "usecond" else
-                                                 (1e-6 if u.get("gpu__time_duration.sum") == "nsecond" else 1.0))
+        ms = num(r["gpu__time_duration.sum"]) * {"usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6, "ns": 1e-6}.get(
+            u.get("gpu__time_duration.sum"), 1.0)
         scale = lambda h: {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}.get(u.get(h, ""), 1.0)  # noqa: E731
         rd = num(r["dram__bytes_read.sum"]) * scale("dram__bytes_read.sum")
         wr = num(r["dram__bytes_write.sum"]) * scale("dram__bytes_write.sum")
