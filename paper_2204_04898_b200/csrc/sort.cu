@@ -329,7 +329,31 @@ __device__ __forceinline__ void os_tile(const PassArgs<P, FROM_COLS, WITH_IDX>& 
         }
     }
     uint32_t ranked = 0;   // rows placed: nvalid, or the kept rows of a filtered pass 0
-    const uint32_t start = block_excl_scan<SORT_THREADS>(tot, s_scan, tf ? &ranked : nullptr);
+    // exclusive scan of the RADIX digit totals (held by threads < RADIX) with one
+    // barrier: warp-inclusive scans, then each thread adds the totals of the
+    // warps before it (a two-level block scan costs a second barrier)
+    uint32_t start;
+    {
+        constexpr int DW = RADIX / 32;
+        static_assert(RADIX % 32 == 0 && RADIX <= SORT_THREADS && DW <= SORT_WARPS + 1, "digit scan layout");
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31 && warp < DW) s_scan[warp] = inc;
+        __syncthreads();
+        start = inc - tot;
+        uint32_t all = 0;
+#pragma unroll
+        for (int w = 0; w < DW; ++w) {
+            const uint32_t x = s_scan[w];
+            if (w < warp) start += x;
+            all += x;
+        }
+        ranked = all;
+    }
     const uint32_t nout = tf ? ranked : nvalid;
     if (tid < RADIX) {
 #pragma unroll
