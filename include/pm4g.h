@@ -265,7 +265,13 @@ pm4g_status pm4g_analyze(const pm4g_log* log, const pm4g_outputs* out, pm4g_comm
  * recomputed before the call returns.  Falls back to the two separate calls
  * when comm != NULL, when no variants are requested (no synchronisation to
  * share), or when the log has extra columns.  An already formatted log is only
- * analysed.  Errors: those of pm4g_sort and pm4g_analyze. */
+ * analysed.  Errors: those of pm4g_sort and pm4g_analyze.
+ * CUDA graphs (opt-in, environment PM4G_GRAPH=1, read once per process): the
+ * launches between the call's host round trips are captured from `stream` and
+ * run as one graph per segment; the executable graphs are kept per (device,
+ * stream, segment) and updated in place by later calls of the same shape
+ * (another shape re-instantiates them).  Results are identical.  `stream` must
+ * be capturable: on the legacy default stream the call runs eagerly. */
 pm4g_status pm4g_sort_analyze(pm4g_log* log, const pm4g_outputs* out, pm4g_comm* comm,
                               pm4g_stream_t stream);
 

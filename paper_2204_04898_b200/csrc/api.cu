@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -66,7 +68,10 @@ void prof_begin(const char* name, double bytes, cudaStream_t s) {
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     ProfRec r{name, bytes, get_event(), get_event()};
-    cudaEventRecord(r.a, s);
+    // inside a captured graph segment the events become external event-record
+    // nodes, recorded each time the graph runs
+    if (gseg_active()) cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal);
+    else cudaEventRecord(r.a, s);
     g_prof_recs.push_back(r);
 }
 // add bytes known only after the launch (e.g. a compaction's kept rows) to
@@ -83,7 +88,10 @@ void prof_add_bytes(const char* name, double bytes) {
 void prof_end(cudaStream_t s) {
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    if (!g_prof_recs.empty()) cudaEventRecord(g_prof_recs.back().b, s);
+    if (!g_prof_recs.empty()) {
+        if (gseg_active()) cudaEventRecordWithFlags(g_prof_recs.back().b, s, cudaEventRecordExternal);
+        else cudaEventRecord(g_prof_recs.back().b, s);
+    }
 }
 
 int num_sms() {
@@ -728,6 +736,141 @@ pm4g_status pm4g_log_info_get(const pm4g_log* L, pm4g_log_info* info) {
     return PM4G_OK;
 }
 
+}  // extern "C" (the graph segment helpers are C++)
+
+// ------------------------------------------------------------------ graph segments
+namespace pm4g {
+namespace {
+struct GraphSeg {
+    bool on = false, capturing = false;
+    int slot = 0;
+    cudaStream_t s = nullptr;
+};
+thread_local GraphSeg t_gseg;
+std::mutex g_exec_mu;
+std::map<std::tuple<int, cudaStream_t, int>, cudaGraphExec_t> g_execs;   // (device, stream, segment slot) -> executable graph
+
+pm4g_status gseg_begin() {
+    if (!t_gseg.on) return PM4G_OK;
+    PM4G_CK(cudaStreamBeginCapture(t_gseg.s, cudaStreamCaptureModeRelaxed));
+    t_gseg.capturing = true;
+    return PM4G_OK;
+}
+}  // namespace
+
+bool graph_mode() {
+    static const bool on = getenv("PM4G_GRAPH") && atoi(getenv("PM4G_GRAPH")) != 0;
+    return on;
+}
+
+bool gseg_active() { return t_gseg.capturing; }
+
+pm4g_status gseg_open(cudaStream_t s) {
+    t_gseg.on = true;
+    t_gseg.slot = 0;
+    t_gseg.s = s;
+    return gseg_begin();
+}
+
+pm4g_status gseg_close(bool discard) {
+    if (!t_gseg.capturing) return PM4G_OK;
+    t_gseg.capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(t_gseg.s, &g);
+    if (e != cudaSuccess || !g) {
+        cudaGetLastError();
+        return discard ? PM4G_OK : cuda_fail(e != cudaSuccess ? e : cudaErrorStreamCaptureInvalidated, "stream capture");
+    }
+    if (discard) {
+        cudaGraphDestroy(g);
+        return PM4G_OK;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaGraphExec_t ex = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_exec_mu);
+        const auto key = std::make_tuple(dev, t_gseg.s, t_gseg.slot++);
+        auto it = g_execs.find(key);
+        if (it != g_execs.end()) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(it->second, g, &info) == cudaSuccess) {
+                ex = it->second;
+            } else {   // another topology: instantiate anew
+                if (getenv("PM4G_GRAPH_TRACE")) {
+                    cudaGraphNodeType nt = cudaGraphNodeTypeCount;
+                    if (info.errorNode) cudaGraphNodeGetType(info.errorNode, &nt);
+                    const char* fn = "";
+                    if (nt == cudaGraphNodeTypeKernel) {
+                        cudaKernelNodeParams kp;
+                        if (cudaGraphKernelNodeGetParams(info.errorNode, &kp) == cudaSuccess) {
+                            cudaFuncAttributes fa;
+                            (void)fa;
+                        }
+                    }
+                    if (nt == cudaGraphNodeTypeMemset) {
+                        cudaMemsetParams mp;
+                        if (cudaGraphMemsetNodeGetParams(info.errorNode, &mp) == cudaSuccess)
+                            fprintf(stderr, "  memset node: elem %u width %zu height %zu value %u\n", mp.elementSize, mp.width,
+                                    mp.height, mp.value);
+                    }
+                    if (nt == cudaGraphNodeTypeMemcpy) {
+                        cudaMemcpy3DParms cp;
+                        if (cudaGraphMemcpyNodeGetParams(info.errorNode, &cp) == cudaSuccess)
+                            fprintf(stderr, "  memcpy node: kind %d extent %zu\n", (int)cp.kind, cp.extent.width);
+                    }
+                    fprintf(stderr, "pm4g graph slot %d: update refused (result %d, node type %d)%s\n", key.second,
+                            (int)info.result, (int)nt, fn);
+                }
+                cudaGetLastError();
+                cudaGraphExecDestroy(it->second);
+                g_execs.erase(it);
+            }
+        }
+        if (!ex) {
+            e = cudaGraphInstantiate(&ex, g, 0);
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(g);
+                return cuda_fail(e, "cudaGraphInstantiate");
+            }
+            g_execs[key] = ex;
+        }
+    }
+    e = cudaGraphLaunch(ex, t_gseg.s);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    return PM4G_OK;
+}
+
+__global__ void k_copy_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+
+pm4g_status copy_words_to_host(void* h, const void* d, size_t bytes, cudaStream_t s) {
+    if (!t_gseg.capturing || (bytes & 3)) {
+        PM4G_CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+        return PM4G_OK;
+    }
+    void* hd = nullptr;
+    PM4G_CK(cudaHostGetDevicePointer(&hd, h, 0));
+    PM4G_LAUNCH("k_copy_words", (double)bytes, s,
+                (k_copy_words<<<1, 32, 0, s>>>((uint32_t*)hd, (const uint32_t*)d, (uint32_t)(bytes / 4))));
+    return PM4G_OK;
+}
+
+pm4g_status stream_sync(cudaStream_t s) {
+    const bool seg = t_gseg.capturing && t_gseg.s == s;
+    if (seg) PM4G_TRY(gseg_close(false));
+    PM4G_CK(cudaStreamSynchronize(s));
+    if (seg) PM4G_TRY(gseg_begin());
+    return PM4G_OK;
+}
+
+}  // namespace pm4g
+
+extern "C" {
+
 static pm4g_status sort_impl(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     PM4G_TRY(sort_log(L, s, d));   // sort + case offsets (format kernel)
     free_log_cols(L, s);
@@ -752,12 +895,23 @@ pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* c
     }
     cudaStream_t s = (cudaStream_t)stream;
     FmtDeferred d(s);
-    PM4G_TRY(sort_impl(L, s, &d));
+    // (the legacy default stream cannot be captured: such calls run eagerly)
+    const bool graphs = graph_mode() && s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread;
+    if (graphs) PM4G_TRY(gseg_open(s));
+    pm4g_status st = sort_impl(L, s, &d);
+    if (st != PM4G_OK) {
+        gseg_close(true);
+        return st;
+    }
     // the analysis synchronises (variant counters); the deferred format check
     // then costs no extra wait (its count is copied right after the aggregate launch)
     t_pending_format = &d;
-    pm4g_status st = pm4g_analyze(L, out, comm, stream);
+    st = pm4g_analyze(L, out, comm, stream);
     t_pending_format = nullptr;
+    if (graphs) {   // the last segment; on an error the captured work never ran
+        const pm4g_status gs = gseg_close(st != PM4G_OK);
+        if (st == PM4G_OK) st = gs;
+    }
     bool fixed = false;
     const pm4g_status fs = sort_finish(&d, s, &fixed);
     if (fs != PM4G_OK) {   // the input columns are gone and the order is provisional

@@ -372,6 +372,23 @@ pm4g_status sort_log(pm4g_log* L, cudaStream_t s, FmtDeferred* d = nullptr);   /
 pm4g_status sort_finish(FmtDeferred* d, cudaStream_t s, bool* fixed);
 pm4g_status segments(pm4g_log* L, cudaStream_t s);            // A4
 pm4g_status fetch_n_cases(const pm4g_log* L, cudaStream_t s);
+
+// CUDA-graph segments of pm4g_sort_analyze (opt-in, PM4G_GRAPH=1): the launches
+// between the call's host round trips are captured from the stream and run as
+// one graph each (an executable graph per segment slot is kept and updated in
+// place when the next call captures the same topology).  stream_sync() is the
+// round trip: it ends and launches the open segment, synchronises, and opens
+// the next one.
+bool graph_mode();
+pm4g_status gseg_open(cudaStream_t s);    // start capturing a sort_analyze call's first segment
+pm4g_status gseg_close(bool discard);     // end and launch (or discard) the open segment
+bool gseg_active();
+pm4g_status stream_sync(cudaStream_t s);
+// a few words device -> pinned host (the host reads them after stream_sync): a
+// cudaMemcpyAsync normally; inside a graph segment a one-warp kernel storing
+// into the mapped pinned words (a kernel node updates in place when the device
+// pointer changes between calls, a device-to-host memcpy node does not)
+pm4g_status copy_words_to_host(void* h, const void* d, size_t bytes, cudaStream_t s);
 pm4g_status radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits,
                            cudaStream_t s);  // generic: (key, u32 payload), in place
 pm4g_status radix_sort_u64_to(const uint64_t* keys, const uint32_t* vals, uint32_t* vals_out, int64_t n,

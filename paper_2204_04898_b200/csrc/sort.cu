@@ -1574,8 +1574,10 @@ thread_local FmtDeferred* t_pending_format = nullptr;
 
 pm4g_status sort_defer_copy(FmtDeferred* d, cudaStream_t s) {
     if (!d || !d->d_nbig) return PM4G_OK;
-    PM4G_CK(cudaMemcpyAsync(d->h_nbig, d->d_nbig, 4, cudaMemcpyDeviceToHost, s));
-    PM4G_CK(cudaEventRecord(d->ev, s));
+    PM4G_TRY(copy_words_to_host(d->h_nbig, d->d_nbig, 4, s));
+    // (inside a captured graph segment the copy completes before the segment's
+    // closing synchronisation, which sort_finish's read follows)
+    if (!gseg_active()) PM4G_CK(cudaEventRecord(d->ev, s));
     d->d_nbig = nullptr;
     return PM4G_OK;
 }

@@ -583,9 +583,9 @@ static pm4g_status group_items(uint64_t n_items, const uint64_t* k1, const uint6
             static thread_local unsigned char* h_stage = nullptr;
             if (!h_stage) PM4G_CK(cudaHostAlloc((void**)&h_stage, 64, cudaHostAllocDefault));
             const size_t o_tot = (size_t)((const char*)d_total - (const char*)counters);   // <= 20
-            PM4G_CK(cudaMemcpyAsync(h_stage, counters, o_tot + 8, cudaMemcpyDeviceToHost, s));
-            if (d_n && !list) PM4G_CK(cudaMemcpyAsync(h_stage + 32, d_n, 8, cudaMemcpyDeviceToHost, s));
-            PM4G_CK(cudaStreamSynchronize(s));
+            PM4G_TRY(copy_words_to_host(h_stage, counters, o_tot + 8, s));
+            if (d_n && !list) PM4G_TRY(copy_words_to_host(h_stage + 32, d_n, 8, s));
+            PM4G_TRY(stream_sync(s));
             memcpy(h, h_stage, 16);
             memcpy(&htot, h_stage + o_tot, 8);
             if (d_n && !list) memcpy(&hn, h_stage + 32, 8);
@@ -1622,9 +1622,9 @@ static pm4g_status group_cases_fast(uint64_t n_items, const uint64_t* k1, const 
         // one host round trip: overflow, gids, collisions, groups, total length (+ the case count)
         static thread_local unsigned char* h_stage = nullptr;
         if (!h_stage) PM4G_CK(cudaHostAlloc((void**)&h_stage, 64, cudaHostAllocDefault));
-        PM4G_CK(cudaMemcpyAsync(h_stage, ctl, 24, cudaMemcpyDeviceToHost, s));
-        if (d_n) PM4G_CK(cudaMemcpyAsync(h_stage + 32, d_n, 8, cudaMemcpyDeviceToHost, s));
-        PM4G_CK(cudaStreamSynchronize(s));
+        PM4G_TRY(copy_words_to_host(h_stage, ctl, 24, s));
+        if (d_n) PM4G_TRY(copy_words_to_host(h_stage + 32, d_n, 8, s));
+        PM4G_TRY(stream_sync(s));
         uint32_t h[4];
         memcpy(h, h_stage, 16);
         memcpy(&htot, h_stage + 16, 8);
