@@ -17,7 +17,10 @@ shard per GPU (weak scaling: rank r holds case codes [r*10M, (r+1)*10M) of a
 global log of N*100M events).  Inputs (1.3 GB/GPU) are larger than L2.
 
 Rank 0 prints ONE JSON line.  `value` = total input events of all ranks / max
-over ranks of the device time of the K timed steps.  `e2e` = the same metric
+over ranks of the device time of the K timed steps (CUDA events around the loop
+only; a second K-step loop with an event pair around every kernel gives the
+per-kernel table and the roofline, `instrumented_ms_per_step`).  `--graph` runs
+pm4g_sort_analyze's segments between its host round trips as CUDA graphs.  `e2e` = the same metric
 from HOST buffers (pinned) with a D2H read of every result, inside the timed
 region.  For steps of >= 64 MB the H2D copy of step k+1's columns is a torch
 copy_ into one of two device column sets on an ingest stream (own host thread),
@@ -25,7 +28,7 @@ followed by pm4g_log_create borrowing them, all under step k's compute and D2H;
 smaller steps pass the pinned host columns to pm4g_log_create with
 PM4G_HOST_INPUT (the copy is then inside the C-ABI call).  `roofline` = the
 dominant kernel (k_onesweep, the radix scatter pass) -- algorithmic bytes /
-CUDA-event time of its launches in the timed region, against
+CUDA-event time of its launches in the instrumented loop, against
 MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the oracle (single-threaded C++)
 timed per stage on the whole config at N = 1 (default), whose every output is
 then compared element by element with a GPU step on the same log

@@ -13,7 +13,7 @@ export PYTHONPATH=.
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 timeout 900 python bench.py --config 1B --filter --steps 5 --warmup 3 --cpu-cases 2000000 > $OUT/bench_1B.json 2> $OUT/bench_1B.err
-for r in 0 7; do timeout 600 python bench.py --config 1B --filter --emulate $r/8 --steps 10 --warmup 3 --cpu-cases 300000 > $OUT/bench_1B_shard${r}of8.json 2>> $OUT/bench_1B_shard.err; done
+for r in 0 7; do timeout 600 python bench.py --config 1B --filter --emulate $r/8 --steps 20 --warmup 5 --cpu-cases 300000 > $OUT/bench_1B_shard${r}of8.json 2>> $OUT/bench_1B_shard.err; done
 for c in tiny roadtraffic bpic2019; do timeout 300 python bench.py --config $c --steps 200 --warmup 20 --cpu-cases 300000 >> $OUT/bench_small.jsonl 2>> $OUT/bench_small.err; done
 for c in tiny roadtraffic bpic2019 bpic2018; do timeout 300 python bench.py --config $c --steps 200 --warmup 20 --no-cpu-baseline --e2e-steps 0 --graph >> $OUT/bench_small_graph.jsonl 2>> $OUT/bench_small.err; done
 timeout 300 python bench.py --config bpic2018 --steps 50 --warmup 5 --cpu-cases 43809 > $OUT/bench_bpic2018.json 2> $OUT/bench_bpic2018.err
