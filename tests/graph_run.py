@@ -21,4 +21,17 @@ for name in sys.argv[1:]:
     r = oracle.run(c, a, t, L.n_activities)
     for rep in range(3):
         assert_parity(gpu_run(c, a, t, L.n_activities, n_case_codes=L.n_case_codes, sort_analyze=True), r)
+# a case longer than the in-shared-memory ranking takes (the exact fallback runs
+# after the graph segments, eagerly) and timestamp ties
+import numpy as np  # noqa: E402
+rng = np.random.default_rng(3)
+n = 60_000
+c = rng.integers(0, 4000, n)
+c[:5000] = 77
+a = rng.integers(0, 9, n)
+t = rng.integers(0, 10**6, n)
+t[::5] = 123
+r = oracle.run(c, a, t, 9)
+for rep in range(3):
+    assert_parity(gpu_run(c, a, t, 9, n_case_codes=4000, sort_analyze=True), r)
 print("graph_run ok")
