@@ -153,13 +153,13 @@ def _ptr(t):
 
 
 def _stream(stream):
-    if stream is None:
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if stream is None:   # the current stream's raw handle (torch.cuda.current_stream() costs ~15 us a call)
+        return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
     return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 
 def _dev():
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cuda", torch._C._cuda_getDevice())
 
 
 def act_bytes_for(n_activities: int) -> int:
