@@ -819,7 +819,7 @@ pm4g_status gseg_close(bool discard) {
                         if (cudaGraphMemcpyNodeGetParams(info.errorNode, &cp) == cudaSuccess)
                             fprintf(stderr, "  memcpy node: kind %d extent %zu\n", (int)cp.kind, cp.extent.width);
                     }
-                    fprintf(stderr, "pm4g graph slot %d: update refused (result %d, node type %d)%s\n", key.second,
+                    fprintf(stderr, "pm4g graph slot %d: update refused (result %d, node type %d)%s\n", std::get<2>(key),
                             (int)info.result, (int)nt, fn);
                 }
                 cudaGetLastError();
