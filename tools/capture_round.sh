@@ -5,7 +5,7 @@
 # one bench step and one ncu --set full capture of the 100M step's kernels.
 set -x
 OUT=${1:-gpurun_out/capture}
-python -m paper_2204_04898_b200.build >/dev/null
+python -m paper_2204_04898_b200.build >/dev/null || { echo "BUILD FAILED"; exit 1; }
 python -c "import oracle; oracle.build()"
 mkdir -p $OUT
 export PYTHONPATH=.
