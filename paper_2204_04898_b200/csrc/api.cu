@@ -451,9 +451,13 @@ pm4g_status fetch_n_cases(const pm4g_log* Lc, cudaStream_t s) {
     pm4g_log* L = const_cast<pm4g_log*>(Lc);
     if (L->n_cases >= 0) return PM4G_OK;
     uint64_t v = 0;
+    pm4g_status gs;
+    const bool seg = gseg_suspend(s, &gs);   // (a pageable copy cannot sit in a graph segment)
+    PM4G_TRY(gs);
     PM4G_CK(cudaMemcpyAsync(&v, L->d_n_cases, sizeof(v), cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
     L->n_cases = (int64_t)v;
+    if (seg) PM4G_TRY(gseg_resume());
     return PM4G_OK;
 }
 
@@ -858,6 +862,15 @@ pm4g_status copy_words_to_host(void* h, const void* d, size_t bytes, cudaStream_
                 (k_copy_words<<<1, 32, 0, s>>>((uint32_t*)hd, (const uint32_t*)d, (uint32_t)(bytes / 4))));
     return PM4G_OK;
 }
+
+bool gseg_suspend(cudaStream_t s, pm4g_status* st) {
+    *st = PM4G_OK;
+    if (!(t_gseg.capturing && t_gseg.s == s)) return false;
+    *st = gseg_close(false);
+    return true;
+}
+
+pm4g_status gseg_resume() { return gseg_begin(); }
 
 pm4g_status stream_sync(cudaStream_t s) {
     const bool seg = t_gseg.capturing && t_gseg.s == s;

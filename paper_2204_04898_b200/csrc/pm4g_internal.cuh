@@ -384,6 +384,10 @@ pm4g_status gseg_open(cudaStream_t s);    // start capturing a sort_analyze call
 pm4g_status gseg_close(bool discard);     // end and launch (or discard) the open segment
 bool gseg_active();
 pm4g_status stream_sync(cudaStream_t s);
+// for a host round trip through pageable memory (not capturable): end and launch
+// the open segment on s (returns whether one was open), then gseg_resume()
+bool gseg_suspend(cudaStream_t s, pm4g_status* st);
+pm4g_status gseg_resume();
 // a few words device -> pinned host (the host reads them after stream_sync): a
 // cudaMemcpyAsync normally; inside a graph segment a one-warp kernel storing
 // into the mapped pinned words (a kernel node updates in place when the device

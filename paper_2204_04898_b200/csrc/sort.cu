@@ -1291,8 +1291,12 @@ static pm4g_status format_fallback(const FmtArgs<P>& fa, uint32_t nbig, cudaStre
     const int gb = std::max(1, std::min<int>((int)((nbig + 255) / 256), num_sms()));
     PM4G_LAUNCH("k_big_bounds", nbig * 12.0, s, (k_big_bounds<<<gb, 256, 0, s>>>(fa.big, nbig, fa.off, se.as<uint32_t>())));
     std::vector<uint32_t> h(2 * (size_t)nbig);
+    pm4g_status gs;
+    const bool seg = gseg_suspend(s, &gs);   // (a pageable copy cannot sit in a graph segment)
+    PM4G_TRY(gs);
     PM4G_CK(cudaMemcpyAsync(h.data(), se.p, (size_t)nbig * 8, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
+    if (seg) PM4G_TRY(gseg_resume());
     std::vector<std::pair<uint64_t, uint64_t>> segs;   // (start, len), ascending start
     for (uint32_t j = 0; j < nbig; ++j)
         if (h[2 * j + 1] > h[2 * j]) segs.push_back({h[2 * j], (uint64_t)h[2 * j + 1] - h[2 * j]});
@@ -1333,8 +1337,12 @@ static pm4g_status format_log(const FmtArgs<P>& fa0, cudaStream_t s) {
     Scratch st(s);
     PM4G_TRY(format_launch<P>(fa, st, s));
     uint32_t nbig = 0;
+    pm4g_status gs;
+    const bool seg = gseg_suspend(s, &gs);   // (a pageable copy cannot sit in a graph segment)
+    PM4G_TRY(gs);
     PM4G_CK(cudaMemcpyAsync(&nbig, fa.big_count, 4, cudaMemcpyDeviceToHost, s));
     PM4G_CK(cudaStreamSynchronize(s));
+    if (seg) PM4G_TRY(gseg_resume());
     return nbig ? format_fallback<P>(fa, nbig, s) : PM4G_OK;
 }
 

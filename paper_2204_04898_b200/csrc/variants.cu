@@ -1800,8 +1800,12 @@ static pm4g_status order_medium(Groups& g, pm4g_variant_table* v, const uint32_t
     count_launch();
     if (trace) {
         unsigned long long h[64];
+        pm4g_status gs;
+        const bool seg = gseg_suspend(s, &gs);
+        PM4G_TRY(gs);
         PM4G_CK(cudaMemcpyAsync(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost, s));
         PM4G_CK(cudaStreamSynchronize(s));
+        if (seg) PM4G_TRY(gseg_resume());
         fprintf(stderr, "k_vorder G=%llu Ga=%llu nc=%llu chunk=%u phases(us):", (unsigned long long)g.G, (unsigned long long)Ga, (unsigned long long)nc, a.chunk);
         for (unsigned i = 1; i < h[63] && i < 63; ++i) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1e3);
         fprintf(stderr, "\n");
