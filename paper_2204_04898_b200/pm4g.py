@@ -147,9 +147,10 @@ def _check(st: int):
 
 
 def _ptr(t):
+    # a plain int: ctypes converts it for c_void_p arguments and fields
     if t is None:
         return None
-    return ctypes.c_void_p(t.data_ptr()) if t.numel() else None
+    return t.data_ptr() if t.numel() else None
 
 
 def _stream(stream):
