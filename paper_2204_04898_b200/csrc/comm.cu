@@ -6,10 +6,10 @@
 //   C1  one ncclAllReduce(sum, uint64) of the packed [cnt | sum | start | end]
 //       table: integer sums are exact in any order (two's complement wraps
 //       identically), so the result is independent of the rank count.
-//   C2  ncclAllGather of (V_r, T_r), then padded all-gathers of the per-rank
-//       variant entries and representative sequences, merged on every rank
-//       with the same exact hash-and-verify engine used locally
-//       (merge_variant_tables).
+//   C2  ncclAllGather of (V_r, T_r), then grouped ncclSend / ncclRecv of every
+//       rank's variant entries and representative sequences straight into the
+//       flat merge input (rank order), merged on every rank with the same
+//       exact hash-and-verify grouping used locally.
 // NCCL is loaded with dlopen on first use so that libpm4g itself has no hard
 // link-time dependency on it; torch.distributed only carries the unique id.
 #include <cuda_runtime.h>
