@@ -549,6 +549,7 @@ pm4g_status pm4g_tables_finalize(const uint64_t* packed, uint32_t A, uint64_t* c
 
 pm4g_status pm4g_dfg(const pm4g_log* L, uint64_t* cnt, int64_t* dur_sum, double* mean,
                      pm4g_comm* comm, pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_dfg");
     PM4G_TRY(require_sorted(L));
     if (!cnt || !dur_sum) return fail(PM4G_EINVAL, "cnt and dur_sum are required");
     cudaStream_t s = (cudaStream_t)stream;
@@ -568,6 +569,7 @@ pm4g_status pm4g_case_capacity(const pm4g_log* L, uint64_t* capacity) {
 
 pm4g_status pm4g_dfg_minmax(const pm4g_log* L, uint64_t* dur_min, uint64_t* dur_max, pm4g_comm* comm,
                             pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_dfg_minmax");
     PM4G_TRY(require_sorted(L));
     if (!dur_min && !dur_max) return fail(PM4G_EINVAL, "dur_min or dur_max is required");
     PM4G_TRY(check_table_size(L));
@@ -592,6 +594,7 @@ pm4g_status pm4g_dfg_minmax(const pm4g_log* L, uint64_t* dur_min, uint64_t* dur_
 
 pm4g_status pm4g_start_end(const pm4g_log* L, uint64_t* start, uint64_t* end, pm4g_comm* comm,
                            pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_start_end");
     PM4G_TRY(require_sorted(L));
     if (!start || !end) return fail(PM4G_EINVAL, "start and end are required");
     cudaStream_t s = (cudaStream_t)stream;
@@ -606,6 +609,7 @@ pm4g_status pm4g_start_end(const pm4g_log* L, uint64_t* start, uint64_t* end, pm
 pm4g_status pm4g_case_durations(const pm4g_log* L, uint32_t* case_code, uint32_t* n_events,
                                 int64_t* dur, uint64_t capacity, uint64_t* n_cases_out,
                                 pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_case_durations");
     PM4G_TRY(require_sorted(L));
     cudaStream_t s = (cudaStream_t)stream;
     PM4G_TRY(fetch_n_cases(L, s));
@@ -626,6 +630,7 @@ pm4g_status pm4g_case_durations(const pm4g_log* L, uint32_t* case_code, uint32_t
 
 pm4g_status pm4g_variants(const pm4g_log* L, pm4g_comm* comm, pm4g_stream_t stream,
                           pm4g_variant_table** out) {
+    PM4G_NVTX("pm4g_variants");
     PM4G_TRY(require_sorted(L));
     if (!out) return fail(PM4G_EINVAL, "null out");
     *out = nullptr;
@@ -650,6 +655,7 @@ pm4g_status pm4g_variants(const pm4g_log* L, pm4g_comm* comm, pm4g_stream_t stre
 
 pm4g_status pm4g_analyze(const pm4g_log* L, const pm4g_outputs* out, pm4g_comm* comm,
                          pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_analyze");
     PM4G_TRY(require_sorted(L));
     if (!out) return fail(PM4G_EINVAL, "null outputs");
     cudaStream_t s = (cudaStream_t)stream;

@@ -582,11 +582,13 @@ pm4g_status pm4g_prof_record(int32_t i, const char** name, double* start_ms, dou
 static pm4g_status log_create_impl(const pm4g_log_desc* d, cudaStream_t s, pm4g_log** out, const int64_t* tfilt);
 
 pm4g_status pm4g_log_create(const pm4g_log_desc* d, pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_log_create");
     return log_create_impl(d, (cudaStream_t)stream, out, nullptr);
 }
 
 pm4g_status pm4g_log_create_filtered(const pm4g_log_desc* d, int64_t t1, int64_t t2, pm4g_stream_t stream,
                                      pm4g_log** out) {
+    PM4G_NVTX("pm4g_log_create_filtered");
     if (!d || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
     if (t1 > t2) return fail(PM4G_EINVAL, "t1 > t2 (S:414)");
@@ -893,12 +895,14 @@ static pm4g_status sort_impl(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
 }
 
 pm4g_status pm4g_sort(pm4g_log* L, pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_sort");
     PM4G_TRY(check_log(L));
     if (L->sorted) return PM4G_OK;
     return sort_impl(L, (cudaStream_t)stream, nullptr);
 }
 
 pm4g_status pm4g_sort_analyze(pm4g_log* L, const pm4g_outputs* out, pm4g_comm* comm, pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_sort_analyze");
     PM4G_TRY(check_log(L));
     if (!out) return fail(PM4G_EINVAL, "null outputs");
     if (L->sorted) return pm4g_analyze(L, out, comm, stream);

@@ -266,6 +266,7 @@ pm4g_status pm4g_comm_destroy(pm4g_comm* c) {
 
 pm4g_status pm4g_repartition(const pm4g_log* in, const uint32_t* bounds, pm4g_comm* c, pm4g_stream_t stream,
                              pm4g_log** out) {
+    PM4G_NVTX("pm4g_repartition");
     if (!in || !bounds || !c || !out) return fail(PM4G_EINVAL, "bad arguments");
     *out = nullptr;
     cudaStream_t s = (cudaStream_t)stream;

@@ -244,6 +244,7 @@ extern "C" {
 
 pm4g_status pm4g_efg(const pm4g_log* L, uint64_t* cnt, uint64_t* dur_sum, uint64_t* dur_sumsq, double* mean,
                      double* stdev, pm4g_comm* comm, pm4g_stream_t stream) {
+    PM4G_NVTX("pm4g_efg");
     PM4G_TRY(check_log(L));
     if (!L->sorted) return fail(PM4G_EINVAL, "log is not sorted (call pm4g_sort first)");
     if (!cnt && !dur_sum && !dur_sumsq && !mean && !stdev) return fail(PM4G_EINVAL, "no output requested");

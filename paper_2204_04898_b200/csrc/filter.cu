@@ -844,6 +844,7 @@ extern "C" {
 
 pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t mode,
                              pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_filter_time");
     if (!in || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
     PM4G_TRY(check_log(in));
@@ -879,6 +880,7 @@ pm4g_status pm4g_filter_time(const pm4g_log* in, int64_t t1, int64_t t2, int32_t
 
 pm4g_status pm4g_filter_cases(const pm4g_log* in, const pm4g_case_pred* pred, int32_t keep,
                               pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_filter_cases");
     if (!in || !pred || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
     PM4G_TRY(check_log(in));
@@ -932,6 +934,7 @@ pm4g_status pm4g_filter_cases(const pm4g_log* in, const pm4g_case_pred* pred, in
 
 pm4g_status pm4g_filter_variants(const pm4g_log* in, const uint64_t* seq_off, const uint32_t* seq_act,
                                  int64_t n_seqs, int32_t keep, pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_filter_variants");
     if (!in || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
     PM4G_TRY(check_log(in));
@@ -1016,6 +1019,7 @@ pm4g_status pm4g_filter_variants(const pm4g_log* in, const uint64_t* seq_off, co
 
 pm4g_status pm4g_filter_attr(const pm4g_log* in, int32_t column, const pm4g_pred* pred,
                              int32_t level, int32_t keep, pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_filter_attr");
     if (!in || !pred || !out) return fail(PM4G_EINVAL, "null argument");
     *out = nullptr;
     PM4G_TRY(check_log(in));

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <functional>
@@ -49,6 +50,14 @@ void prof_begin(const char* name, double bytes, cudaStream_t s);
 void prof_end(cudaStream_t s);
 void prof_add_bytes(const char* name, double bytes);
 void count_launch();
+
+// NVTX range around a C-ABI entry point (visible in nsys / ncu timelines; a
+// push / pop costs tens of nanoseconds when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define PM4G_NVTX(name) ::pm4g::NvtxRange _pm4g_nvtx_range(name)
 
 #define PM4G_LAUNCH(name, bytes, stream, ...)                                  \
     do {                                                                       \

@@ -180,6 +180,7 @@ extern "C" {
 
 pm4g_status pm4g_partition_by_case(const pm4g_log* in, const uint32_t* bounds, int32_t n_parts,
                                    pm4g_stream_t stream, pm4g_log** parts) {
+    PM4G_NVTX("pm4g_partition_by_case");
     if (!in || !bounds || !parts || n_parts < 1) return fail(PM4G_EINVAL, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
     for (int r = 0; r < n_parts; ++r) parts[r] = nullptr;
@@ -209,6 +210,7 @@ pm4g_status pm4g_partition_by_case(const pm4g_log* in, const uint32_t* bounds, i
 
 pm4g_status pm4g_log_concat(const pm4g_log* const* logs, int32_t n_logs, uint32_t case_lo, uint32_t case_hi,
                             pm4g_stream_t stream, pm4g_log** out) {
+    PM4G_NVTX("pm4g_log_concat");
     if (!logs || n_logs < 1 || !out) return fail(PM4G_EINVAL, "bad arguments");
     *out = nullptr;
     cudaStream_t s = (cudaStream_t)stream;

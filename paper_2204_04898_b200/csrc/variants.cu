@@ -2093,6 +2093,7 @@ pm4g_status pm4g_variants_destroy(pm4g_variant_table* v) {
 
 pm4g_status pm4g_variants_merge(const pm4g_variant_table* const* parts, int32_t n_parts, int32_t local_part,
                                 pm4g_stream_t stream, pm4g_variant_table** out) {
+    PM4G_NVTX("pm4g_variants_merge");
     if (!parts || n_parts <= 0 || !out || local_part >= n_parts) return fail(PM4G_EINVAL, "bad arguments");
     for (int i = 0; i < n_parts; ++i)
         if (!parts[i]) return fail(PM4G_EINVAL, "null part");
