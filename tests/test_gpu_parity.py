@@ -536,3 +536,15 @@ def test_wide_activity_codes_with_dense_table(dtype, A):
     assert np.array_equal(o["dur_max"].cpu().numpy().view(np.uint64), rmx.reshape(-1).astype(np.uint64))
     o["variants"].close()
     log.close()
+
+
+def test_fallback_rows_written_before_the_deferred_fallback():
+    """Every formatted row holds a valid activity code before the deferred exact
+    fallback runs (the analysis reads the provisional order first): the formatted
+    column is poisoned before k_format and checked after it (PM4G_DEBUG_POISON_FORMAT)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "poison_run.py")],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert "poison_run ok" in r.stdout, (r.stdout + r.stderr)[-4000:]
