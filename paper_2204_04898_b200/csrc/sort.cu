@@ -886,7 +886,6 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
     uint32_t* s_c = s_idx + FMT_BUF;                                                      // WIDE: case of each row
     __shared__ uint32_t s_tile, s_wt[FMT_THREADS / 32], s_scan[FMT_THREADS / 32 + 1];
     __shared__ uint32_t s_prefix, s_nbig, s_bigh[16], s_ntie, s_anywide;
-    __shared__ int s_utail;   // first row of an unowned last case (tn: none)
     __shared__ uint16_t s_tie[FMT_TIES];   // slots starting a group of equal keys
     __shared__ int s_ext, s_wlast[FMT_THREADS / 32];
     __shared__ __align__(8) uint64_t s_bar;
@@ -1148,11 +1147,7 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         };
         for (int q = h0 + wt; q < oend; q += NW) {
             const uint32_t p = s_perm[q];
-            if (p == 0xffff) continue;   // an empty slot after a tie
-            if (p == 0xfffe) {           // a fallback case's row keeps its grouped (ingest) order for now
-                put(q, q);
-                continue;
-            }
+            if (p >= 0xfffe) continue;   // a fallback case's row, or an empty slot after a tie
             if (q + 1 < oend && s_perm[q + 1] == 0xffff) {
                 const uint32_t t = atomicAdd(&s_ntie, 1u);
                 if (t < FMT_TIES) s_tie[t] = (uint16_t)q;
@@ -1163,29 +1158,8 @@ __global__ __launch_bounds__(FMT_THREADS) void k_format(FmtArgs<P> a) {
         }
         wsync();
         for (uint32_t t = wt; t < min(s_ntie, (uint32_t)FMT_TIES); t += NW) ties(s_tie[t]);
-        if (wt == 0) s_utail = Hown == (int)H ? tn : (int)s_head[H - 1];
     }
     __syncthreads();
-
-    // ---- 5b. rows of exact-fallback cases that no tile ranks keep their grouped
-    // (ingest) order until the fallback sorts them, so the provisional order holds
-    // valid codes (the analysis runs before the fallback): the rows after this
-    // tile's last head when that case runs far past the tile, and a prefix longer
-    // than the previous tile's extension could own (the earlier tile's case ran
-    // more than FMT_EXT rows into this one)
-    {
-        const int pre = H > 0 ? (int)s_head[0] : tn;
-        const int ut = H > 0 ? s_utail : tn;
-        for (int r = tid; r < tn; r += FMT_THREADS) {
-            if ((pre > FMT_EXT && r < pre) || r >= ut) {
-                const int64_t g = base + r;
-                a.key_out[g] = s_key[r];
-                a.act_out[g] = s_act[r];
-                if (WI && a.perm_out) a.perm_out[g] = s_idx[r];
-                if (WIDE) a.rcase_out[g] = s_c[r];
-            }
-        }
-    }
 
     // ---- 6. case offsets and codes (ranks known now)
     const uint32_t R0 = s_prefix;
@@ -1256,6 +1230,25 @@ __global__ void k_big_gather(FmtArgs<P> a, const uint64_t* __restrict__ seg_star
     }
 }
 
+// Rows of the cases k_format listed for the exact fallback are not written by
+// k_format.  Before the (deferred) fallback runs, the provisional order must
+// still hold valid codes for every row: copy those cases' grouped rows through
+// unchanged (same case, ingest order), so anything derived from the provisional
+// order stays in bounds; the fallback then overwrites them with the exact order.
+template <class P>
+__global__ void k_big_identity(const uint32_t* __restrict__ big, const uint32_t* __restrict__ big_count,
+                               const uint32_t* __restrict__ off, const uint64_t* __restrict__ gkey,
+                               const P* __restrict__ gact, uint64_t* __restrict__ key_out, P* __restrict__ act_out) {
+    const uint32_t nb = *big_count;
+    for (uint32_t e = blockIdx.x; e < nb; e += gridDim.x) {
+        const uint32_t r = big[e];
+        const uint32_t a = off[r], b = off[r + 1];
+        for (uint32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+            key_out[i] = gkey[i];
+            act_out[i] = gact[i];
+        }
+    }
+}
 
 // launch k_format; st holds its scratch (tile status, fallback list + count)
 template <class P>
@@ -1410,11 +1403,16 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
     // deferred: no host wait here; the caller runs sort_finish at its next
     // synchronisation (the grouped keys stay alive for the fallback)
     d->st.s = s;
-    // test hook: every formatted row must be written by k_format, fallback rows
-    // included (the analysis reads the provisional order before the fallback)
+    // test hook: every formatted row must hold a valid code before the deferred
+    // fallback (the analysis reads the provisional order first)
     static const bool poison = getenv("PM4G_DEBUG_POISON_FORMAT") != nullptr;
     if (poison && n) PM4G_CK(cudaMemsetAsync(fa.act_out, 0xff, (size_t)n * sizeof(P), s));
     PM4G_TRY(format_launch<P>(fa, d->st, s));
+    // fallback cases hold their grouped rows until the fallback runs (no stale bytes);
+    // writing them inside k_format instead cost that kernel 2% at 100M
+    PM4G_LAUNCH("k_big_identity", 0, s,
+                (k_big_identity<P><<<num_sms(), 256, 0, s>>>(fa.big, fa.big_count, fa.off, fa.gkey, fa.gact,
+                                                              fa.key_out, fa.act_out)));
     if (poison && n) {
         Scratch fl(s);
         PM4G_TRY(fl.alloc(16));
@@ -1426,8 +1424,6 @@ static pm4g_status sort_log_t(pm4g_log* L, cudaStream_t s, FmtDeferred* d) {
         PM4G_CK(cudaStreamSynchronize(s));
         if (bad) return fail(PM4G_ECUDA, "formatted rows left unwritten before the deferred fallback");
     }
-    // (fallback cases hold their grouped rows until the fallback runs: k_format
-    // writes them, phase 5b)
     // the fallback count goes to pinned host memory now (stream order); the
     // caller's own synchronisation later makes it readable without a wait.
     // Events belong to the device current at creation: one per device.
